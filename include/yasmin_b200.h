@@ -1,0 +1,200 @@
+/*
+ * yasmin-b200 — C-ABI of the B200-native yasmin core.
+ *
+ * This is the drop-in boundary for the reference solver ("aspine") program
+ * loading / solve / enumerate path. Every entry point names the reference
+ * interface it replaces (paths under /root/reference/proj). Plain C types
+ * only; no torch or CUDA types cross this boundary. All functions are
+ * synchronous and re-entrant (no globals), like aspine::solve.
+ *
+ * Errors: functions return a yas_status; on failure a message is written to
+ * the caller's (err, err_cap) buffer when given. The reference's exception
+ * classes map to status codes:
+ *   ParseError (program.hpp:79-83)          -> YAS_ERR_PARSE (+ line number)
+ *   StoreCapacityError (nogood_store.hpp:47)-> YAS_ERR_CAPACITY
+ *   VerificationError (solver.hpp:109-111)  -> YAS_ERR_VERIFY
+ *   std::logic_error (learn.cpp:97-100, solver.cpp:77-82) -> YAS_ERR_LOGIC
+ */
+#ifndef YASMIN_B200_H
+#define YASMIN_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum yas_status {
+    YAS_OK = 0,
+    YAS_ERR_PARSE = 1,
+    YAS_ERR_CAPACITY = 2,
+    YAS_ERR_VERIFY = 3,
+    YAS_ERR_LOGIC = 4,
+    YAS_ERR_DEVICE = 5, /* CUDA error / no device: the product has no CPU fallback */
+    YAS_ERR_ARG = 6,
+    YAS_ERR_IO = 7
+} yas_status;
+
+typedef struct yas_program yas_program;       /* aspine::GroundProgram */
+typedef struct yas_result yas_result;         /* aspine::SolveResult */
+typedef struct yas_store yas_store;           /* aspine::NogoodStore (static partition) */
+typedef struct yas_propagator yas_propagator; /* aspine::Propagator + Assignment + Frontier */
+
+/* ---- library ------------------------------------------------------------ */
+const char* yas_version(void);
+/* Number of CUDA devices visible (0 when none). */
+int yas_device_count(void);
+/* Device name into buf; returns YAS_ERR_DEVICE when unavailable. */
+int yas_device_name(int device, char* buf, size_t cap);
+
+/* ---- program loading: parse_program (program.hpp:87-88, program.cpp:141-179) */
+int yas_program_parse(const char* text, size_t len, yas_program** out, int* err_line, char* err, size_t err_cap);
+int yas_program_parse_file(const char* path, yas_program** out, int* err_line, char* err, size_t err_cap);
+void yas_program_free(yas_program* p);
+uint32_t yas_program_atom_count(const yas_program* p);       /* GroundProgram::atom_count */
+uint32_t yas_program_rule_count(const yas_program* p);       /* rules().size() */
+uint32_t yas_program_constraint_count(const yas_program* p); /* constraints().size() */
+/* Atom name (GroundProgram::name), NUL-terminated, valid while p lives. */
+const char* yas_program_atom_name(const yas_program* p, uint32_t id);
+uint32_t yas_program_find(const yas_program* p, const char* name); /* GroundProgram::find */
+/* Rule r: head, |pos|, |neg| and the bodies (program.hpp:41-49). */
+int yas_program_rule(const yas_program* p, uint32_t r, uint32_t* head, const uint32_t** pos, uint32_t* n_pos,
+                     const uint32_t** neg, uint32_t* n_neg);
+/* Text outputs: return the full length; copy at most cap-1 bytes + NUL. */
+size_t yas_program_print(const yas_program* p, char* buf, size_t cap);         /* print_program */
+size_t yas_program_dump_nogoods(const yas_program* p, char* buf, size_t cap);  /* dump_nogoods */
+size_t yas_program_store_csv(const yas_program* p, char* buf, size_t cap);     /* NogoodStore::dump_csv */
+size_t yas_program_diagnostics(const yas_program* p, char* buf, size_t cap);   /* validate, '\n'-joined */
+/* Completion ids (completion.hpp:48-80): out = {b, t, n, vacuous}. */
+int yas_program_rule_aux(const yas_program* p, uint32_t rule, uint32_t out[4]);
+uint32_t yas_program_total_atoms(const yas_program* p); /* AuxMap::total_atoms */
+/* nogood_census vs compiled counts: census[3], counts[3] = rule, atom, constraint. */
+int yas_program_census(const yas_program* p, uint64_t census[3], uint64_t counts[3]);
+/* tp_step (program.hpp:96): interp sorted; out gets up to cap ids; returns count. */
+size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap);
+/* verify_model (solver.hpp:116): 1 when the sorted atom set is an answer set. */
+int yas_verify_model(const yas_program* p, const uint32_t* atom_ids, size_t n);
+
+/* ---- solve / enumerate: solve(GroundProgram, SolverConfig) (solver.hpp:113) */
+typedef struct yas_trace {
+    int mode; /* 0 fwd, 1 res */
+    int32_t conflict_id;
+    uint64_t learned_length;
+    uint32_t backjump_level;
+} yas_trace; /* ConflictTrace, solver.hpp:37-42 */
+typedef void (*yas_trace_fn)(const yas_trace* t, void* user);
+
+typedef struct yas_config {
+    /* SolverConfig (solver.hpp:44-57) */
+    int mode;              /* 0 fwd (default), 1 res */
+    int heuristic;         /* 0 occ (default), 1 jw, 2 act */
+    double activity_decay; /* 0.95 */
+    unsigned workers;      /* accepted for API parity; the device decides parallelism */
+    int restarts_enabled;
+    uint64_t restart_base;  /* 100 */
+    double restart_factor;  /* 1.5 */
+    uint64_t max_models;    /* 1; 0 = enumerate all */
+    uint32_t deps_words;    /* 16 */
+    uint32_t conflict_fanout; /* 1 */
+    uint64_t seed;          /* accepted, unused (as in the reference) */
+    int verify;
+    int debug_validate;
+    uint64_t learned_capacity; /* 1 << 22 */
+    yas_trace_fn trace;
+    void* trace_user;
+    /* device extensions */
+    int device;          /* CUDA ordinal */
+    int engine;          /* 0 auto, 1 one CTA per search, 2 whole-grid search */
+    uint32_t cube_atoms; /* enumeration split over the first k choice atoms (0 = single search) */
+    uint32_t slots;      /* concurrent searches per GPU for cubes (0 = auto) */
+    int rank, world;     /* cube partition across processes/GPUs: cube i runs on rank i % world */
+} yas_config;
+
+void yas_config_default(yas_config* cfg);
+
+typedef struct yas_stats {
+    /* SolveStats (solver.hpp:59-93) */
+    uint64_t decisions, propagations, conflicts, learned_count, learned_length_sum, restarts, models;
+    double wall_ms;
+    uint64_t passes, watch_replacements, duplicate_learned, blocking_nogoods, res_learned, fwd_learned,
+        fwd_fallbacks, uip_check_failures, fwd_decision_only_failures, asserting_failures;
+    /* device extensions */
+    uint64_t checks;   /* nogood checks (deduplicated propagation items) */
+    uint64_t searches; /* searches run (cubes) */
+    uint64_t launches; /* kernel launches */
+    double device_ms;  /* kernel time, CUDA events */
+    uint64_t cubes;    /* cubes assigned to this rank */
+} yas_stats;
+
+int yas_solve(const yas_program* p, const yas_config* cfg, yas_result** out, char* err, size_t err_cap);
+int yas_result_status(const yas_result* r); /* SolveStatus: 0 sat, 1 unsat */
+uint64_t yas_result_model_count(const yas_result* r);
+/* Model m: sorted program atom ids (Model::atom_ids); n receives the size. */
+const uint32_t* yas_result_model(const yas_result* r, uint64_t m, uint32_t* n);
+uint32_t yas_result_model_cube(const yas_result* r, uint64_t m);
+void yas_result_stats(const yas_result* r, yas_stats* s);
+void yas_result_free(yas_result* r);
+/* emit_stats / stats_csv_header (solver.hpp:131-133); ctx strings may be NULL. */
+size_t yas_stats_csv_header(char* buf, size_t cap);
+size_t yas_emit_stats(const yas_stats* s, const char* instance, const char* mode, const char* heur,
+                      unsigned workers, int status, uint64_t models, int csv, char* buf, size_t cap);
+
+/* ---- low level: NogoodStore::build (nogood_store.hpp:64-65) ------------- */
+/* Nogood k = lits[offsets[k] .. offsets[k+1]), canonicalised like Nogood::make
+ * (nogood.hpp:80-87); a vacuous set is YAS_ERR_ARG. guards may be NULL
+ * (kAnyTruth = 0xFFFFFFFF); origins may be NULL (constraint). */
+int yas_store_build(const int32_t* lits, const uint32_t* offsets, size_t n_nogoods, const uint32_t* guards,
+                    const uint8_t* origins, uint32_t total_atoms, yas_store** out, char* err, size_t err_cap);
+void yas_store_free(yas_store* s);
+uint32_t yas_store_size(const yas_store* s);
+uint32_t yas_store_total_atoms(const yas_store* s);
+size_t yas_store_dump_csv(const yas_store* s, char* buf, size_t cap);
+/* static_units (literals), unit_ids, static_class_bounds */
+size_t yas_store_units(const yas_store* s, int32_t* out, size_t cap);
+size_t yas_store_unit_ids(const yas_store* s, int32_t* out, size_t cap);
+void yas_store_bounds(const yas_store* s, uint32_t out[4]);
+/* occurrences(l, class) (nogood_store.hpp:98-100) */
+size_t yas_store_occurrences(const yas_store* s, int32_t lit, uint32_t cls, int32_t* out, size_t cap);
+/* Planted benchmark store: builds the store and
+ * the seeded frontier; decision = H-literal of atom 1. */
+int yas_store_planted(uint32_t atoms, uint64_t nogoods, uint32_t pct, uint64_t seed, yas_store** out,
+                      int32_t** seeded, size_t* n_seeded, int32_t* decision);
+void yas_free_ints(int32_t* p);
+
+/* ---- low level: Propagator (propagate.hpp:54-97) over one device search -- */
+typedef struct yas_outcome {
+    int violated;
+    uint64_t propagations, passes, checks;
+    uint32_t n_conflicts;
+    float device_ms;
+} yas_outcome; /* PropagationOutcome (+ device extras) */
+
+int yas_propagator_create(const yas_store* s, uint32_t deps_words, int engine, int device, yas_propagator** out,
+                          char* err, size_t err_cap);
+void yas_propagator_free(yas_propagator* p);
+int yas_propagator_reset(yas_propagator* p); /* fresh Assignment + Frontier */
+int yas_propagator_initial(yas_propagator* p, yas_outcome* o);                 /* initial_propagation */
+int yas_propagator_propagate(yas_propagator* p, uint32_t level, yas_outcome* o); /* propagate_and_check */
+int yas_propagator_push_decision(yas_propagator* p, int32_t lit);              /* Assignment::push_decision */
+/* Assignment::assign_propagated for each literal (same level/deps/antecedent). */
+int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level,
+                          const uint64_t* deps, uint32_t n_deps, int overflow, int32_t antecedent);
+int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n); /* Frontier::seed / last.push_back */
+int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n); /* NogoodStore::add_learned */
+/* Read back. cells: A+1 entries (cell[p] = +-level). reasons: >= 0 antecedent,
+ * -1 none, -2 decision, -3 unit, -4 completion. deps: word w of every atom. */
+uint32_t yas_propagator_atoms(const yas_propagator* p);
+int yas_propagator_cells(const yas_propagator* p, int32_t* out);
+int yas_propagator_reasons(const yas_propagator* p, int32_t* out);
+int yas_propagator_deps(const yas_propagator* p, uint32_t word, uint64_t* out, uint8_t* overflow);
+size_t yas_propagator_trail(const yas_propagator* p, int32_t* out, size_t cap);
+size_t yas_propagator_conflicts(const yas_propagator* p, int32_t* out, size_t cap);
+size_t yas_propagator_frontier(const yas_propagator* p, int32_t* out, size_t cap);
+uint32_t yas_propagator_level(const yas_propagator* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* YASMIN_B200_H */

@@ -1,0 +1,581 @@
+"""Host-side mirror of the reference solver's public API over the C-ABI.
+
+Names, argument meaning and error behaviour follow the reference ("aspine"):
+
+  parse_program            /root/reference/proj/include/aspine/program.hpp:87-88
+  GroundProgram            program.hpp:51-77           ParseError  program.hpp:79-83
+  SolverConfig             solver.hpp:44-57            solve       solver.hpp:113
+  SolveResult/Model/Stats  solver.hpp:59-107           verify_model solver.hpp:116
+  emit_stats/csv header    solver.hpp:131-133
+  NogoodStore.build        nogood_store.hpp:64-65      Propagator  propagate.hpp:54-97
+  StoreCapacityError       nogood_store.hpp:47         VerificationError solver.hpp:109
+
+Everything computes on the GPU through ``libyasmin_b200.so``; this module only
+marshals arguments.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import Callable, Iterable, List, Optional, Sequence
+
+from . import _native as N
+
+kAnyTruth = 0xFFFFFFFF
+kNoTruth = 0
+
+
+class ParseError(RuntimeError):
+    def __init__(self, line: int, what: str):
+        super().__init__(what)
+        self.line = line
+
+
+class StoreCapacityError(RuntimeError):
+    pass
+
+
+class VerificationError(RuntimeError):
+    pass
+
+
+class LogicError(RuntimeError):
+    """std::logic_error in the reference (res_learning, debug_validate)."""
+
+
+class DeviceError(RuntimeError):
+    """No usable CUDA device / CUDA failure. There is no CPU fallback."""
+
+
+def _raise(code: int, msg: bytes, line: int = 0):
+    text = msg.decode(errors="replace") if msg else f"error {code}"
+    if code == 1:
+        raise ParseError(line, text)
+    exc = {2: StoreCapacityError, 3: VerificationError, 4: LogicError, 5: DeviceError, 7: OSError}.get(code, ValueError)
+    raise exc(text)
+
+
+def _text(fn, *args) -> str:
+    n = fn(*args, None, 0)
+    buf = C.create_string_buffer(n + 1)
+    fn(*args, buf, n + 1)
+    return buf.value.decode()
+
+
+class LearnMode(enum.IntEnum):
+    fwd = 0
+    res = 1
+
+
+class HeuristicKind(enum.IntEnum):
+    occurrence_count = 0
+    jeroslow_wang = 1
+    activity = 2
+
+
+class SolveStatus(enum.IntEnum):
+    sat = 0
+    unsat = 1
+
+
+def to_string(x) -> str:
+    if isinstance(x, LearnMode):
+        return "fwd" if x == LearnMode.fwd else "res"
+    if isinstance(x, HeuristicKind):
+        return {0: "occ", 1: "jw", 2: "act"}[int(x)]
+    if isinstance(x, SolveStatus):
+        return "SAT" if x == SolveStatus.sat else "UNSAT"
+    raise TypeError(x)
+
+
+@dataclass
+class HeuristicConfig:
+    kind: HeuristicKind = HeuristicKind.occurrence_count
+    activity_decay: float = 0.95
+
+
+@dataclass
+class RestartPolicy:
+    enabled: bool = False
+    base: int = 100
+    factor: float = 1.5
+
+
+@dataclass
+class ConflictTrace:
+    mode_used: LearnMode
+    conflict_id: int
+    learned_length: int
+    backjump_level: int
+
+
+@dataclass
+class SolverConfig:
+    mode: LearnMode = LearnMode.fwd
+    heuristic: HeuristicConfig = field(default_factory=HeuristicConfig)
+    workers: int = 1
+    restarts: RestartPolicy = field(default_factory=RestartPolicy)
+    max_models: int = 1
+    deps_words: int = 16
+    conflict_fanout: int = 1
+    seed: int = 0
+    verify: bool = False
+    debug_validate: bool = False
+    learned_capacity: int = 1 << 22
+    trace: Optional[Callable[[ConflictTrace], None]] = None
+    # device extensions
+    device: int = 0
+    engine: str = "auto"  # "auto" | "block" | "grid"
+    cube_atoms: int = 0
+    slots: int = 0
+    rank: int = 0
+    world: int = 1
+
+
+_STAT_FIELDS = ["decisions", "propagations", "conflicts", "learned_count", "learned_length_sum", "restarts",
+                "models", "wall_ms", "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods",
+                "res_learned", "fwd_learned", "fwd_fallbacks", "uip_check_failures",
+                "fwd_decision_only_failures", "asserting_failures", "checks", "searches", "launches",
+                "device_ms", "cubes"]
+
+
+@dataclass
+class SolveStats:
+    decisions: int = 0
+    propagations: int = 0
+    conflicts: int = 0
+    learned_count: int = 0
+    learned_length_sum: int = 0
+    restarts: int = 0
+    models: int = 0
+    wall_ms: float = 0.0
+    passes: int = 0
+    watch_replacements: int = 0
+    duplicate_learned: int = 0
+    blocking_nogoods: int = 0
+    res_learned: int = 0
+    fwd_learned: int = 0
+    fwd_fallbacks: int = 0
+    uip_check_failures: int = 0
+    fwd_decision_only_failures: int = 0
+    asserting_failures: int = 0
+    checks: int = 0
+    searches: int = 0
+    launches: int = 0
+    device_ms: float = 0.0
+    cubes: int = 0
+
+    def avg_learned_len(self) -> float:
+        return 0.0 if self.learned_count == 0 else self.learned_length_sum / self.learned_count
+
+    def wall_seconds(self) -> float:
+        return self.wall_ms / 1000.0
+
+    def per_second(self, counter: int) -> float:
+        return 0.0 if self.wall_ms <= 0.0 else counter / self.wall_seconds()
+
+    def propagations_per_sec(self) -> float:
+        return self.per_second(self.propagations)
+
+    def decisions_per_sec(self) -> float:
+        return self.per_second(self.decisions)
+
+    def learned_per_sec(self) -> float:
+        return self.per_second(self.learned_count)
+
+    def _c(self) -> N.yas_stats:
+        s = N.yas_stats()
+        for f in _STAT_FIELDS:
+            setattr(s, f, getattr(self, f))
+        return s
+
+
+@dataclass
+class Model:
+    atom_ids: List[int]
+    atoms: List[str]
+
+
+@dataclass
+class SolveResult:
+    models: List[Model]
+    stats: SolveStats
+    status: SolveStatus
+    cubes: List[int] = field(default_factory=list)
+
+
+class GroundProgram:
+    """Handle to a parsed program (immutable, shareable read-only)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        self._names: Optional[List[str]] = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().yas_program_free(h)
+            self._h = C.c_void_p(0)
+
+    def atom_count(self) -> int:
+        return N.lib().yas_program_atom_count(self._h)
+
+    def name(self, atom_id: int) -> str:
+        if self._names is None:
+            L = N.lib()
+            self._names = [""] + [L.yas_program_atom_name(self._h, i).decode() for i in range(1, self.atom_count() + 1)]
+        return self._names[atom_id]
+
+    def find(self, name: str) -> int:
+        return N.lib().yas_program_find(self._h, name.encode())
+
+    def rule_count(self) -> int:
+        return N.lib().yas_program_rule_count(self._h)
+
+    def constraint_count(self) -> int:
+        return N.lib().yas_program_constraint_count(self._h)
+
+    def total_atoms(self) -> int:
+        return N.lib().yas_program_total_atoms(self._h)
+
+    def rule_aux(self, rule: int):
+        out = (C.c_uint32 * 4)()
+        if N.lib().yas_program_rule_aux(self._h, rule, out) != 0:
+            raise IndexError(rule)
+        return {"b": out[0], "t": out[1], "n": out[2], "vacuous": bool(out[3])}
+
+    def census(self):
+        a, b = (C.c_uint64 * 3)(), (C.c_uint64 * 3)()
+        N.lib().yas_program_census(self._h, a, b)
+        return tuple(a), tuple(b)
+
+
+def parse_program(text) -> GroundProgram:
+    """parse_program(std::string_view) — raises ParseError(line) on bad input."""
+    if isinstance(text, str):
+        text = text.encode()
+    h = C.c_void_p()
+    line = C.c_int(0)
+    err = C.create_string_buffer(512)
+    rc = N.lib().yas_program_parse(text, len(text), C.byref(h), C.byref(line), err, 512)
+    if rc != 0:
+        _raise(rc, err.value, line.value)
+    return GroundProgram(h.value)
+
+
+def parse_file(path: str) -> GroundProgram:
+    h = C.c_void_p()
+    line = C.c_int(0)
+    err = C.create_string_buffer(512)
+    rc = N.lib().yas_program_parse_file(path.encode(), C.byref(h), C.byref(line), err, 512)
+    if rc != 0:
+        _raise(rc, err.value, line.value)
+    return GroundProgram(h.value)
+
+
+def print_program(prog: GroundProgram) -> str:
+    return _text(N.lib().yas_program_print, prog._h)
+
+
+def dump_nogoods(prog: GroundProgram) -> str:
+    return _text(N.lib().yas_program_dump_nogoods, prog._h)
+
+
+def store_csv(prog: GroundProgram) -> str:
+    return _text(N.lib().yas_program_store_csv, prog._h)
+
+
+def validate(prog: GroundProgram) -> List[str]:
+    t = _text(N.lib().yas_program_diagnostics, prog._h)
+    return [x for x in t.split("\n") if x]
+
+
+def tp_step(prog: GroundProgram, interp: Sequence[int]) -> List[int]:
+    arr = (C.c_uint32 * max(1, len(interp)))(*interp)
+    cap = prog.atom_count() + 1
+    out = (C.c_uint32 * cap)()
+    n = N.lib().yas_program_tp_step(prog._h, arr, len(interp), out, cap)
+    return list(out[:n])
+
+
+def verify_model(prog: GroundProgram, model: Model) -> bool:
+    ids = (C.c_uint32 * max(1, len(model.atom_ids)))(*model.atom_ids)
+    return N.lib().yas_verify_model(prog._h, ids, len(model.atom_ids)) == 1
+
+
+def _config(cfg: SolverConfig) -> N.yas_config:
+    c = N.yas_config()
+    N.lib().yas_config_default(C.byref(c))
+    c.mode = int(cfg.mode)
+    c.heuristic = int(cfg.heuristic.kind)
+    c.activity_decay = cfg.heuristic.activity_decay
+    c.workers = cfg.workers
+    c.restarts_enabled = 1 if cfg.restarts.enabled else 0
+    c.restart_base = cfg.restarts.base
+    c.restart_factor = cfg.restarts.factor
+    c.max_models = cfg.max_models
+    c.deps_words = cfg.deps_words
+    c.conflict_fanout = cfg.conflict_fanout
+    c.seed = cfg.seed
+    c.verify = 1 if cfg.verify else 0
+    c.debug_validate = 1 if cfg.debug_validate else 0
+    c.learned_capacity = cfg.learned_capacity
+    c.device = cfg.device
+    c.engine = {"auto": 0, "block": 1, "grid": 2}[cfg.engine]
+    c.cube_atoms = cfg.cube_atoms
+    c.slots = cfg.slots
+    c.rank = cfg.rank
+    c.world = cfg.world
+    return c
+
+
+def solve(prog: GroundProgram, cfg: Optional[SolverConfig] = None) -> SolveResult:
+    """solve(GroundProgram, SolverConfig) — max_models = 0 enumerates all."""
+    cfg = cfg or SolverConfig()
+    c = _config(cfg)
+    keep = None
+    if cfg.trace is not None:
+        user = cfg.trace
+
+        def _cb(tp, _user):
+            t = tp.contents
+            user(ConflictTrace(LearnMode(t.mode), t.conflict_id, t.learned_length, t.backjump_level))
+
+        keep = N.TRACE_FN(_cb)
+        c.trace = keep
+    L = N.lib()
+    h = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    rc = L.yas_solve(prog._h, C.byref(c), C.byref(h), err, 1024)
+    del keep
+    if rc != 0:
+        _raise(rc, err.value)
+    try:
+        st = N.yas_stats()
+        L.yas_result_stats(h, C.byref(st))
+        stats = SolveStats(**{f: getattr(st, f) for f in _STAT_FIELDS})
+        models, cubes = [], []
+        n = C.c_uint32(0)
+        for m in range(L.yas_result_model_count(h)):
+            p = L.yas_result_model(h, m, C.byref(n))
+            ids = list(p[: n.value]) if n.value else []
+            models.append(Model(ids, sorted(prog.name(a) for a in ids)))
+            cubes.append(L.yas_result_model_cube(h, m))
+        status = SolveStatus(L.yas_result_status(h))
+    finally:
+        L.yas_result_free(h)
+    return SolveResult(models, stats, status, cubes)
+
+
+def stats_csv_header() -> str:
+    return _text(N.lib().yas_stats_csv_header)
+
+
+@dataclass
+class StatsContext:
+    instance: str = ""
+    mode: str = ""
+    heuristic: str = ""
+    workers: int = 1
+    status: SolveStatus = SolveStatus.unsat
+    models: int = 0
+
+
+def emit_stats(stats: SolveStats, ctx: StatsContext, csv: bool) -> str:
+    s = stats._c()
+    L = N.lib()
+    args = (C.byref(s), ctx.instance.encode(), ctx.mode.encode(), ctx.heuristic.encode(), ctx.workers,
+            int(ctx.status), ctx.models, 1 if csv else 0)
+    n = L.yas_emit_stats(*args, None, 0)
+    buf = C.create_string_buffer(n + 1)
+    L.yas_emit_stats(*args, buf, n + 1)
+    return buf.value.decode()
+
+
+# ---------------------------------------------------------------------------
+# low level: store + propagator
+# ---------------------------------------------------------------------------
+def _ints(xs: Sequence[int]):
+    return (C.c_int32 * max(1, len(xs)))(*xs)
+
+
+class NogoodStore:
+    """Static partition of the nogood store (NogoodStore::build)."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().yas_store_free(h)
+            self._h = C.c_void_p(0)
+
+    @staticmethod
+    def build(nogoods: Iterable[Sequence[int]], total_atoms: int, guards: Optional[Sequence[int]] = None,
+              origins: Optional[Sequence[int]] = None) -> "NogoodStore":
+        lits, offs = [], [0]
+        for ng in nogoods:
+            lits.extend(ng)
+            offs.append(len(lits))
+        n = len(offs) - 1
+        h = C.c_void_p()
+        err = C.create_string_buffer(256)
+        g = (C.c_uint32 * max(1, n))(*guards) if guards is not None else None
+        o = (C.c_uint8 * max(1, n))(*origins) if origins is not None else None
+        rc = N.lib().yas_store_build(_ints(lits), (C.c_uint32 * len(offs))(*offs), n, g, o, total_atoms,
+                                     C.byref(h), err, 256)
+        if rc != 0:
+            _raise(rc, err.value)
+        return NogoodStore(h.value)
+
+    @staticmethod
+    def planted(atoms: int, nogoods: int, pct: int, seed: int = 0x1B00B5):
+        """Config 4b store + seeded frontier."""
+        h = C.c_void_p()
+        p = C.POINTER(C.c_int32)()
+        n = C.c_size_t(0)
+        d = C.c_int32(0)
+        rc = N.lib().yas_store_planted(atoms, nogoods, pct, seed, C.byref(h), C.byref(p), C.byref(n), C.byref(d))
+        if rc != 0:
+            _raise(rc, b"planted store")
+        seeded = list(p[: n.value])
+        N.lib().yas_free_ints(p)
+        return NogoodStore(h.value), seeded, d.value
+
+    def size(self) -> int:
+        return N.lib().yas_store_size(self._h)
+
+    def total_atoms(self) -> int:
+        return N.lib().yas_store_total_atoms(self._h)
+
+    def dump_csv(self) -> str:
+        return _text(N.lib().yas_store_dump_csv, self._h)
+
+    def static_units(self) -> List[int]:
+        n = N.lib().yas_store_units(self._h, None, 0)
+        out = (C.c_int32 * max(1, n))()
+        N.lib().yas_store_units(self._h, out, n)
+        return list(out[:n])
+
+    def unit_ids(self) -> List[int]:
+        n = N.lib().yas_store_unit_ids(self._h, None, 0)
+        out = (C.c_int32 * max(1, n))()
+        N.lib().yas_store_unit_ids(self._h, out, n)
+        return list(out[:n])
+
+    def static_class_bounds(self) -> List[int]:
+        out = (C.c_uint32 * 4)()
+        N.lib().yas_store_bounds(self._h, out)
+        return list(out)
+
+    def occurrences(self, lit: int, cls: int) -> List[int]:
+        n = N.lib().yas_store_occurrences(self._h, lit, cls, None, 0)
+        out = (C.c_int32 * max(1, n))()
+        N.lib().yas_store_occurrences(self._h, lit, cls, out, n)
+        return list(out[:n])
+
+
+@dataclass
+class PropagationOutcome:
+    violated: bool
+    conflicts: List[int]
+    propagations: int
+    passes: int
+    checks: int
+    device_ms: float
+
+
+REASON_NONE, REASON_DECISION, REASON_UNIT, REASON_COMPLETION = -1, -2, -3, -4
+
+
+class Propagator:
+    """Propagator + Assignment + Frontier of one device search."""
+
+    def __init__(self, store: NogoodStore, deps_words: int = 16, engine: str = "auto", device: int = 0):
+        self.store = store
+        self.deps_words = deps_words
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = N.lib().yas_propagator_create(store._h, deps_words, {"auto": 0, "block": 1, "grid": 2}[engine], device,
+                                           C.byref(h), err, 512)
+        if rc != 0:
+            _raise(rc, err.value)
+        self._h = h
+        self.atoms = N.lib().yas_propagator_atoms(h)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            N.lib().yas_propagator_free(h)
+            self._h = C.c_void_p(0)
+
+    def _outcome(self, o: N.yas_outcome) -> PropagationOutcome:
+        return PropagationOutcome(bool(o.violated), self.conflicts(), o.propagations, o.passes, o.checks, o.device_ms)
+
+    def reset(self):
+        N.lib().yas_propagator_reset(self._h)
+
+    def initial_propagation(self) -> PropagationOutcome:
+        o = N.yas_outcome()
+        N.lib().yas_propagator_initial(self._h, C.byref(o))
+        return self._outcome(o)
+
+    def propagate_and_check(self, level: int) -> PropagationOutcome:
+        o = N.yas_outcome()
+        N.lib().yas_propagator_propagate(self._h, level, C.byref(o))
+        return self._outcome(o)
+
+    def push_decision(self, lit: int):
+        N.lib().yas_propagator_push_decision(self._h, lit)
+
+    def assign_propagated(self, lits: Sequence[int], level: int, deps: Sequence[int] = (), overflow: bool = False,
+                          antecedent: int = 0):
+        d = (C.c_uint64 * max(1, len(deps)))(*deps)
+        N.lib().yas_propagator_assign(self._h, _ints(lits), len(lits), level, d, len(deps), 1 if overflow else 0,
+                                      antecedent)
+
+    def seed(self, lits: Sequence[int]):
+        N.lib().yas_propagator_seed(self._h, _ints(lits), len(lits))
+
+    def add_learned(self, lits: Sequence[int]) -> int:
+        return N.lib().yas_propagator_add_learned(self._h, _ints(lits), len(lits))
+
+    def level(self) -> int:
+        return N.lib().yas_propagator_level(self._h)
+
+    def cells(self) -> List[int]:
+        out = (C.c_int32 * (self.atoms + 1))()
+        N.lib().yas_propagator_cells(self._h, out)
+        return list(out)
+
+    def reasons(self) -> List[int]:
+        out = (C.c_int32 * (self.atoms + 1))()
+        N.lib().yas_propagator_reasons(self._h, out)
+        return list(out)
+
+    def deps(self, word: int = 0):
+        out = (C.c_uint64 * (self.atoms + 1))()
+        ovf = (C.c_uint8 * (self.atoms + 1))()
+        N.lib().yas_propagator_deps(self._h, word, out, ovf)
+        return list(out), list(ovf)
+
+    def _list(self, fn) -> List[int]:
+        n = fn(self._h, None, 0)
+        out = (C.c_int32 * max(1, n))()
+        fn(self._h, out, n)
+        return list(out[:n])
+
+    def trail(self) -> List[int]:
+        return self._list(N.lib().yas_propagator_trail)
+
+    def conflicts(self) -> List[int]:
+        return self._list(N.lib().yas_propagator_conflicts)
+
+    def frontier(self) -> List[int]:
+        return self._list(N.lib().yas_propagator_frontier)
+
+
+def device_count() -> int:
+    return N.lib().yas_device_count()

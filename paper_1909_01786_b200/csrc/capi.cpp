@@ -1,0 +1,683 @@
+// C-ABI of yasmin-b200 (include/yasmin_b200.h). Host orchestration only:
+// parse -> completion -> static store -> device engine. There is no CPU
+// solving path: when no CUDA device is usable the solve entry points fail
+// with YAS_ERR_DEVICE.
+#include "../../include/yasmin_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "device/engine_api.hpp"
+#include "host/compile.hpp"
+#include "host/program.hpp"
+
+using namespace yas;
+
+struct yas_program {
+    Program prog;
+    // lazily compiled views
+    std::unique_ptr<Completion> comp;
+    std::unique_ptr<StaticStore> store;
+
+    const Completion& completion() {
+        if (!comp) comp = std::make_unique<Completion>(compile_completion(prog));
+        return *comp;
+    }
+    const StaticStore& static_store() {
+        if (!store) store = std::make_unique<StaticStore>(build_store(completion().nogoods, completion().total_atoms));
+        return *store;
+    }
+};
+
+struct yas_result {
+    std::vector<std::vector<std::uint32_t>> models;
+    std::vector<std::uint32_t> cubes;
+    yas_stats stats{};
+    int status = 1;
+};
+
+struct yas_store {
+    StaticStore st;
+};
+
+struct yas_propagator {
+    std::unique_ptr<Session> s;
+    std::uint32_t atoms = 0;
+};
+
+namespace {
+
+void put_err(char* err, std::size_t cap, const std::string& msg) {
+    if (!err || cap == 0) return;
+    const std::size_t n = std::min(cap - 1, msg.size());
+    std::memcpy(err, msg.data(), n);
+    err[n] = '\0';
+}
+
+std::size_t put_text(const std::string& s, char* buf, std::size_t cap) {
+    if (buf && cap) {
+        const std::size_t n = std::min(cap - 1, s.size());
+        std::memcpy(buf, s.data(), n);
+        buf[n] = '\0';
+    }
+    return s.size();
+}
+
+struct DeviceMissing : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CapacityError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct VerifyError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void require_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        throw DeviceMissing("no CUDA device available: yasmin-b200 has no CPU solving path");
+    if (device < 0 || device >= n) throw DeviceMissing("CUDA device ordinal out of range");
+}
+
+template <class F>
+int guarded(char* err, std::size_t cap, F&& f) {
+    try {
+        return f();
+    } catch (const ParseFailure& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_PARSE;
+    } catch (const CapacityError& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_CAPACITY;
+    } catch (const VerifyError& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_VERIFY;
+    } catch (const std::logic_error& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_LOGIC;
+    } catch (const DeviceMissing& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_DEVICE;
+    } catch (const std::runtime_error& e) {
+        put_err(err, cap, e.what());
+        return static_cast<int>(std::string(e.what()).rfind("CUDA", 0) == 0 ? YAS_ERR_DEVICE : YAS_ERR_ARG);
+    } catch (const std::exception& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_ARG;
+    }
+}
+
+// Choice atoms: a with rules "a :- not b." and "b :- not a." (the even-loop
+// choice encoding). The first k of them, partners skipped, define the cubes.
+std::vector<AtomId> choice_atoms(const Program& prog, std::uint32_t k) {
+    std::vector<AtomId> partner(prog.atom_count() + 1, 0);
+    for (const Rule& r : prog.rules())
+        if (r.pos_body.empty() && r.neg_body.size() == 1) {
+            const AtomId a = r.head, b = r.neg_body[0];
+            for (std::uint32_t ri : prog.rules_of(b)) {
+                const Rule& s = prog.rules()[ri];
+                if (s.pos_body.empty() && s.neg_body.size() == 1 && s.neg_body[0] == a) {
+                    partner[a] = b;
+                    break;
+                }
+            }
+        }
+    std::vector<AtomId> out;
+    std::vector<char> taken(prog.atom_count() + 1, 0);
+    for (AtomId a = 1; a <= prog.atom_count() && out.size() < k; ++a) {
+        if (!partner[a] || taken[a]) continue;
+        out.push_back(a);
+        taken[a] = taken[partner[a]] = 1;
+    }
+    return out;
+}
+
+void fill_stats(yas_stats& o, const dev::Stats& s) {
+    o.decisions = s.decisions;
+    o.propagations = s.propagations;
+    o.conflicts = s.conflicts;
+    o.learned_count = s.learned_count;
+    o.learned_length_sum = s.learned_length_sum;
+    o.restarts = s.restarts;
+    o.models = s.models;
+    o.passes = s.passes;
+    o.watch_replacements = 0;  // no watched literals on the device
+    o.duplicate_learned = s.duplicate_learned;
+    o.blocking_nogoods = s.blocking_nogoods;
+    o.res_learned = s.res_learned;
+    o.fwd_learned = s.fwd_learned;
+    o.fwd_fallbacks = s.fwd_fallbacks;
+    o.uip_check_failures = s.uip_check_failures;
+    o.fwd_decision_only_failures = s.fwd_decision_only_failures;
+    o.asserting_failures = s.asserting_failures;
+    o.checks = s.checks;
+    o.searches = s.searches;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* yas_version(void) { return "yasmin-b200 0.1 (sm_100a)"; }
+
+int yas_device_count(void) {
+    int n = 0;
+    return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
+int yas_device_name(int device, char* buf, size_t cap) {
+    if (device < 0 || device >= yas_device_count()) return YAS_ERR_DEVICE;
+    put_text(device_name(device), buf, cap);
+    return YAS_OK;
+}
+
+int yas_program_parse(const char* text, size_t len, yas_program** out, int* err_line, char* err, size_t err_cap) {
+    if (!out) return YAS_ERR_ARG;
+    *out = nullptr;
+    if (err_line) *err_line = 0;
+    return guarded(err, err_cap, [&] {
+        try {
+            auto p = std::make_unique<yas_program>();
+            p->prog = parse_text(std::string_view(text ? text : "", text ? len : 0));
+            *out = p.release();
+            return static_cast<int>(YAS_OK);
+        } catch (const ParseFailure& e) {
+            if (err_line) *err_line = e.line;
+            throw;
+        }
+    });
+}
+
+int yas_program_parse_file(const char* path, yas_program** out, int* err_line, char* err, size_t err_cap) {
+    if (!path || !out) return YAS_ERR_ARG;
+    std::ifstream in(path, std::ios::binary);
+    if (!in) {
+        put_err(err, err_cap, std::string("cannot open ") + path);
+        return YAS_ERR_IO;
+    }
+    std::stringstream ss;
+    ss << in.rdbuf();
+    const std::string text = ss.str();
+    return yas_program_parse(text.data(), text.size(), out, err_line, err, err_cap);
+}
+
+void yas_program_free(yas_program* p) { delete p; }
+uint32_t yas_program_atom_count(const yas_program* p) { return p ? p->prog.atom_count() : 0; }
+uint32_t yas_program_rule_count(const yas_program* p) { return p ? static_cast<uint32_t>(p->prog.rules().size()) : 0; }
+uint32_t yas_program_constraint_count(const yas_program* p) {
+    return p ? static_cast<uint32_t>(p->prog.constraints().size()) : 0;
+}
+const char* yas_program_atom_name(const yas_program* p, uint32_t id) {
+    if (!p || id > p->prog.atom_count()) return nullptr;
+    return p->prog.name(id).c_str();
+}
+uint32_t yas_program_find(const yas_program* p, const char* name) { return p && name ? p->prog.find(name) : 0; }
+
+int yas_program_rule(const yas_program* p, uint32_t r, uint32_t* head, const uint32_t** pos, uint32_t* n_pos,
+                     const uint32_t** neg, uint32_t* n_neg) {
+    if (!p) return YAS_ERR_ARG;
+    const std::size_t nr = p->prog.rules().size();
+    if (r >= nr + p->prog.constraints().size()) return YAS_ERR_ARG;
+    const Rule& rule = r < nr ? p->prog.rules()[r] : p->prog.constraints()[r - nr];
+    if (head) *head = rule.head;
+    if (pos) *pos = rule.pos_body.data();
+    if (n_pos) *n_pos = static_cast<uint32_t>(rule.pos_body.size());
+    if (neg) *neg = rule.neg_body.data();
+    if (n_neg) *n_neg = static_cast<uint32_t>(rule.neg_body.size());
+    return YAS_OK;
+}
+
+size_t yas_program_print(const yas_program* p, char* buf, size_t cap) { return p ? put_text(print_text(p->prog), buf, cap) : 0; }
+size_t yas_program_dump_nogoods(const yas_program* p, char* buf, size_t cap) {
+    if (!p) return 0;
+    auto* q = const_cast<yas_program*>(p);
+    return put_text(dump_nogoods(q->completion(), q->prog), buf, cap);
+}
+size_t yas_program_store_csv(const yas_program* p, char* buf, size_t cap) {
+    if (!p) return 0;
+    return put_text(const_cast<yas_program*>(p)->static_store().dump_csv(), buf, cap);
+}
+size_t yas_program_diagnostics(const yas_program* p, char* buf, size_t cap) {
+    if (!p) return 0;
+    std::string s;
+    for (const std::string& d : diagnostics(p->prog)) s += d + "\n";
+    return put_text(s, buf, cap);
+}
+int yas_program_rule_aux(const yas_program* p, uint32_t rule, uint32_t out[4]) {
+    if (!p || rule >= p->prog.rules().size()) return YAS_ERR_ARG;
+    const RuleAux& a = const_cast<yas_program*>(p)->completion().aux[rule];
+    out[0] = a.b;
+    out[1] = a.t;
+    out[2] = a.n;
+    out[3] = a.vacuous ? 1 : 0;
+    return YAS_OK;
+}
+uint32_t yas_program_total_atoms(const yas_program* p) {
+    return p ? const_cast<yas_program*>(p)->completion().total_atoms : 0;
+}
+int yas_program_census(const yas_program* p, uint64_t census_out[3], uint64_t counts[3]) {
+    if (!p) return YAS_ERR_ARG;
+    const Census c = census(p->prog);
+    const Census& k = const_cast<yas_program*>(p)->completion().counts;
+    census_out[0] = c.rule_nogoods;
+    census_out[1] = c.atom_nogoods;
+    census_out[2] = c.constraint_nogoods;
+    counts[0] = k.rule_nogoods;
+    counts[1] = k.atom_nogoods;
+    counts[2] = k.constraint_nogoods;
+    return YAS_OK;
+}
+size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap) {
+    if (!p) return 0;
+    std::vector<AtomId> in(interp, interp + n);
+    const std::vector<AtomId> r = tp_step(p->prog, in);
+    for (std::size_t i = 0; i < r.size() && i < cap; ++i) out[i] = r[i];
+    return r.size();
+}
+int yas_verify_model(const yas_program* p, const uint32_t* ids, size_t n) {
+    if (!p) return 0;
+    return is_answer_set(p->prog, std::vector<AtomId>(ids, ids + n)) ? 1 : 0;
+}
+
+void yas_config_default(yas_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->mode = 0;
+    c->heuristic = 0;
+    c->activity_decay = 0.95;
+    c->workers = 1;
+    c->restart_base = 100;
+    c->restart_factor = 1.5;
+    c->max_models = 1;
+    c->deps_words = 16;
+    c->conflict_fanout = 1;
+    c->learned_capacity = 1ull << 22;
+    c->world = 1;
+}
+
+int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, char* err, size_t err_cap) {
+    if (!p || !out) return YAS_ERR_ARG;
+    *out = nullptr;
+    yas_config cfg;
+    if (cfg_in) cfg = *cfg_in;
+    else yas_config_default(&cfg);
+    return guarded(err, err_cap, [&] {
+        if (cfg.deps_words < 1 || cfg.deps_words > 1024) throw std::invalid_argument("deps_words must be in [1, 1024]");
+        if (cfg.world < 1) cfg.world = 1;
+        require_device(cfg.device);
+        auto* q = const_cast<yas_program*>(p);
+        const Program& prog = q->prog;
+        const Completion& comp = q->completion();
+        const StaticStore& st = q->static_store();
+
+        EngineProgram ep;
+        ep.store = &st;
+        ep.n_prog = prog.atom_count();
+        ep.rules.reserve(prog.rules().size());
+        for (std::size_t r = 0; r < prog.rules().size(); ++r) {
+            const RuleAux& a = comp.aux[r];
+            ep.rules.push_back({prog.rules()[r].head, a.b, a.t, a.n | (a.vacuous ? 0x80000000u : 0u)});
+        }
+
+        dev::Config dc{};
+        dc.mode = cfg.mode == 1 ? 1u : 0u;
+        dc.heur = cfg.heuristic == 1 ? 1u : cfg.heuristic == 2 ? 2u : 0u;
+        dc.decay = cfg.activity_decay;
+        dc.restarts = cfg.restarts_enabled ? 1u : 0u;
+        dc.W = cfg.deps_words;
+        dc.restart_base = cfg.restart_base;
+        dc.restart_factor = cfg.restart_factor;
+        dc.max_models = cfg.max_models;
+        dc.fanout = std::max<std::uint32_t>(1, std::min<std::uint32_t>(cfg.conflict_fanout, 64));
+        dc.debug_validate = cfg.debug_validate ? 1u : 0u;
+        dc.learned_capacity = cfg.learned_capacity;
+        dc.trace = cfg.trace ? 1u : 0u;
+
+        // cubes: every sign pattern over the first k choice atoms, as
+        // integrity constraints (":- a." -> nogood {T a}; ":- not a." -> {F a}).
+        std::vector<std::int32_t> cubes;
+        std::uint32_t width = 0, n_cubes = 1;
+        if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
+            const std::vector<AtomId> ca = choice_atoms(prog, std::min<std::uint32_t>(cfg.cube_atoms, 24));
+            width = static_cast<std::uint32_t>(ca.size());
+            const std::uint32_t total = 1u << width;
+            n_cubes = 0;
+            for (std::uint32_t pat = 0; pat < total; ++pat) {
+                if (static_cast<int>(pat % static_cast<std::uint32_t>(cfg.world)) != cfg.rank) continue;
+                for (std::uint32_t k = 0; k < width; ++k)
+                    cubes.push_back(((pat >> k) & 1u) ? -static_cast<std::int32_t>(ca[k]) : static_cast<std::int32_t>(ca[k]));
+                ++n_cubes;
+            }
+        } else if (cfg.rank != 0) {
+            n_cubes = 0;  // a single search runs on rank 0 only
+        }
+
+        EngineOptions eo;
+        eo.device = cfg.device;
+        const bool wide = cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0);
+        eo.grid = wide;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
+        eo.slots = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * 4;
+        const bool many = width > 0;
+        const std::uint64_t cap = cfg.learned_capacity;
+        eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, many ? (1u << 14) : (1u << 18)));
+        eo.lpool = many ? (1u << 20) : (1u << 22);
+
+        auto res = std::make_unique<yas_result>();
+        for (int attempt = 0;; ++attempt) {
+            std::vector<std::vector<std::uint32_t>> models;
+            std::vector<std::uint32_t> mcubes;
+            std::vector<yas_trace> traces;
+            EngineCallbacks cb;
+            const std::uint32_t np = prog.atom_count();
+            cb.on_model = [&](const EngineModel& m) {
+                std::vector<std::uint32_t> ids;
+                for (std::size_t w = 0; w < m.bits.size(); ++w)
+                    for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
+                        const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
+                        if (a <= np) ids.push_back(a);
+                    }
+                if (cfg.verify) {
+                    // record_model's checks (solver.cpp:221-229)
+                    if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
+                    if (tp_step(prog, ids) != ids)
+                        throw VerifyError("computed model is not a fixpoint of the consequence operator");
+                }
+                models.push_back(std::move(ids));
+                mcubes.push_back(m.cube);
+                return true;
+            };
+            if (cfg.trace)
+                cb.on_trace = [&](std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj) {
+                    traces.push_back({static_cast<int>(mode), conflict, len, bj});
+                };
+            EngineResult er;
+            if (n_cubes > 0) er = engine_solve(ep, dc, eo, cubes, n_cubes, width, cb);
+            if (er.status == dev::kErrArena && attempt < 8) {
+                eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, 2ull * eo.lcap));
+                eo.lpool *= 2;
+                if (many && eo.slots > 64) eo.slots /= 2;
+                continue;
+            }
+            if (er.status == dev::kErrArena) throw std::runtime_error("device learned-nogood arena exhausted");
+            if (er.status == dev::kErrCapacity)
+                throw CapacityError("learned nogood store capacity exceeded (" + std::to_string(cap) + " nogoods)");
+            if (er.status == dev::kErrLogic)
+                throw std::logic_error("res_learning: literal at conflict level has no antecedent");
+            if (er.status == dev::kErrValidate) throw std::logic_error("fixpoint invariant broken");
+            if (cfg.trace)
+                for (const yas_trace& t : traces) cfg.trace(&t, cfg.trace_user);
+            res->models = std::move(models);
+            res->cubes = std::move(mcubes);
+            fill_stats(res->stats, er.stats);
+            res->stats.models = res->models.size();
+            res->stats.wall_ms = er.wall_ms;
+            res->stats.device_ms = er.device_ms;
+            res->stats.launches = er.launches;
+            res->stats.cubes = n_cubes;
+            res->status = res->models.empty() ? 1 : 0;
+            break;
+        }
+        *out = res.release();
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+int yas_result_status(const yas_result* r) { return r ? r->status : 1; }
+uint64_t yas_result_model_count(const yas_result* r) { return r ? r->models.size() : 0; }
+const uint32_t* yas_result_model(const yas_result* r, uint64_t m, uint32_t* n) {
+    if (!r || m >= r->models.size()) {
+        if (n) *n = 0;
+        return nullptr;
+    }
+    if (n) *n = static_cast<uint32_t>(r->models[m].size());
+    return r->models[m].data();
+}
+uint32_t yas_result_model_cube(const yas_result* r, uint64_t m) {
+    return r && m < r->cubes.size() ? r->cubes[m] : 0;
+}
+void yas_result_stats(const yas_result* r, yas_stats* s) {
+    if (r && s) *s = r->stats;
+}
+void yas_result_free(yas_result* r) { delete r; }
+
+size_t yas_stats_csv_header(char* buf, size_t cap) {
+    return put_text(
+        "instance,mode,heuristic,workers,status,models,decisions,propagations,conflicts,learned,avg_learned_len,"
+        "restarts,wall_ms,props_per_sec,decisions_per_sec,learned_per_sec",
+        buf, cap);
+}
+
+size_t yas_emit_stats(const yas_stats* s, const char* instance, const char* mode, const char* heur, unsigned workers,
+                      int status, uint64_t models, int csv, char* buf, size_t cap) {
+    // SolveStats rates and emit_stats formatting (solver.hpp:80-92, solver.cpp:336-360)
+    const double avg = s->learned_count ? static_cast<double>(s->learned_length_sum) / static_cast<double>(s->learned_count) : 0.0;
+    auto rate = [&](uint64_t c) { return s->wall_ms <= 0.0 ? 0.0 : static_cast<double>(c) / (s->wall_ms / 1000.0); };
+    const char* st = status == 0 ? "SAT" : "UNSAT";
+    std::ostringstream o;
+    if (csv) {
+        o << (instance ? instance : "") << ',' << (mode ? mode : "") << ',' << (heur ? heur : "") << ',' << workers << ','
+          << st << ',' << models << ',' << s->decisions << ',' << s->propagations << ',' << s->conflicts << ','
+          << s->learned_count << ',' << avg << ',' << s->restarts << ',' << s->wall_ms << ',' << rate(s->propagations)
+          << ',' << rate(s->decisions) << ',' << rate(s->learned_count);
+    } else {
+        o << "instance       : " << (instance ? instance : "") << '\n'
+          << "mode/heuristic : " << (mode ? mode : "") << '/' << (heur ? heur : "") << " (workers " << workers << ")\n"
+          << "status         : " << st << '\n'
+          << "models         : " << models << '\n'
+          << "decisions      : " << s->decisions << " (" << rate(s->decisions) << "/s)\n"
+          << "propagations   : " << s->propagations << " (" << rate(s->propagations) << "/s)\n"
+          << "conflicts      : " << s->conflicts << '\n'
+          << "learned        : " << s->learned_count << " (" << rate(s->learned_count) << "/s, avg len " << avg << ")\n"
+          << "restarts       : " << s->restarts << '\n'
+          << "wall time      : " << s->wall_ms << " ms";
+    }
+    return put_text(o.str(), buf, cap);
+}
+
+int yas_store_build(const int32_t* lits, const uint32_t* offsets, size_t n, const uint32_t* guards,
+                    const uint8_t* origins, uint32_t total_atoms, yas_store** out, char* err, size_t err_cap) {
+    if (!out) return YAS_ERR_ARG;
+    *out = nullptr;
+    return guarded(err, err_cap, [&] {
+        std::vector<Nogood> ngs;
+        ngs.reserve(n);
+        for (size_t k = 0; k < n; ++k) {
+            std::vector<std::int32_t> l(lits + offsets[k], lits + offsets[k + 1]);
+            for (std::int32_t x : l)
+                if (x == 0 || lit_atom(x) > total_atoms) throw std::invalid_argument("literal out of range");
+            auto ng = Nogood::make(std::move(l), origins ? origins[k] : kConstraint, guards ? guards[k] : kAnyTruth);
+            if (!ng || ng->lits.empty()) throw std::invalid_argument("vacuous or empty nogood " + std::to_string(k));
+            ngs.push_back(std::move(*ng));
+        }
+        auto s = std::make_unique<yas_store>();
+        s->st = build_store(ngs, total_atoms);
+        *out = s.release();
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+void yas_store_free(yas_store* s) { delete s; }
+uint32_t yas_store_size(const yas_store* s) { return s ? s->st.size() : 0; }
+uint32_t yas_store_total_atoms(const yas_store* s) { return s ? s->st.total_atoms : 0; }
+size_t yas_store_dump_csv(const yas_store* s, char* buf, size_t cap) { return s ? put_text(s->st.dump_csv(), buf, cap) : 0; }
+size_t yas_store_units(const yas_store* s, int32_t* out, size_t cap) {
+    if (!s) return 0;
+    for (size_t i = 0; i < s->st.units.size() && i < cap; ++i) out[i] = s->st.units[i];
+    return s->st.units.size();
+}
+size_t yas_store_unit_ids(const yas_store* s, int32_t* out, size_t cap) {
+    if (!s) return 0;
+    for (size_t i = 0; i < s->st.unit_ids.size() && i < cap; ++i) out[i] = s->st.unit_ids[i];
+    return s->st.unit_ids.size();
+}
+void yas_store_bounds(const yas_store* s, uint32_t out[4]) {
+    for (int i = 0; i < 4; ++i) out[i] = s ? s->st.bounds[i] : 0;
+}
+size_t yas_store_occurrences(const yas_store* s, int32_t lit, uint32_t cls, int32_t* out, size_t cap) {
+    if (!s || cls > 3 || lit == 0 || lit_atom(lit) > s->st.total_atoms) return 0;
+    const std::uint32_t key = lit_index(lit) * 4 + cls;
+    const std::uint32_t lo = s->st.occ_off[key], hi = s->st.occ_off[key + 1];
+    for (std::uint32_t i = lo; i < hi && i - lo < cap; ++i) out[i - lo] = s->st.occ_ids[i];
+    return hi - lo;
+}
+
+int yas_store_planted(uint32_t atoms, uint64_t count, uint32_t pct, uint64_t seed, yas_store** out, int32_t** seeded,
+                      size_t* n_seeded, int32_t* decision) {
+    if (!out || atoms < 2) return YAS_ERR_ARG;
+    // SplitMix64 stream as in /root/reference/proj/tests/support/gen.hpp:16-29.
+    std::uint64_t state = seed;
+    auto next = [&]() {
+        std::uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    };
+    auto below = [&](std::uint64_t n) { return n == 0 ? 0 : next() % n; };
+    std::vector<std::uint8_t> h(atoms + 1, 0);
+    for (uint32_t a = 1; a <= atoms; ++a) h[a] = below(100) < 50 ? 1 : 0;
+    auto hlit = [&](uint32_t a) { return h[a] ? static_cast<std::int32_t>(a) : -static_cast<std::int32_t>(a); };
+    std::vector<Nogood> ngs;
+    ngs.reserve(count);
+    while (ngs.size() < count) {
+        const uint32_t len = 2 + static_cast<uint32_t>(below(5));
+        std::vector<std::int32_t> l;
+        for (uint32_t k = 0; k < len; ++k) {
+            const std::int32_t a = static_cast<std::int32_t>(1 + below(atoms));
+            l.push_back(below(100) < 50 ? a : -a);
+        }
+        l[0] = -hlit(lit_atom(l[0]));
+        if (auto ng = Nogood::make(std::move(l), kConstraint)) ngs.push_back(std::move(*ng));
+    }
+    std::vector<std::int32_t> sd;
+    for (uint32_t a = 2; a <= atoms; ++a)
+        if (below(100) < pct) sd.push_back(hlit(a));
+    auto s = std::make_unique<yas_store>();
+    s->st = build_store(ngs, atoms);
+    *out = s.release();
+    if (decision) *decision = hlit(1);
+    if (seeded && n_seeded) {
+        *n_seeded = sd.size();
+        *seeded = static_cast<int32_t*>(std::malloc(std::max<size_t>(1, sd.size()) * sizeof(int32_t)));
+        std::copy(sd.begin(), sd.end(), *seeded);
+    }
+    return YAS_OK;
+}
+
+void yas_free_ints(int32_t* p) { std::free(p); }
+
+int yas_propagator_create(const yas_store* s, uint32_t deps_words, int engine, int device, yas_propagator** out,
+                          char* err, size_t err_cap) {
+    if (!s || !out) return YAS_ERR_ARG;
+    *out = nullptr;
+    return guarded(err, err_cap, [&] {
+        require_device(device);
+        if (deps_words < 1 || deps_words > 1024) throw std::invalid_argument("deps_words must be in [1, 1024]");
+        auto p = std::make_unique<yas_propagator>();
+        const bool grid = engine == 2 || (engine == 0 && s->st.size() >= (1u << 18));
+        p->s = std::make_unique<Session>(s->st, deps_words, grid, device);
+        p->atoms = s->st.total_atoms;
+        *out = p.release();
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+void yas_propagator_free(yas_propagator* p) { delete p; }
+
+static void outcome_from(yas_propagator* p, bool violated, const dev::Ctl& before, yas_outcome* o) {
+    if (!o) return;
+    const dev::Ctl c = p->s->ctl();
+    o->violated = violated ? 1 : 0;
+    o->propagations = c.st.propagations - before.st.propagations;
+    o->passes = c.st.passes - before.st.passes;
+    o->checks = c.st.checks - before.st.checks;
+    o->n_conflicts = c.n_confl;
+    o->device_ms = p->s->last_ms();
+}
+
+int yas_propagator_reset(yas_propagator* p) {
+    return guarded(nullptr, 0, [&] { p->s->reset(); return static_cast<int>(YAS_OK); });
+}
+int yas_propagator_initial(yas_propagator* p, yas_outcome* o) {
+    return guarded(nullptr, 0, [&] {
+        const dev::Ctl before = p->s->ctl();
+        const bool v = p->s->initial_propagation();
+        outcome_from(p, v, before, o);
+        return static_cast<int>(YAS_OK);
+    });
+}
+int yas_propagator_propagate(yas_propagator* p, uint32_t level, yas_outcome* o) {
+    return guarded(nullptr, 0, [&] {
+        const dev::Ctl before = p->s->ctl();
+        const bool v = p->s->propagate(level);
+        outcome_from(p, v, before, o);
+        return static_cast<int>(YAS_OK);
+    });
+}
+int yas_propagator_push_decision(yas_propagator* p, int32_t lit) {
+    return guarded(nullptr, 0, [&] { p->s->push_decision(lit); return static_cast<int>(YAS_OK); });
+}
+int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level, const uint64_t* deps,
+                          uint32_t n_deps, int overflow, int32_t antecedent) {
+    return guarded(nullptr, 0, [&] {
+        std::vector<unsigned long long> d(deps, deps + n_deps);
+        p->s->assign(std::vector<std::int32_t>(lits, lits + n), level, antecedent, d, overflow != 0);
+        return static_cast<int>(YAS_OK);
+    });
+}
+int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n) {
+    return guarded(nullptr, 0, [&] { p->s->seed(std::vector<std::int32_t>(lits, lits + n)); return static_cast<int>(YAS_OK); });
+}
+int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n) {
+    int32_t id = -1;
+    guarded(nullptr, 0, [&] { id = p->s->add_learned(std::vector<std::int32_t>(lits, lits + n)); return 0; });
+    return id;
+}
+uint32_t yas_propagator_atoms(const yas_propagator* p) { return p ? p->atoms : 0; }
+uint32_t yas_propagator_level(const yas_propagator* p) { return p ? p->s->ctl().cdl : 0; }
+int yas_propagator_cells(const yas_propagator* p, int32_t* out) {
+    const auto v = p->s->cells();
+    std::copy(v.begin(), v.end(), out);
+    return YAS_OK;
+}
+int yas_propagator_reasons(const yas_propagator* p, int32_t* out) {
+    const auto v = p->s->reasons();
+    std::copy(v.begin(), v.end(), out);
+    return YAS_OK;
+}
+int yas_propagator_deps(const yas_propagator* p, uint32_t word, uint64_t* out, uint8_t* overflow) {
+    if (word >= p->s->deps_words()) return YAS_ERR_ARG;
+    const auto v = p->s->deps_word(word);
+    std::copy(v.begin(), v.end(), out);
+    if (overflow) {
+        const auto o = p->s->deps_overflow();
+        std::copy(o.begin(), o.end(), overflow);
+    }
+    return YAS_OK;
+}
+size_t yas_propagator_trail(const yas_propagator* p, int32_t* out, size_t cap) {
+    const auto v = p->s->trail();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    return v.size();
+}
+size_t yas_propagator_conflicts(const yas_propagator* p, int32_t* out, size_t cap) {
+    const auto v = p->s->conflicts();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    return v.size();
+}
+size_t yas_propagator_frontier(const yas_propagator* p, int32_t* out, size_t cap) {
+    const auto v = p->s->frontier();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+    return v.size();
+}
+
+}  // extern "C"

@@ -1,0 +1,1460 @@
+// yasmin-b200 device engine (sm_100a).
+//
+// The whole conflict-driven loop of the reference (Driver::run,
+// /root/reference/proj/src/solver.cpp:248-303) runs on the device. The code is
+// written once against a "group" abstraction and instantiated twice:
+//   * BlockG  — one CTA owns one search; passes are separated by __syncthreads
+//               and the control block lives in shared memory. Used for
+//               structured/small stores and for cube-split enumeration (one
+//               search per CTA, many CTAs per GPU).
+//   * GridG   — every CTA of a cooperative grid works on ONE search; passes are
+//               separated by a grid barrier. Used for wide propagation over
+//               large stores (the 1M-nogood configurations).
+//
+// One propagation pass (propagate.cpp:170-205) is made exact and
+// order-independent by a dense "expansion index" e: the frontier literals'
+// occurrence lists, concatenated in frontier order and, per literal, in class
+// (unit, binary, ternary, long) then id order, are numbered 0..T-1. The
+// reference's item order (build_items, propagate.cpp:71-84) is exactly
+// "ascending min-e of each nogood", and its merge (first proposal in item
+// order wins an atom) is an atomicMin on (e, sign) per atom. Winners are
+// compacted in e order with one group scan, which also yields the next
+// frontier's occurrence offsets. Watched literals are not used: the reference
+// results do not depend on them, so every check scans the
+// nogood (a few literals, L1/L2 resident).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "engine_api.hpp"
+
+namespace yas::dev {
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ std::uint32_t atom_of(std::int32_t l) { return l < 0 ? -l : l; }
+__device__ __forceinline__ std::uint32_t lidx(std::int32_t l) { return 2u * atom_of(l) + (l < 0 ? 1u : 0u); }
+__device__ __forceinline__ std::uint32_t lvl_of(std::int32_t c) { return c < 0 ? -c : c; }
+__device__ __forceinline__ bool may_assert(std::uint32_t guard, std::int32_t l) {
+    return l < 0 || guard == kAny || guard == atom_of(l);
+}
+__device__ __forceinline__ std::uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned long long wkey(std::uint32_t gen, std::uint32_t e, bool neg) {
+    return (static_cast<unsigned long long>(~gen) << 32) | (static_cast<unsigned long long>(e) << 1) | (neg ? 1ull : 0ull);
+}
+__device__ __forceinline__ unsigned long long ckey(std::uint32_t gen, std::uint32_t e) {
+    return (static_cast<unsigned long long>(~gen) << 32) | e;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ bool better(double s, std::uint32_t i, double bs, std::uint32_t bi) {
+    return s > bs || (s == bs && i < bi);
+}
+
+// Warp-aggregated append: every lane of the (converged) warp calls it.
+__device__ __forceinline__ std::uint32_t warp_append(std::uint32_t* ctr, bool pred) {
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    if (b == 0) return 0xffffffffu;
+    const int leader = __ffs(b) - 1;
+    std::uint32_t base = 0;
+    if (static_cast<int>(lane_id()) == leader) base = atomicAdd(ctr, static_cast<std::uint32_t>(__popc(b)));
+    base = __shfl_sync(0xffffffffu, base, leader);
+    return pred ? base + __popc(b & ((1u << lane_id()) - 1u)) : 0xffffffffu;
+}
+__device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
+    const unsigned b = __ballot_sync(0xffffffffu, pred);
+    if (b && lane_id() == static_cast<std::uint32_t>(__ffs(b) - 1)) atomicAdd(ctr, static_cast<unsigned long long>(__popc(b)));
+}
+
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        unsigned long long o = __shfl_up_sync(0xffffffffu, v, d);
+        if (static_cast<int>(lane_id()) >= d) v += o;
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// Groups
+// ---------------------------------------------------------------------------
+template <int BS>
+struct BlockG {
+    static constexpr int kWarps = BS / 32;
+    Ctl* c;
+    unsigned long long* sbuf;  // kWarps+2 words of shared scratch
+    double* sd;                // kWarps doubles
+    std::uint32_t* si;         // kWarps words
+
+    __device__ std::uint32_t tid() const { return threadIdx.x; }
+    __device__ std::uint32_t size() const { return BS; }
+    __device__ bool leader() const { return threadIdx.x == 0; }
+    __device__ void sync() { __syncthreads(); }
+
+    // Exclusive scan of one value per thread over the whole group.
+    __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
+        const std::uint32_t w = threadIdx.x >> 5;
+        unsigned long long inc = warp_incl_scan(v);
+        if (lane_id() == 31) sbuf[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long x = lane_id() < kWarps ? sbuf[lane_id()] : 0ull;
+            unsigned long long xi = warp_incl_scan(x);
+            if (lane_id() < kWarps) sbuf[lane_id()] = xi - x;
+            if (lane_id() == 31) sbuf[kWarps] = xi;
+        }
+        __syncthreads();
+        const unsigned long long r = sbuf[w] + inc - v;
+        total = sbuf[kWarps];
+        __syncthreads();
+        return r;
+    }
+
+    __device__ void argmax(double& s, std::uint32_t& i) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            double os = __shfl_down_sync(0xffffffffu, s, d);
+            std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+            if (better(os, oi, s, i)) { s = os; i = oi; }
+        }
+        const std::uint32_t w = threadIdx.x >> 5;
+        if (lane_id() == 0) { sd[w] = s; si[w] = i; }
+        __syncthreads();
+        if (w == 0) {
+            s = lane_id() < kWarps ? sd[lane_id()] : -1.0;
+            i = lane_id() < kWarps ? si[lane_id()] : 0xffffffffu;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                double os = __shfl_down_sync(0xffffffffu, s, d);
+                std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+                if (better(os, oi, s, i)) { s = os; i = oi; }
+            }
+            if (lane_id() == 0) { sd[0] = s; si[0] = i; }
+        }
+        __syncthreads();
+        s = sd[0];
+        i = si[0];
+        __syncthreads();
+    }
+};
+
+template <int BS>
+struct GridG {
+    static constexpr int kWarps = BS / 32;
+    Ctl* c;
+    Shared* sh;
+    unsigned long long* partial;  // 2 * gridDim.x
+    double* pd;                   // gridDim.x
+    std::uint32_t* pi;            // gridDim.x
+    unsigned long long* sbuf;
+    double* sd;
+    std::uint32_t* si;
+    std::uint32_t parity;
+
+    __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
+    __device__ std::uint32_t size() const { return gridDim.x * BS; }
+    __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
+
+    __device__ void sync() {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            volatile std::uint32_t* vgen = &sh->bar_gen;
+            const std::uint32_t g0 = *vgen;
+            __threadfence();
+            const std::uint32_t arrived = atomicAdd(&sh->bar_count, 1u);
+            if (arrived == gridDim.x - 1) {
+                sh->bar_count = 0;
+                __threadfence();
+                atomicAdd(&sh->bar_gen, 1u);
+            } else {
+                while (*vgen == g0) { }
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+
+    __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
+        const std::uint32_t w = threadIdx.x >> 5;
+        unsigned long long inc = warp_incl_scan(v);
+        if (lane_id() == 31) sbuf[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long x = lane_id() < kWarps ? sbuf[lane_id()] : 0ull;
+            unsigned long long xi = warp_incl_scan(x);
+            if (lane_id() < kWarps) sbuf[lane_id()] = xi - x;
+            if (lane_id() == 31) sbuf[kWarps] = xi;
+        }
+        __syncthreads();
+        unsigned long long* part = partial + parity * gridDim.x;
+        parity ^= 1u;
+        if (threadIdx.x == 0) part[blockIdx.x] = sbuf[kWarps];
+        sync();
+        if (w == 0) {
+            unsigned long long before = 0, all = 0;
+            for (std::uint32_t b = lane_id(); b < gridDim.x; b += 32) {
+                const unsigned long long x = part[b];
+                all += x;
+                if (b < blockIdx.x) before += x;
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                before += __shfl_down_sync(0xffffffffu, before, d);
+                all += __shfl_down_sync(0xffffffffu, all, d);
+            }
+            if (lane_id() == 0) { sbuf[kWarps + 1] = before; sbuf[kWarps + 2] = all; }
+        }
+        __syncthreads();
+        const unsigned long long r = sbuf[kWarps + 1] + sbuf[w] + inc - v;
+        total = sbuf[kWarps + 2];
+        __syncthreads();
+        return r;
+    }
+
+    __device__ void argmax(double& s, std::uint32_t& i) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            double os = __shfl_down_sync(0xffffffffu, s, d);
+            std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+            if (better(os, oi, s, i)) { s = os; i = oi; }
+        }
+        const std::uint32_t w = threadIdx.x >> 5;
+        if (lane_id() == 0) { sd[w] = s; si[w] = i; }
+        __syncthreads();
+        if (w == 0) {
+            s = lane_id() < kWarps ? sd[lane_id()] : -1.0;
+            i = lane_id() < kWarps ? si[lane_id()] : 0xffffffffu;
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                double os = __shfl_down_sync(0xffffffffu, s, d);
+                std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+                if (better(os, oi, s, i)) { s = os; i = oi; }
+            }
+            if (lane_id() == 0) { pd[blockIdx.x] = s; pi[blockIdx.x] = i; }
+        }
+        sync();
+        if (w == 0) {
+            s = -1.0;
+            i = 0xffffffffu;
+            for (std::uint32_t b = lane_id(); b < gridDim.x; b += 32)
+                if (better(pd[b], pi[b], s, i)) { s = pd[b]; i = pi[b]; }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                double os = __shfl_down_sync(0xffffffffu, s, d);
+                std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+                if (better(os, oi, s, i)) { s = os; i = oi; }
+            }
+            if (lane_id() == 0) { sd[0] = s; si[0] = i; }
+        }
+        __syncthreads();
+        s = sd[0];
+        i = si[0];
+        // every block leaves pd/pi untouched until the next argmax, which is
+        // separated from this one by at least one grid barrier.
+        __syncthreads();
+    }
+};
+
+// ---------------------------------------------------------------------------
+// The search (one instance per group)
+// ---------------------------------------------------------------------------
+template <class G>
+struct Search {
+    G& g;
+    const Static& S;
+    const Config& C;
+    const Slot& sl;
+    const Caps& K;
+    Shared* sh;
+    Ctl* c;
+    unsigned long long t0;
+
+    __device__ Search(G& g_, const Static& s, const Config& cf, const Slot& slot, const Caps& k, Shared* shared,
+                      unsigned long long start)
+        : g(g_), S(s), C(cf), sl(slot), K(k), sh(shared), c(g_.c), t0(start) {}
+
+    // ---- store access ----------------------------------------------------
+    __device__ const std::int32_t* lits_of(std::uint32_t id, std::uint32_t& len) const {
+        if (id < S.N) {
+            const std::uint32_t lo = __ldg(S.off + id);
+            len = __ldg(S.off + id + 1) - lo;
+            return S.pool + lo;
+        }
+        const std::uint32_t k = id - S.N;
+        const std::uint32_t lo = sl.loff[k];
+        len = sl.loff[k + 1] - lo;
+        return sl.lpool + lo;
+    }
+    __device__ std::int32_t lit_at(const std::int32_t* p, std::uint32_t k, std::uint32_t id) const {
+        return id < S.N ? __ldg(p + k) : p[k];
+    }
+    __device__ std::uint32_t length_of(std::uint32_t id) const {
+        if (id < S.N) return __ldg(S.off + id + 1) - __ldg(S.off + id);
+        return sl.loff[id - S.N + 1] - sl.loff[id - S.N];
+    }
+    __device__ std::uint32_t guard_of(std::uint32_t id) const { return id < S.N ? __ldg(S.guard + id) : kNone; }
+    __device__ std::uint32_t occ_total(std::uint32_t li) const {
+        return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot[li];
+    }
+    // j-th entry of the literal's occurrence list [static c0, learned c0, ..., static c3, learned c3]
+    __device__ std::int32_t occ_entry(std::uint32_t li, std::uint32_t j) const {
+#pragma unroll 1
+        for (std::uint32_t cl = 0; cl < 4; ++cl) {
+            const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
+            if (j < hi - lo) return __ldg(S.occ_ids + lo + j);
+            j -= hi - lo;
+            const std::uint32_t* h = sl.lhdr + 3 * (li * 4 + cl);
+            const std::uint32_t n = h[1];
+            if (j < n) return sl.larena[h[0] + j];
+            j -= n;
+        }
+        return -1;
+    }
+    __device__ std::uint32_t nwords(std::uint32_t level) const {
+        const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
+        return nw < C.W ? nw : C.W;
+    }
+    __device__ unsigned long long& dep(std::uint32_t w, std::uint32_t a) const {
+        return sl.deps[static_cast<std::size_t>(w) * (S.A + 1) + a];
+    }
+    __device__ bool holds(std::int32_t l) const {
+        const std::int32_t cv = sl.cells[atom_of(l)];
+        return cv != 0 && ((cv > 0) == (l > 0));
+    }
+
+    __device__ void fail(std::uint32_t status) {
+        if (g.leader()) c->status = status;
+    }
+
+    // Deps of the literal derived from nogood (lits,len) on atom `a`:
+    // OR of Deps[x] over the other atoms with level > 1 (propagate.cpp:49-62).
+    __device__ void write_deps_from(const std::int32_t* L, std::uint32_t len, std::uint32_t id, std::uint32_t a,
+                                    std::uint32_t level) const {
+        const std::uint32_t nw = nwords(level);
+        std::uint8_t ovf = 0;
+        for (std::uint32_t w = 0; w < nw; ++w) {
+            unsigned long long acc = 0;
+            for (std::uint32_t k = 0; k < len; ++k) {
+                const std::uint32_t x = atom_of(lit_at(L, k, id));
+                if (x == a) continue;
+                if (lvl_of(sl.cells[x]) <= 1) continue;
+                acc |= dep(w, x);
+                if (w == 0) ovf |= sl.dovf[x];
+            }
+            dep(w, a) = acc;
+        }
+        sl.dovf[a] = ovf;
+    }
+
+    // ---- group-parallel building blocks -------------------------------------
+    // Exclusive occurrence offsets of the current frontier; sets c->T.
+    __device__ void frontier_offsets() {
+        const std::uint32_t F = c->F;
+        const std::int32_t* fr = sl.fr[c->cur];
+        unsigned long long carry = 0;
+        for (std::uint32_t base = 0; base < F; base += g.size()) {
+            const std::uint32_t p = base + g.tid();
+            const unsigned long long v = p < F ? occ_total(lidx(fr[p])) : 0ull;
+            unsigned long long tot;
+            const unsigned long long pre = g.scan(v, tot) + carry;
+            if (p < F) sl.froff[p] = static_cast<std::uint32_t>(pre);
+            carry += tot;
+        }
+        g.sync();
+        if (g.leader()) {
+            sl.froff[F] = static_cast<std::uint32_t>(carry);
+            c->T = static_cast<std::uint32_t>(carry);
+            c->b[11] = 0;
+        }
+        g.sync();
+    }
+
+    // Winners marked in the bitmap (bits e < T) are written, in e order, to the
+    // frontier buffer `dst`, appended to the trail, and the occurrence offsets
+    // of that new frontier are produced by the same scan.
+    __device__ void compact(std::uint32_t T, std::uint32_t dst, bool pass) {
+        const std::uint32_t nw = (T + 31) / 32;
+        const std::uint32_t ts0 = c->ts;
+        std::int32_t* out = sl.fr[dst];
+        unsigned long long carry = 0;
+        for (std::uint32_t base = 0; base < nw; base += g.size()) {
+            const std::uint32_t wi = base + g.tid();
+            std::uint32_t bits = wi < nw ? sl.bitmap[wi] : 0u;
+            unsigned long long occ = 0;
+            for (std::uint32_t b = bits; b; b &= b - 1) occ += occ_total(lidx(sl.litat[wi * 32 + __ffs(b) - 1]));
+            const unsigned long long v = (static_cast<unsigned long long>(__popc(bits)) << 32) | occ;
+            unsigned long long tot;
+            const unsigned long long pre = g.scan(v, tot) + carry;
+            std::uint32_t r = static_cast<std::uint32_t>(pre >> 32);
+            std::uint32_t o = static_cast<std::uint32_t>(pre);
+            for (std::uint32_t b = bits; b; b &= b - 1) {
+                const std::int32_t lit = sl.litat[wi * 32 + __ffs(b) - 1];
+                out[r] = lit;
+                sl.froff[r] = o;
+                sl.trail[ts0 + r] = lit;
+                sl.tpos[atom_of(lit)] = ts0 + r;
+                o += occ_total(lidx(lit));
+                ++r;
+            }
+            if (bits) sl.bitmap[wi] = 0u;
+            carry += tot;
+        }
+        g.sync();
+        if (g.leader()) {
+            const std::uint32_t cnt = static_cast<std::uint32_t>(carry >> 32);
+            sl.froff[cnt] = static_cast<std::uint32_t>(carry);
+            c->ts = ts0 + cnt;
+            c->F = cnt;
+            c->T = static_cast<std::uint32_t>(carry);
+            c->st.propagations += cnt;
+            c->n_props = 0;
+            if (pass) {
+                c->st.passes += 1;
+                c->cur = dst;
+                c->b[11] = c->n_confl > 0 ? 1u : 0u;
+            }
+            c->gen += 1;
+        }
+        g.sync();
+    }
+
+    // Apply proposals: per atom the smallest key wins (newly_set); an opposite
+    // loser turns its nogood into a conflict (assignment.cpp:116-124).
+    __device__ void apply(std::uint32_t level, bool unit) {
+        const std::uint32_t np = c->n_props;
+        const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
+        for (std::uint32_t base = g.tid() & ~31u; base < np; base += g.size()) {
+            const std::uint32_t i = base + lane_id();
+            bool lose = false;
+            int4 p = make_int4(0, 0, 0, 0);
+            if (i < np) {
+                p = sl.props[i];
+                const std::uint32_t a = atom_of(p.y);
+                const unsigned long long w = sl.win[a];
+                if ((static_cast<std::uint32_t>(w) >> 1) == static_cast<std::uint32_t>(p.z)) {
+                    sl.cells[a] = p.y > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level);
+                    if (unit) {
+                        sl.reason[a] = kReasonUnit;
+                    } else {
+                        sl.reason[a] = p.x;
+                        std::uint32_t len;
+                        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(p.x), len);
+                        write_deps_from(L, len, static_cast<std::uint32_t>(p.x), a, dlev);
+                    }
+                    atomicOr(sl.bitmap + (p.z >> 5), 1u << (p.z & 31));
+                    sl.litat[p.z] = p.y;
+                } else {
+                    lose = (w & 1ull) != (p.y < 0 ? 1ull : 0ull);
+                }
+            }
+            __syncwarp();
+            const std::uint32_t slot = warp_append(&c->n_confl, lose);
+            if (lose) sl.confl[slot] = p.x;
+        }
+        g.sync();
+    }
+
+    // One propagation call to fixpoint or violation (propagate.cpp:170-205).
+    // Returns true when conflicts were found (they are in confl[0..n_confl)).
+    __device__ bool propagate(std::uint32_t level) {
+        frontier_offsets();
+        for (;;) {
+            const std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur;
+            if (F == 0) break;
+            const std::int32_t* fr = sl.fr[cur];
+            // expand + claim + evaluate against the pass-start snapshot
+            for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
+                const std::uint32_t e = base + lane_id();
+                bool first = false, conflict = false, prop = false;
+                std::int32_t id = -1, plit = 0;
+                if (e < T) {
+                    std::uint32_t lo = 0, hi = F;  // largest p with froff[p] <= e
+                    while (hi - lo > 1) {
+                        const std::uint32_t mid = (lo + hi) >> 1;
+                        if (sl.froff[mid] <= e) lo = mid; else hi = mid;
+                    }
+                    id = occ_entry(lidx(fr[lo]), e - sl.froff[lo]);
+                    const unsigned long long old = atomicMin(sl.claim + id, ckey(gen, e));
+                    first = static_cast<std::uint32_t>(old >> 32) != ~gen;
+                    if (first) {
+                        std::uint32_t len;
+                        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+                        if (len == 1) {
+                            conflict = holds(lit_at(L, 0, id));
+                        } else {
+                            std::uint32_t nfree = 0;
+                            std::int32_t u1 = 0;
+                            bool dead = false;
+                            for (std::uint32_t k = 0; k < len; ++k) {
+                                const std::int32_t l = lit_at(L, k, id);
+                                const std::int32_t cv = sl.cells[atom_of(l)];
+                                if (cv == 0) {
+                                    if (nfree == 0) u1 = l;
+                                    if (++nfree == 2) break;
+                                } else if ((cv > 0) != (l > 0)) {
+                                    dead = true;
+                                    break;
+                                }
+                            }
+                            if (!dead) {
+                                if (nfree == 0) conflict = true;
+                                else if (nfree == 1 && may_assert(guard_of(id), -u1)) { prop = true; plit = -u1; }
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                warp_count(&c->st.checks, first);
+                const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+                if (conflict) sl.confl[cs] = id;
+                const std::uint32_t ps = warp_append(&c->n_props, prop);
+                if (prop) sl.props[ps] = make_int4(id, plit, 0, 0);
+            }
+            g.sync();
+            // resolve: final min-e of every proposing nogood, atomicMin per atom
+            const std::uint32_t np = c->n_props;
+            for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
+                int4 p = sl.props[i];
+                const std::uint32_t e = static_cast<std::uint32_t>(sl.claim[p.x]);
+                p.z = static_cast<std::int32_t>(e);
+                sl.props[i] = p;
+                atomicMin(sl.win + atom_of(p.y), wkey(gen, e, p.y < 0));
+            }
+            g.sync();
+            apply(level, false);
+            compact(T, cur ^ 1u, true);
+            if (c->b[11]) return true;
+        }
+        return false;
+    }
+
+    // Initial propagation (propagate.cpp:23-47): static units in compile order
+    // (conflict id -(k+1)), then every length-1 store entry in id order,
+    // asserted if its guard allows, else a passive violation check. The
+    // sequential semantics are reproduced with order keys e.
+    __device__ bool initial_propagation(bool keep_conflicts) {
+        const std::uint32_t n1 = S.n_units, n2 = S.n_uids + c->lunits_n, total = n1 + n2;
+        const std::uint32_t gen = c->gen;
+        for (std::uint32_t base = g.tid() & ~31u; base < total; base += g.size()) {
+            const std::uint32_t e = base + lane_id();
+            bool conflict = false, prop = false;
+            std::int32_t id = 0, lit = 0;
+            if (e < total) {
+                std::int32_t sigma;
+                bool force = true;
+                if (e < n1) {
+                    sigma = __ldg(S.units + e);
+                    id = -static_cast<std::int32_t>(e) - 1;
+                } else {
+                    const std::uint32_t m = e - n1;
+                    id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits[m - S.n_uids];
+                    std::uint32_t len;
+                    const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+                    sigma = lit_at(L, 0, static_cast<std::uint32_t>(id));
+                    force = may_assert(guard_of(static_cast<std::uint32_t>(id)), -sigma);
+                }
+                if (force) {
+                    lit = -sigma;
+                    const std::int32_t cv = sl.cells[atom_of(lit)];
+                    if (cv != 0) {
+                        conflict = (cv > 0) != (lit > 0);
+                    } else {
+                        prop = true;
+                        atomicMin(sl.win + atom_of(lit), wkey(gen, e, lit < 0));
+                    }
+                }
+            }
+            __syncwarp();
+            const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+            if (conflict) sl.confl[cs] = id;
+            const std::uint32_t ps = warp_append(&c->n_props, prop);
+            if (prop) sl.props[ps] = make_int4(id, lit, static_cast<std::int32_t>(e), 0);
+        }
+        g.sync();
+        // passive unit entries see the assignments made before them in order
+        for (std::uint32_t base = g.tid() & ~31u; base < n2; base += g.size()) {
+            const std::uint32_t m = base + lane_id();
+            bool conflict = false;
+            std::int32_t id = 0;
+            if (m < n2) {
+                id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits[m - S.n_uids];
+                std::uint32_t len;
+                const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+                const std::int32_t sigma = lit_at(L, 0, static_cast<std::uint32_t>(id));
+                if (!may_assert(guard_of(static_cast<std::uint32_t>(id)), -sigma)) {
+                    const std::uint32_t a = atom_of(sigma);
+                    const std::int32_t cv = sl.cells[a];
+                    if (cv != 0) {
+                        conflict = (cv > 0) == (sigma > 0);
+                    } else {
+                        const unsigned long long w = sl.win[a];
+                        conflict = static_cast<std::uint32_t>(w >> 32) == ~gen &&
+                                   (static_cast<std::uint32_t>(w) >> 1) < n1 + m &&
+                                   ((w & 1ull) != 0) == (sigma < 0);
+                    }
+                }
+            }
+            __syncwarp();
+            const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+            if (conflict) sl.confl[cs] = id;
+        }
+        g.sync();
+        apply(1, true);
+        compact(total, c->cur, false);
+        const bool violated = c->n_confl > 0;
+        g.sync();
+        if (!keep_conflicts && g.leader()) c->n_confl = 0;
+        g.sync();
+        return violated;
+    }
+
+    // Erase everything above `target` (assignment.cpp:166-178).
+    __device__ void backjump(std::uint32_t target) {
+        if (g.leader()) {
+            const std::uint32_t cdl = c->cdl;
+            c->b[8] = target < cdl ? sl.tpos[atom_of(sl.ldec[target + 1])] : c->ts;
+        }
+        g.sync();
+        const std::uint32_t from = c->b[8], to = c->ts;
+        for (std::uint32_t i = from + g.tid(); i < to; i += g.size()) {
+            const std::uint32_t a = atom_of(sl.trail[i]);
+            const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
+            for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
+            sl.dovf[a] = 0;
+            sl.cells[a] = 0;
+            sl.tpos[a] = 0;
+            sl.reason[a] = kReasonNone;
+        }
+        g.sync();
+        if (g.leader() && target < c->cdl) {
+            c->ts = from;
+            c->cdl = target;
+        }
+        g.sync();
+    }
+
+    // ---- leader-only sequential pieces ---------------------------------------
+    __device__ void sort_by_atom(std::int32_t* v, std::uint32_t n) const {
+        // heapsort keyed by atom id (Nogood::make order; one sign per atom here)
+        auto key = [](std::int32_t x) { return atom_of(x); };
+        auto sift = [&](std::uint32_t root, std::uint32_t end) {
+            for (;;) {
+                std::uint32_t ch = 2 * root + 1;
+                if (ch >= end) return;
+                if (ch + 1 < end && key(v[ch + 1]) > key(v[ch])) ++ch;
+                if (key(v[root]) >= key(v[ch])) return;
+                const std::int32_t t = v[root]; v[root] = v[ch]; v[ch] = t;
+                root = ch;
+            }
+        };
+        for (std::uint32_t i = n / 2; i-- > 0;) sift(i, n);
+        for (std::uint32_t end = n; end > 1; --end) {
+            const std::int32_t t = v[0]; v[0] = v[end - 1]; v[end - 1] = t;
+            sift(0, end - 1);
+        }
+    }
+
+    // NogoodStore::add_learned (nogood_store.cpp:81-107). Returns id or -1.
+    __device__ std::int32_t add_learned(const std::int32_t* lits, std::uint32_t len, bool count_capacity = true) {
+        if (count_capacity && c->learned_n >= C.learned_capacity) {
+            c->status = kErrCapacity;
+            return -1;
+        }
+        if (c->learned_n >= K.lcap || c->lpool_used + len > K.lpool) {
+            c->status = kErrArena;
+            return -1;
+        }
+        // duplicate census (learned_seen_, nogood_store.cpp:87-89)
+        unsigned long long h = 0xcbf29ce484222325ull;
+        for (std::uint32_t k = 0; k < len; ++k) h = (h ^ static_cast<std::uint32_t>(lits[k])) * 0x100000001b3ull;
+        const std::uint32_t mask = K.dupcap - 1;
+        const unsigned long long tag = static_cast<unsigned long long>(c->epoch) << 32;
+        for (std::uint32_t at = static_cast<std::uint32_t>(h ^ (h >> 32)) & mask;; at = (at + 1) & mask) {
+            const unsigned long long ent = sl.dup[at];
+            if ((ent >> 32) != c->epoch || ent == 0) {
+                sl.dup[at] = tag | (c->learned_n + 1);
+                break;
+            }
+            const std::uint32_t other = static_cast<std::uint32_t>(ent) - 1;
+            const std::uint32_t olo = sl.loff[other], olen = sl.loff[other + 1] - olo;
+            bool same = olen == len;
+            for (std::uint32_t k = 0; same && k < len; ++k) same = sl.lpool[olo + k] == lits[k];
+            if (same) {
+                c->st.duplicate_learned += 1;
+                break;
+            }
+        }
+        const std::uint32_t k = c->learned_n;
+        const std::uint32_t id = S.N + k;
+        const std::uint32_t lo = c->lpool_used;
+        for (std::uint32_t j = 0; j < len; ++j) sl.lpool[lo + j] = lits[j];
+        sl.loff[k + 1] = lo + len;
+        c->lpool_used = lo + len;
+        const std::uint32_t cls = len >= 4 ? 3u : len - 1u;
+        for (std::uint32_t j = 0; j < len; ++j) {
+            const std::uint32_t li = lidx(lits[j]);
+            std::uint32_t* h3 = sl.lhdr + 3 * (li * 4 + cls);
+            if (h3[1] == h3[2]) {
+                const std::uint32_t ncap = h3[2] ? 2 * h3[2] : 4u;
+                if (c->locc_used + ncap > K.larena) {
+                    c->status = kErrArena;
+                    return -1;
+                }
+                const std::uint32_t np = c->locc_used;
+                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena[np + q] = sl.larena[h3[0] + q];
+                h3[0] = np;
+                h3[2] = ncap;
+                c->locc_used = np + ncap;
+            }
+            sl.larena[h3[0] + h3[1]] = static_cast<std::int32_t>(id);
+            h3[1] += 1;
+            sl.ltot[li] += 1;
+        }
+        if (len == 1) sl.lunits[c->lunits_n++] = static_cast<std::int32_t>(id);
+        c->learned_n = k + 1;
+        return static_cast<std::int32_t>(id);
+    }
+
+    // Driver::try_assert (solver.cpp:117-146) on the current frontier.
+    __device__ void try_assert(std::uint32_t id) {
+        std::uint32_t len;
+        const std::int32_t* L = lits_of(id, len);
+        std::int32_t rem = 0;
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::int32_t l = lit_at(L, k, id);
+            const std::int32_t cv = sl.cells[atom_of(l)];
+            if (cv == 0) {
+                if (rem != 0) return;
+                rem = l;
+            } else if ((cv > 0) != (l > 0)) {
+                return;
+            }
+        }
+        if (rem == 0) {
+            sl.pending[c->n_pending++] = static_cast<std::int32_t>(id);
+            return;
+        }
+        if (!may_assert(guard_of(id), -rem)) return;
+        const std::int32_t lit = -rem;
+        const std::uint32_t a = atom_of(lit), cdl = c->cdl;
+        write_deps_from(L, len, id, a, cdl);
+        sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl);
+        sl.reason[a] = static_cast<std::int32_t>(id);
+        sl.tpos[a] = c->ts;
+        sl.trail[c->ts++] = lit;
+        sl.fr[c->cur][c->F++] = lit;
+        c->st.propagations += 1;
+    }
+
+    __device__ bool is_unit_now(std::uint32_t id) const {
+        std::uint32_t len, nfree = 0;
+        const std::int32_t* L = lits_of(id, len);
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::int32_t l = lit_at(L, k, id);
+            const std::int32_t cv = sl.cells[atom_of(l)];
+            if (cv == 0) ++nfree;
+            else if ((cv > 0) != (l > 0)) return false;
+        }
+        return nfree == 1;
+    }
+
+    // fwd_learning (learn.cpp:106-142). Writes the learned literals to out and
+    // returns their count, or 0xffffffff on a Deps overflow (-> res fallback).
+    __device__ std::uint32_t fwd(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+        std::uint32_t len;
+        const std::int32_t* L = lits_of(delta, len);
+        std::uint32_t cl = 0;
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::uint32_t a = atom_of(lit_at(L, k, delta));
+            const std::uint32_t lv = lvl_of(sl.cells[a]);
+            cl = lv > cl ? lv : cl;
+            if (sl.dovf[a]) return 0xffffffffu;
+        }
+        const std::uint32_t nw = nwords(c->cdl);
+        std::uint32_t n = 0;
+        target = 0;
+        for (std::uint32_t w = 0; w < nw; ++w) {
+            unsigned long long m = 0;
+            for (std::uint32_t k = 0; k < len; ++k) {
+                const std::uint32_t a = atom_of(lit_at(L, k, delta));
+                if (lvl_of(sl.cells[a]) > 1) m |= dep(w, a);
+            }
+            for (unsigned long long b = m; b; b &= b - 1) {
+                const std::uint32_t level = 64 * w + static_cast<std::uint32_t>(__ffsll(static_cast<long long>(b))) ;
+                out[n++] = sl.ldec[level];
+                if (level < cl && level > target) target = level;
+            }
+        }
+        if (target == 0) target = 1;
+        sort_by_atom(out, n);
+        return n;
+    }
+
+    // res_learning (learn.cpp:53-104): resolve until a positive UIP.
+    __device__ std::uint32_t res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+        std::uint32_t* mark = sl.mark;
+        const std::uint32_t stamp = ++c->stamp;
+        std::uint32_t len;
+        const std::int32_t* L = lits_of(delta, len);
+        std::uint32_t n = 0;
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::uint32_t a = atom_of(lit_at(L, k, delta));
+            mark[a] = stamp;
+            out[n++] = static_cast<std::int32_t>(a);
+        }
+        for (;;) {
+            std::uint32_t si = 0;
+            for (std::uint32_t k = 1; k < n; ++k)
+                if (sl.tpos[out[k]] > sl.tpos[out[si]]) si = k;
+            const std::uint32_t sa = static_cast<std::uint32_t>(out[si]);
+            const std::uint32_t slev = lvl_of(sl.cells[sa]);
+            std::uint32_t kappa = 0;
+            for (std::uint32_t k = 0; k < n; ++k)
+                if (k != si) { const std::uint32_t lv = lvl_of(sl.cells[out[k]]); kappa = lv > kappa ? lv : kappa; }
+            if (kappa != slev && sl.cells[sa] > 0) {
+                target = kappa > 1 ? kappa : 1;
+                for (std::uint32_t k = 0; k < n; ++k) {
+                    const std::int32_t a = out[k];
+                    out[k] = sl.cells[a] > 0 ? a : -a;
+                }
+                sort_by_atom(out, n);
+                return n;
+            }
+            const std::int32_t r = sl.reason[sa];
+            out[si] = out[--n];
+            mark[sa] = 0;
+            if (r >= 0) {
+                std::uint32_t elen;
+                const std::int32_t* E = lits_of(static_cast<std::uint32_t>(r), elen);
+                for (std::uint32_t k = 0; k < elen; ++k) {
+                    const std::uint32_t a = atom_of(lit_at(E, k, static_cast<std::uint32_t>(r)));
+                    if (a == sa || mark[a] == stamp) continue;
+                    mark[a] = stamp;
+                    out[n++] = static_cast<std::int32_t>(a);
+                }
+            } else if (r == kReasonCompletion) {
+                for (std::uint32_t lv = 2; lv <= c->cdl; ++lv) {
+                    const std::uint32_t a = atom_of(sl.ldec[lv]);
+                    if (a == sa || mark[a] == stamp) continue;
+                    mark[a] = stamp;
+                    out[n++] = static_cast<std::int32_t>(a);
+                }
+            } else {
+                c->status = kErrLogic;
+                return 0;
+            }
+        }
+    }
+
+    __device__ void bump_activity(const std::int32_t* lits, std::uint32_t n) {
+        if (C.heur != 2) return;
+        for (std::uint32_t k = 0; k < n; ++k) sl.act[atom_of(lits[k])] += c->act_inc;
+    }
+
+    // Driver::handle_conflicts (solver.cpp:161-214), leader part. Returns
+    // 0 = exhausted, 1 = continue; writes the backjump plan to c->b.
+    __device__ void analyze_and_learn() {
+        c->st.conflicts += 1;
+        c->b[0] = 0;
+        if (c->cdl == 1) return;  // nothing to revise
+        const std::uint32_t nc = c->n_confl;
+        // select conflicts: min (length, id); fanout K in fwd mode (learn.cpp:148-157)
+        const std::uint32_t K2 = (C.mode == 0 && C.fanout > 1) ? C.fanout : 1u;
+        std::int32_t* added = sl.scratch;            // ids of added nogoods
+        std::int32_t* levels = sl.scratch + 64;      // their backjump levels
+        std::int32_t* buf = sl.scratch + 128;        // learned literal buffer
+        std::uint32_t n_sel = 0;
+        unsigned long long prev = 0;
+        bool have_prev = false;
+        std::uint32_t bj = 0xffffffffu;
+        while (n_sel < K2) {
+            unsigned long long best = ~0ull;
+            for (std::uint32_t i = 0; i < nc; ++i) {
+                const std::uint32_t id = static_cast<std::uint32_t>(sl.confl[i]);
+                const unsigned long long key = (static_cast<unsigned long long>(length_of(id)) << 32) | id;
+                if ((!have_prev || key > prev) && key < best) best = key;
+            }
+            if (best == ~0ull) break;
+            prev = best;
+            have_prev = true;
+            const std::uint32_t delta = static_cast<std::uint32_t>(best);
+            std::uint32_t target = 1, n = 0xffffffffu;
+            std::uint32_t used = 1;  // 0 fwd, 1 res
+            if (C.mode == 0) {
+                n = fwd(delta, buf, target);
+                if (n != 0xffffffffu) used = 0;
+            }
+            if (n == 0xffffffffu) {
+                n = res(delta, buf, target);
+                if (c->status != kRunning) return;
+            }
+            // structural self-checks (solver.cpp:171-186)
+            if (used == 1) {
+                std::uint32_t cl = 0, at = 0;
+                for (std::uint32_t k = 0; k < n; ++k) { const std::uint32_t lv = lvl_of(sl.cells[atom_of(buf[k])]); cl = lv > cl ? lv : cl; }
+                for (std::uint32_t k = 0; k < n; ++k) at += lvl_of(sl.cells[atom_of(buf[k])]) == cl;
+                if (at != 1) c->st.uip_check_failures += 1;
+                c->st.res_learned += 1;
+                if (C.mode == 0) c->st.fwd_fallbacks += 1;
+            } else {
+                for (std::uint32_t k = 0; k < n; ++k)
+                    if (sl.reason[atom_of(buf[k])] != kReasonDecision) c->st.fwd_decision_only_failures += 1;
+                c->st.fwd_learned += 1;
+            }
+            const std::int32_t id = add_learned(buf, n);
+            if (id < 0) return;
+            added[n_sel] = id;
+            levels[n_sel] = static_cast<std::int32_t>(target);
+            ++n_sel;
+            bj = target < bj ? target : bj;
+            c->st.learned_count += 1;
+            c->st.learned_length_sum += n;
+            bump_activity(buf, n);
+            if (C.trace && c->n_trace < K.tcap)
+                sl.tbuf[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
+        }
+        // Heuristic::on_conflict (decide.cpp:34-41)
+        if (C.heur == 2) {
+            c->act_inc /= C.decay;
+            if (c->act_inc > 1e100) {
+                for (std::uint32_t a = 0; a <= S.A; ++a) sl.act[a] *= 1e-100;
+                c->act_inc *= 1e-100;
+            }
+        }
+        const bool restart = C.restarts && c->st.conflicts - c->conflicts_at_restart >= c->restart_threshold;
+        if (restart) {
+            c->st.restarts += 1;
+            c->conflicts_at_restart = c->st.conflicts;
+            c->restart_threshold = static_cast<unsigned long long>(
+                ceil(static_cast<double>(c->restart_threshold) * C.restart_factor));
+        }
+        c->b[0] = 1;
+        c->b[1] = restart ? 1u : 0u;
+        c->b[2] = restart ? 1u : bj;
+        c->b[3] = n_sel;
+        c->F = 0;
+        c->n_confl = 0;
+    }
+
+    __device__ bool handle_conflicts() {
+        if (g.leader()) analyze_and_learn();
+        g.sync();
+        if (c->status != kRunning) return false;
+        if (c->b[0] == 0) return false;
+        const bool restart = c->b[1] != 0;
+        const std::uint32_t target = c->b[2];
+        backjump(target);
+        if (restart) initial_propagation(false);
+        if (g.leader()) {
+            const std::uint32_t n_sel = c->b[3];
+            const std::int32_t* added = sl.scratch;
+            const std::int32_t* levels = sl.scratch + 64;
+            if (!restart)
+                for (std::uint32_t i = 0; i < n_sel; ++i)
+                    if (static_cast<std::uint32_t>(levels[i]) == target && !is_unit_now(static_cast<std::uint32_t>(added[i])))
+                        c->st.asserting_failures += 1;
+            for (std::uint32_t i = 0; i < n_sel; ++i) try_assert(static_cast<std::uint32_t>(added[i]));
+        }
+        g.sync();
+        return true;
+    }
+
+    __device__ double score(std::uint32_t head) const {
+        if (C.heur == 2) return sl.act[head];
+        if (C.heur == 0) return static_cast<double>(occ_total(2 * head) + occ_total(2 * head + 1));
+        double s = 0.0;  // Jeroslow-Wang, summed in the reference's list order
+        for (std::uint32_t li = 2 * head; li <= 2 * head + 1; ++li)
+            for (std::uint32_t cl = 0; cl < 4; ++cl) {
+                const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
+                for (std::uint32_t j = lo; j < hi; ++j)
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ_ids + j)))));
+                const std::uint32_t* h = sl.lhdr + 3 * (li * 4 + cl);
+                for (std::uint32_t j = 0; j < h[1]; ++j)
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena[h[0] + j]))));
+            }
+        return s;
+    }
+
+    // decide (decide.cpp:107-122) or complete_assignment (decide.cpp:124-135)
+    __device__ void decide_or_complete() {
+        double best = -1.0;
+        std::uint32_t bi = 0xffffffffu;
+        for (std::uint32_t r = g.tid(); r < S.R; r += g.size()) {
+            const uint4 ru = __ldg(S.rules + r);
+            if (ru.w >> 31) continue;
+            const std::uint32_t n = ru.w & 0x7fffffffu;
+            if (sl.cells[ru.x] != 0) continue;
+            if (ru.z != 0 && sl.cells[ru.z] <= 0) continue;
+            if (n != 0 && sl.cells[n] < 0) continue;
+            const double s = score(ru.x);
+            if (better(s, r, best, bi)) { best = s; bi = r; }
+        }
+        g.argmax(best, bi);
+        if (bi != 0xffffffffu) {
+            if (g.leader()) {
+                const std::uint32_t b = __ldg(S.rules + bi).y;
+                const std::uint32_t cdl = ++c->cdl;
+                sl.ldec[cdl] = static_cast<std::int32_t>(b);
+                sl.cells[b] = static_cast<std::int32_t>(cdl);
+                sl.tpos[b] = c->ts;
+                sl.trail[c->ts++] = static_cast<std::int32_t>(b);
+                sl.reason[b] = kReasonDecision;
+                const std::uint32_t bit = cdl - 1;
+                if (bit >= 64 * C.W) sl.dovf[b] = 1;
+                else dep(bit / 64, b) |= 1ull << (bit % 64);
+                c->st.decisions += 1;
+                sl.fr[c->cur][0] = static_cast<std::int32_t>(b);
+                c->F = 1;
+            }
+            g.sync();
+            return;
+        }
+        // complete: falsify open program atoms in atom order at cdl
+        const std::uint32_t cdl = c->cdl, ts0 = c->ts, cur = c->cur, np = S.n_prog;
+        const std::uint32_t nw = nwords(cdl);
+        const std::uint32_t hi = (cdl - 1 < 64 * C.W) ? cdl - 1 : 64 * C.W - 1;  // top bit index set
+        const std::uint8_t ovf = (cdl - 1 >= 64 * C.W) ? 1 : 0;
+        unsigned long long carry = 0;
+        for (std::uint32_t base = 0; base < np; base += g.size()) {
+            const std::uint32_t a = base + g.tid() + 1;
+            const bool open = a <= np && sl.cells[a] == 0;
+            unsigned long long tot;
+            const std::uint32_t r = static_cast<std::uint32_t>(g.scan(open ? 1ull : 0ull, tot) + carry);
+            if (open) {
+                sl.cells[a] = -static_cast<std::int32_t>(cdl);
+                sl.reason[a] = kReasonCompletion;
+                for (std::uint32_t w = 0; w < nw; ++w) {
+                    unsigned long long m = 0;
+                    if (cdl >= 2) {
+                        const std::uint32_t lo_b = w * 64, hi_b = w * 64 + 63;
+                        const std::uint32_t from = lo_b > 1 ? lo_b : 1, to = hi_b < hi ? hi_b : hi;
+                        if (from <= to) {
+                            const std::uint32_t cnt = to - from + 1;
+                            m = (cnt == 64 ? ~0ull : ((1ull << cnt) - 1)) << (from - lo_b);
+                        }
+                    }
+                    dep(w, a) = m;
+                }
+                sl.dovf[a] = ovf;
+                sl.tpos[a] = ts0 + r;
+                sl.trail[ts0 + r] = -static_cast<std::int32_t>(a);
+                sl.fr[cur][r] = -static_cast<std::int32_t>(a);
+            }
+            carry += tot;
+        }
+        g.sync();
+        if (g.leader()) {
+            c->ts = ts0 + static_cast<std::uint32_t>(carry);
+            c->F = static_cast<std::uint32_t>(carry);
+        }
+        g.sync();
+    }
+
+    __device__ void record_model(std::uint32_t cube) {
+        const std::uint32_t m = c->n_mbuf, words = K.mwords;
+        for (std::uint32_t w = g.tid(); w < words; w += g.size()) {
+            std::uint32_t bits = 0;
+            for (std::uint32_t b = 0; b < 32; ++b) {
+                const std::uint32_t a = 32 * w + b + 1;
+                if (a <= S.n_prog && sl.cells[a] > 0) bits |= 1u << b;
+            }
+            sl.mbuf[static_cast<std::size_t>(m) * words + w] = bits;
+        }
+        g.sync();
+        if (g.leader()) {
+            sl.mcube[m] = cube;
+            c->n_mbuf = m + 1;
+            c->st.models += 1;
+            c->pad0 += 1;  // models of this search
+        }
+        g.sync();
+    }
+
+    // block_current_model (solver.cpp:234-246). false = enumeration complete.
+    __device__ bool block_model() {
+        if (g.leader()) {
+            c->b[0] = 0;
+            const std::uint32_t cdl = c->cdl;
+            if (cdl > 1) {
+                std::int32_t* buf = sl.scratch + 128;
+                for (std::uint32_t lv = 2; lv <= cdl; ++lv) buf[lv - 2] = sl.ldec[lv];
+                sort_by_atom(buf, cdl - 1);
+                const std::int32_t id = add_learned(buf, cdl - 1);
+                if (id >= 0) {
+                    c->st.blocking_nogoods += 1;
+                    c->b[0] = 1;
+                    c->b[1] = static_cast<std::uint32_t>(id);
+                    c->F = 0;
+                }
+            }
+        }
+        g.sync();
+        if (c->b[0] == 0) return false;
+        const std::uint32_t id = c->b[1];
+        backjump(1);
+        if (g.leader()) try_assert(id);
+        g.sync();
+        return true;
+    }
+
+    // validate_fixpoint (propagate.cpp:251-266) for cfg.debug_validate
+    __device__ void validate() {
+        const std::uint32_t total = S.N + c->learned_n;
+        for (std::uint32_t id = g.tid(); id < total; id += g.size()) {
+            std::uint32_t len, nfree = 0, nhold = 0;
+            const std::int32_t* L = lits_of(id, len);
+            std::int32_t open = 0;
+            bool dead = false;
+            for (std::uint32_t k = 0; k < len; ++k) {
+                const std::int32_t l = lit_at(L, k, id);
+                const std::int32_t cv = sl.cells[atom_of(l)];
+                if (cv == 0) { ++nfree; open = l; }
+                else if ((cv > 0) == (l > 0)) ++nhold;
+                else dead = true;
+            }
+            if (dead) continue;
+            if (nfree == 0 || (nfree == 1 && may_assert(guard_of(id), -open))) c->status = kErrValidate;
+        }
+        for (std::uint32_t k = g.tid(); k < S.n_units; k += g.size())
+            if (!holds(-__ldg(S.units + k))) c->status = kErrValidate;
+        g.sync();
+    }
+
+    // Fresh search in this slot: clear what the previous search touched.
+    __device__ void begin_search(std::uint32_t cube) {
+        const std::uint32_t ts = c->ts;
+        for (std::uint32_t i = g.tid(); i < ts; i += g.size()) {
+            const std::uint32_t a = atom_of(sl.trail[i]);
+            const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
+            for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
+            sl.dovf[a] = 0;
+            sl.cells[a] = 0;
+            sl.tpos[a] = 0;
+            sl.reason[a] = kReasonNone;
+        }
+        const std::uint32_t keys = (2 * S.A + 2) * 4;
+        if (c->learned_n > 0 || c->epoch == 0) {
+            for (std::uint32_t i = g.tid(); i < 3 * keys; i += g.size()) sl.lhdr[i] = 0;
+            for (std::uint32_t i = g.tid(); i < 2 * S.A + 2; i += g.size()) sl.ltot[i] = 0;
+        }
+        if (C.heur == 2)
+            for (std::uint32_t i = g.tid(); i <= S.A; i += g.size()) sl.act[i] = 0.0;
+        g.sync();
+        if (g.leader()) {
+            c->cdl = 1;
+            c->ts = 0;
+            c->F = 0;
+            c->cur = 0;
+            c->T = 0;
+            c->n_props = c->n_confl = c->n_pending = 0;
+            c->learned_n = c->lpool_used = c->locc_used = c->lunits_n = 0;
+            sl.loff[0] = 0;
+            c->cube = cube;
+            c->epoch += 1;
+            c->pad0 = 0;
+            c->restart_threshold = C.restart_base;
+            c->conflicts_at_restart = c->st.conflicts;
+            c->act_inc = 1.0;
+            c->st.searches += 1;
+            // cube constraints enter as unit nogoods ahead of any learned one
+            for (std::uint32_t k = 0; k < C.cube_width; ++k) {
+                const std::int32_t l = __ldg(S.cubes + static_cast<std::size_t>(cube) * C.cube_width + k);
+                if (l != 0) add_learned(&l, 1, false);
+            }
+            c->phase = kInit;
+        }
+        g.sync();
+    }
+
+    // The Alg. 1 state machine (solver.cpp:248-303). Returns when the search
+    // is finished (phase kFinished), on error, or when it must yield.
+    __device__ void run() {
+        for (;;) {
+            const std::uint32_t ph = c->phase;
+            if (c->status != kRunning) return;
+            g.sync();
+            if (ph == kInit) {
+                const bool violated = initial_propagation(true);
+                if (g.leader()) {
+                    c->n_confl = 0;
+                    c->phase = violated ? kFinished : kLoop;
+                }
+                g.sync();
+                continue;
+            }
+            if (ph == kAfterModel) {
+                if (C.max_models != 0 && c->pad0 >= C.max_models) {
+                    if (g.leader()) c->phase = kFinished;
+                    g.sync();
+                    return;
+                }
+                const bool more = block_model();
+                if (c->status != kRunning) return;
+                if (g.leader()) c->phase = more ? kLoop : kFinished;
+                g.sync();
+                if (!more) return;
+                continue;
+            }
+            if (ph != kLoop) return;
+            // yield check at the loop top (clean state)
+            if (g.leader()) {
+                bool y = sh->stop != 0;
+                if (c->n_mbuf >= K.mcap || (C.trace && c->n_trace + 64 > K.tcap)) {
+                    y = true;
+                    sh->stop = 1;
+                }
+                if (C.slice_ns && gtimer() - t0 > C.slice_ns) y = true;
+                c->b[15] = y ? 1u : 0u;
+            }
+            g.sync();
+            if (c->b[15]) {
+                if (g.leader()) c->status = kYield;
+                g.sync();
+                return;
+            }
+            bool conflicted;
+            if (c->n_pending == 0) {
+                conflicted = propagate(c->cdl);
+            } else {
+                if (g.leader()) {
+                    for (std::uint32_t i = 0; i < c->n_pending; ++i) sl.confl[i] = sl.pending[i];
+                    c->n_confl = c->n_pending;
+                    c->n_pending = 0;
+                }
+                g.sync();
+                conflicted = true;
+            }
+            if (conflicted) {
+                if (!handle_conflicts()) {
+                    if (c->status != kRunning) return;
+                    if (g.leader()) c->phase = kFinished;
+                    g.sync();
+                    return;
+                }
+                continue;
+            }
+            if (C.debug_validate) {
+                validate();
+                if (c->status != kRunning) return;
+            }
+            if (c->ts != S.A) {
+                decide_or_complete();
+                continue;
+            }
+            record_model(c->cube);
+            if (g.leader()) c->phase = kAfterModel;
+            g.sync();
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Kernels
+// ---------------------------------------------------------------------------
+template <class G>
+__device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh) {
+    const unsigned long long t0 = gtimer();
+    Search<G> s(g, S, C, sl, K, sh, t0);
+    for (;;) {
+        g.sync();
+        if (g.c->status != kRunning) return;
+        if (g.c->phase == kIdle || g.c->phase == kFinished) {
+            g.sync();
+            if (g.leader()) {
+                g.c->phase = kIdle;
+                g.c->b[9] = sh->stop ? 0xffffffffu : atomicAdd(&sh->cube_next, 1u);
+            }
+            g.sync();
+            const std::uint32_t cube = g.c->b[9];
+            if (cube >= C.n_cubes) {
+                if (g.leader()) g.c->status = cube == 0xffffffffu ? kYield : kDone;
+                g.sync();
+                return;
+            }
+            s.begin_search(cube);
+        }
+        s.run();
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
+                                                   Shared* sh) {
+    __shared__ Ctl ctl;
+    __shared__ unsigned long long sbuf[BS / 32 + 4];
+    __shared__ double sd[BS / 32];
+    __shared__ std::uint32_t si[BS / 32];
+    const Slot sl = slots[blockIdx.x];
+    {
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&ctl);
+        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && ctl.status == kYield) ctl.status = kRunning;
+    BlockG<BS> g{&ctl, sbuf, sd, si};
+    slot_loop(g, S, C, sl, K, sh);
+    __syncthreads();
+    {
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl);
+        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) grid_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
+                                                  Shared* sh, unsigned long long* partial, double* pd,
+                                                  std::uint32_t* pi) {
+    __shared__ unsigned long long sbuf[BS / 32 + 4];
+    __shared__ double sd[BS / 32];
+    __shared__ std::uint32_t si[BS / 32];
+    const Slot sl = slots[0];
+    GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
+    if (g.leader() && sl.ctl->status == kYield) sl.ctl->status = kRunning;
+    g.sync();
+    slot_loop(g, S, C, sl, K, sh);
+}
+
+// Low-level operations on one slot (Propagator-style API for tests and the
+// propagation microbenchmark).
+enum Op : std::uint32_t { kOpReset = 0, kOpInitial = 1, kOpPropagate = 2, kOpDecide = 3, kOpAssign = 4, kOpSeed = 5, kOpLearn = 6 };
+
+struct OpArgs {
+    std::uint32_t op;
+    std::uint32_t level;
+    std::int32_t lit;
+    std::int32_t antecedent;
+    const std::int32_t* lits;  // bulk
+    std::uint32_t n;
+    const unsigned long long* deps;  // W words for kOpAssign
+    std::uint32_t ovf;
+};
+
+template <class G>
+__device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh,
+                      const OpArgs& op) {
+    Search<G> s(g, S, C, sl, K, sh, 0);
+    Ctl* c = g.c;
+    switch (op.op) {
+        case kOpReset:
+            s.begin_search(0);
+            if (g.leader()) c->phase = kLoop;
+            g.sync();
+            break;
+        case kOpInitial: {
+            if (g.leader()) { c->F = 0; c->n_confl = 0; }
+            g.sync();
+            const bool v = s.initial_propagation(true);
+            if (g.leader()) c->b[10] = v;
+            g.sync();
+            break;
+        }
+        case kOpPropagate: {
+            if (g.leader()) c->n_confl = 0;
+            g.sync();
+            const bool v = s.propagate(op.level);
+            if (g.leader()) c->b[10] = v;
+            g.sync();
+            break;
+        }
+        case kOpDecide:  // push_decision(lit) (assignment.cpp:155-164)
+            if (g.leader()) {
+                const std::int32_t lit = op.lit;
+                const std::uint32_t a = atom_of(lit);
+                const std::uint32_t cdl = ++c->cdl;
+                sl.ldec[cdl] = lit;
+                sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl);
+                sl.tpos[a] = c->ts;
+                sl.trail[c->ts++] = lit;
+                sl.reason[a] = kReasonDecision;
+                const std::uint32_t bit = cdl - 1;
+                if (bit >= 64 * C.W) sl.dovf[a] = 1;
+                else s.dep(bit / 64, a) |= 1ull << (bit % 64);
+            }
+            g.sync();
+            break;
+        case kOpAssign:  // assign_propagated for a bulk of literals (assignment.cpp:135-144)
+            if (g.leader()) {
+                for (std::uint32_t k = 0; k < op.n; ++k) {
+                    const std::int32_t lit = op.lits[k];
+                    const std::uint32_t a = atom_of(lit);
+                    if (sl.cells[a] != 0) continue;
+                    sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(op.level) : -static_cast<std::int32_t>(op.level);
+                    sl.tpos[a] = c->ts;
+                    sl.trail[c->ts++] = lit;
+                    sl.reason[a] = op.antecedent;
+                    for (std::uint32_t w = 0; w < C.W; ++w) s.dep(w, a) = op.deps ? op.deps[w] : 0ull;
+                    sl.dovf[a] = static_cast<std::uint8_t>(op.ovf);
+                }
+            }
+            g.sync();
+            break;
+        case kOpSeed:  // frontier.last.push_back for a bulk of literals
+            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr[c->cur][c->F + k] = op.lits[k];
+            g.sync();
+            if (g.leader()) c->F += op.n;
+            g.sync();
+            break;
+        case kOpLearn:  // NogoodStore::add_learned (kNoTruth guard)
+            if (g.leader()) {
+                std::int32_t* buf = sl.scratch + 128;
+                for (std::uint32_t k = 0; k < op.n; ++k) buf[k] = op.lits[k];
+                s.sort_by_atom(buf, op.n);
+                c->b[12] = static_cast<std::uint32_t>(s.add_learned(buf, op.n));
+            }
+            g.sync();
+            break;
+        default:
+            break;
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) op_block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
+                                                      Shared* sh, OpArgs op) {
+    __shared__ Ctl ctl;
+    __shared__ unsigned long long sbuf[BS / 32 + 4];
+    __shared__ double sd[BS / 32];
+    __shared__ std::uint32_t si[BS / 32];
+    const Slot sl = slots[0];
+    {
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&ctl);
+        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
+    }
+    __syncthreads();
+    BlockG<BS> g{&ctl, sbuf, sd, si};
+    do_op(g, S, C, sl, K, sh, op);
+    __syncthreads();
+    {
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl);
+        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
+    }
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) op_grid_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
+                                                     Shared* sh, unsigned long long* partial, double* pd,
+                                                     std::uint32_t* pi, OpArgs op) {
+    __shared__ unsigned long long sbuf[BS / 32 + 4];
+    __shared__ double sd[BS / 32];
+    __shared__ std::uint32_t si[BS / 32];
+    const Slot sl = slots[0];
+    GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
+    do_op(g, S, C, sl, K, sh, op);
+}
+
+}  // namespace yas::dev
+
+#include "engine_host.inl"

@@ -1,0 +1,145 @@
+// Device-resident solver state shared between the host launcher and the
+// sm_100a kernels. One "slot" = the complete mutable state of one search
+// (assignment, trail, Deps bitmaps, learned arena, pass scratch). The static
+// store is shared read-only by all slots.
+//
+// Everything a search needs lives in device memory, so a kernel can stop at a
+// loop boundary (model buffer full, time slice over) and a relaunch resumes
+// exactly where it stopped; this is how models/traces stream to the host.
+#pragma once
+
+#include <cstdint>
+
+namespace yas::dev {
+
+constexpr std::uint32_t kAny = 0xFFFFFFFFu;  // kAnyTruth (nogood.hpp:72)
+constexpr std::uint32_t kNone = 0u;          // kNoTruth  (nogood.hpp:73)
+
+// reason[] encoding: >= 0 is the antecedent nogood id (Reason::propagated).
+constexpr std::int32_t kReasonNone = -1;
+constexpr std::int32_t kReasonDecision = -2;
+constexpr std::int32_t kReasonUnit = -3;
+constexpr std::int32_t kReasonCompletion = -4;
+
+enum Status : std::uint32_t {
+    kRunning = 0,
+    kDone = 1,
+    kYield = 2,
+    kErrCapacity = 3,  // StoreCapacityError (nogood_store.cpp:83-85)
+    kErrArena = 4,     // device arena too small: host re-runs with more memory
+    kErrLogic = 5,     // res_learning without antecedent (learn.cpp:97-100)
+    kErrValidate = 6,  // debug_validate fixpoint check failed (solver.cpp:77-82)
+};
+
+enum Phase : std::uint32_t { kIdle = 0, kInit = 1, kLoop = 2, kAfterModel = 3, kFinished = 4 };
+
+struct Config {
+    std::uint32_t mode;  // 0 fwd, 1 res
+    std::uint32_t heur;  // 0 occ, 1 jw, 2 act
+    double decay;
+    std::uint32_t restarts;
+    std::uint32_t W;  // deps words
+    std::uint64_t restart_base;
+    double restart_factor;
+    std::uint64_t max_models;  // 0 = all
+    std::uint32_t fanout;
+    std::uint32_t debug_validate;
+    std::uint64_t learned_capacity;
+    std::uint32_t trace;
+    std::uint32_t n_cubes;
+    std::uint32_t cube_width;   // literals per cube
+    std::uint64_t slice_ns;     // time slice per launch before yielding
+};
+
+// Read-only static store + program rules (host-built, uploaded once).
+struct Static {
+    std::uint32_t A;       // total atoms (program + aux)
+    std::uint32_t n_prog;  // program atoms 1..n_prog
+    std::uint32_t N;       // static CSR nogoods
+    std::uint32_t n_units, n_uids, R;
+    const std::uint32_t* off;   // N+1
+    const std::int32_t* pool;   // literal codes
+    const std::uint32_t* guard; // N
+    const std::uint32_t* occ_off;  // (2A+2)*4+1, key = lit_index*4 + class
+    const std::int32_t* occ_ids;
+    const std::int32_t* units;     // static unit literals (nogood literal sigma)
+    const std::int32_t* uids;      // static length-1 CSR ids
+    const uint4* rules;            // (head, b, t, n | vacuous<<31)
+    const std::int32_t* cubes;     // n_cubes * cube_width nogood literals (0 = pad)
+};
+
+struct Stats {
+    unsigned long long decisions, propagations, conflicts, learned_count, learned_length_sum,
+        restarts, models, passes, duplicate_learned, blocking_nogoods, res_learned, fwd_learned,
+        fwd_fallbacks, uip_check_failures, fwd_decision_only_failures, asserting_failures,
+        checks, searches;
+};
+
+// Per-slot control block. Mirrored into shared memory by single-CTA searches.
+struct Ctl {
+    std::uint32_t phase, status;
+    std::uint32_t cdl, ts, F, cur, T, gen;
+    std::uint32_t n_props, n_confl, n_pending, n_mbuf, n_trace;
+    std::uint32_t learned_n, lpool_used, locc_used, lunits_n;
+    std::uint32_t cube, epoch, stamp, pad0;
+    unsigned long long restart_threshold, conflicts_at_restart;
+    double act_inc;
+    std::uint32_t b[16];  // leader -> group broadcast scratch
+    Stats st;
+};
+
+struct Caps {
+    std::uint32_t items;   // claim/props/confl entries (>= N + learned)
+    std::uint32_t tbits;   // expansion bitmap bits / lit_at entries
+    std::uint32_t lcap;    // learned nogoods (arena)
+    std::uint32_t lpool;   // learned literals
+    std::uint32_t larena;  // learned occurrence arena (ids)
+    std::uint32_t dupcap;  // power of two
+    std::uint32_t mcap;    // models per slot buffer
+    std::uint32_t tcap;    // trace records per slot
+    std::uint32_t mwords;  // words per model bitset
+};
+
+struct Slot {
+    Ctl* ctl;
+    std::int32_t* cells;
+    std::uint32_t* tpos;
+    std::int32_t* reason;
+    unsigned long long* deps;  // word-major: deps[w*(A+1) + atom]
+    std::uint8_t* dovf;
+    std::int32_t* trail;
+    std::int32_t* ldec;
+    std::int32_t* fr[2];
+    std::uint32_t* froff;
+    unsigned long long* claim;  // per nogood id: (~gen << 32) | min expansion index
+    unsigned long long* win;    // per atom: (~gen << 32) | (e << 1) | negative
+    int4* props;                // (id, lit, e, -)
+    std::int32_t* confl;
+    std::int32_t* pending;
+    std::uint32_t* bitmap;
+    std::int32_t* litat;
+    std::uint32_t* loff;     // lcap+1
+    std::int32_t* lpool;
+    std::uint32_t* lhdr;     // (2A+2)*4 * {ptr,size,cap}
+    std::int32_t* larena;
+    std::int32_t* lunits;
+    std::uint32_t* ltot;     // per literal index: learned occurrences
+    double* act;
+    unsigned long long* dup;
+    std::int32_t* scratch;   // >= 2*(A+2) ints
+    std::uint32_t* mark;     // A+1
+    unsigned long long* merged;  // W words
+    std::uint32_t* mbuf;     // mcap * mwords
+    std::uint32_t* mcube;    // mcap
+    uint4* tbuf;             // tcap trace records (mode, conflict id, len, backjump)
+};
+
+struct Shared {  // global (all-slot) coordination
+    std::uint32_t cube_next;
+    std::uint32_t stop;
+    std::uint32_t bar_count, bar_gen;
+    unsigned long long t_start;
+    std::uint32_t partial_pad[27];
+};
+
+}  // namespace yas::dev

@@ -1,0 +1,455 @@
+// Host side of the engine: uploads, per-slot arenas, the launch/drain loop.
+// Included at the end of engine.cu (needs the kernel templates).
+#include <chrono>
+
+namespace yas {
+
+namespace {
+
+constexpr int kBlockBS = 256;
+constexpr int kGridBS = 512;
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+T* dalloc(std::size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "cudaMalloc");
+    owned.push_back(p);
+    return static_cast<T*>(p);
+}
+
+template <class T>
+T* dupload(const std::vector<T>& v, std::vector<void*>& owned) {
+    T* p = dalloc<T>(v.size(), owned);
+    if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
+    return p;
+}
+
+std::uint32_t pow2_at_least(std::uint64_t x) {
+    std::uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// All device memory of one run: static store + S slots.
+struct Arena {
+    std::vector<void*> owned;
+    dev::Static S{};
+    dev::Caps K{};
+    std::vector<dev::Slot> slots;
+    dev::Slot* d_slots = nullptr;
+    dev::Shared* sh = nullptr;
+    unsigned long long* partial = nullptr;
+    double* pd = nullptr;
+    std::uint32_t* pi = nullptr;
+    std::uint32_t W = 16;
+    std::uint32_t A = 0;
+
+    ~Arena() {
+        for (void* p : owned) cudaFree(p);
+    }
+
+    void upload_static(const StaticStore& st, const std::vector<RuleRec>& rules, std::uint32_t n_prog,
+                       const std::vector<std::int32_t>& cubes) {
+        S.A = st.total_atoms;
+        S.n_prog = n_prog;
+        S.N = st.size();
+        S.n_units = static_cast<std::uint32_t>(st.units.size());
+        S.n_uids = static_cast<std::uint32_t>(st.unit_ids.size());
+        S.R = static_cast<std::uint32_t>(rules.size());
+        S.off = dupload(st.off, owned);
+        S.pool = dupload(st.pool, owned);
+        S.guard = dupload(st.guard, owned);
+        S.occ_off = dupload(st.occ_off, owned);
+        S.occ_ids = dupload(st.occ_ids, owned);
+        S.units = dupload(st.units, owned);
+        S.uids = dupload(st.unit_ids, owned);
+        std::vector<uint4> r(rules.size());
+        for (std::size_t i = 0; i < rules.size(); ++i) r[i] = make_uint4(rules[i].head, rules[i].b, rules[i].t, rules[i].n);
+        S.rules = dupload(r, owned);
+        S.cubes = dupload(cubes, owned);
+        A = st.total_atoms;
+    }
+
+    void alloc_slots(std::uint32_t n_slots, std::uint32_t W_, std::uint32_t lcap, std::uint32_t lpool,
+                     std::uint32_t mcap, std::uint32_t tcap, std::uint32_t cube_width, std::uint32_t grid_blocks) {
+        W = W_;
+        const std::size_t A1 = static_cast<std::size_t>(A) + 1;
+        const std::size_t keys = (2 * static_cast<std::size_t>(A) + 2) * 4;
+        K.lcap = lcap + cube_width + 1;
+        K.lpool = lpool + cube_width + 1;
+        K.larena = 4 * K.lpool + 64;
+        K.items = S.N + K.lcap + S.n_units + 64;
+        K.dupcap = pow2_at_least(2ull * K.lcap + 2);
+        K.mcap = mcap;
+        K.tcap = tcap;
+        K.mwords = (S.n_prog + 31) / 32 ? (S.n_prog + 31) / 32 : 1;
+        slots.resize(n_slots);
+        auto each = [&](auto* base, std::size_t per, std::uint32_t s) { return base + per * s; };
+        // per-array bases for all slots
+        const std::size_t ns = n_slots;
+        auto* ctl = dalloc<dev::Ctl>(ns, owned);
+        auto* cells = dalloc<std::int32_t>(ns * A1, owned);
+        auto* tpos = dalloc<std::uint32_t>(ns * A1, owned);
+        auto* reason = dalloc<std::int32_t>(ns * A1, owned);
+        auto* deps = dalloc<unsigned long long>(ns * W * A1, owned);
+        auto* dovf = dalloc<std::uint8_t>(ns * A1, owned);
+        auto* trail = dalloc<std::int32_t>(ns * A1, owned);
+        auto* ldec = dalloc<std::int32_t>(ns * (A1 + 1), owned);
+        auto* fr0 = dalloc<std::int32_t>(ns * A1, owned);
+        auto* fr1 = dalloc<std::int32_t>(ns * A1, owned);
+        auto* froff = dalloc<std::uint32_t>(ns * (A1 + 1), owned);
+        auto* claim = dalloc<unsigned long long>(ns * K.items, owned);
+        auto* win = dalloc<unsigned long long>(ns * A1, owned);
+        auto* props = dalloc<int4>(ns * K.items, owned);
+        auto* confl = dalloc<std::int32_t>(ns * K.items, owned);
+        auto* pending = dalloc<std::int32_t>(ns * 64, owned);
+        auto* loff = dalloc<std::uint32_t>(ns * (K.lcap + 1), owned);
+        auto* lpoolp = dalloc<std::int32_t>(ns * K.lpool, owned);
+        auto* lhdr = dalloc<std::uint32_t>(ns * keys * 3, owned);
+        auto* larena = dalloc<std::int32_t>(ns * K.larena, owned);
+        auto* lunits = dalloc<std::int32_t>(ns * K.lcap, owned);
+        auto* ltot = dalloc<std::uint32_t>(ns * (2 * A1), owned);
+        auto* act = dalloc<double>(ns * A1, owned);
+        auto* dup = dalloc<unsigned long long>(ns * K.dupcap, owned);
+        auto* scratch = dalloc<std::int32_t>(ns * (A1 + 256), owned);
+        auto* mark = dalloc<std::uint32_t>(ns * A1, owned);
+        auto* merged = dalloc<unsigned long long>(ns * W, owned);
+        auto* mbuf = dalloc<std::uint32_t>(ns * static_cast<std::size_t>(mcap) * K.mwords, owned);
+        auto* mcube = dalloc<std::uint32_t>(ns * mcap, owned);
+        auto* tbuf = dalloc<uint4>(ns * tcap, owned);
+        // expansion bitmap: bounded by the literal occurrences of the store
+        // (static + learned) and by the initial-propagation item count.
+        std::uint64_t tbits = std::max<std::uint64_t>(pool_size_ + K.lpool, S.n_units + S.n_uids + K.lcap) + 64;
+        tbits = (tbits + 31) / 32 * 32;
+        K.tbits = static_cast<std::uint32_t>(tbits);
+        auto* bitmap = dalloc<std::uint32_t>(ns * (tbits / 32), owned);
+        auto* litat = dalloc<std::int32_t>(ns * tbits, owned);
+
+        ck(cudaMemset(ctl, 0, ns * sizeof(dev::Ctl)), "memset");
+        ck(cudaMemset(cells, 0, ns * A1 * 4), "memset");
+        ck(cudaMemset(tpos, 0, ns * A1 * 4), "memset");
+        ck(cudaMemset(reason, 0xFF, ns * A1 * 4), "memset");
+        ck(cudaMemset(deps, 0, ns * W * A1 * 8), "memset");
+        ck(cudaMemset(dovf, 0, ns * A1), "memset");
+        ck(cudaMemset(claim, 0xFF, ns * K.items * 8), "memset");
+        ck(cudaMemset(win, 0xFF, ns * A1 * 8), "memset");
+        ck(cudaMemset(bitmap, 0, ns * (tbits / 32) * 4), "memset");
+        ck(cudaMemset(loff, 0, ns * (K.lcap + 1) * 4), "memset");
+        ck(cudaMemset(lhdr, 0, ns * keys * 3 * 4), "memset");
+        ck(cudaMemset(ltot, 0, ns * 2 * A1 * 4), "memset");
+        ck(cudaMemset(act, 0, ns * A1 * 8), "memset");
+        ck(cudaMemset(dup, 0, ns * static_cast<std::size_t>(K.dupcap) * 8), "memset");
+        ck(cudaMemset(mark, 0, ns * A1 * 4), "memset");
+
+        for (std::uint32_t s = 0; s < n_slots; ++s) {
+            dev::Slot& q = slots[s];
+            q.ctl = ctl + s;
+            q.cells = each(cells, A1, s);
+            q.tpos = each(tpos, A1, s);
+            q.reason = each(reason, A1, s);
+            q.deps = each(deps, W * A1, s);
+            q.dovf = each(dovf, A1, s);
+            q.trail = each(trail, A1, s);
+            q.ldec = each(ldec, A1 + 1, s);
+            q.fr[0] = each(fr0, A1, s);
+            q.fr[1] = each(fr1, A1, s);
+            q.froff = each(froff, A1 + 1, s);
+            q.claim = each(claim, K.items, s);
+            q.win = each(win, A1, s);
+            q.props = each(props, K.items, s);
+            q.confl = each(confl, K.items, s);
+            q.pending = each(pending, 64, s);
+            q.bitmap = each(bitmap, tbits / 32, s);
+            q.litat = each(litat, tbits, s);
+            q.loff = each(loff, K.lcap + 1, s);
+            q.lpool = each(lpoolp, K.lpool, s);
+            q.lhdr = each(lhdr, keys * 3, s);
+            q.larena = each(larena, K.larena, s);
+            q.lunits = each(lunits, K.lcap, s);
+            q.ltot = each(ltot, 2 * A1, s);
+            q.act = each(act, A1, s);
+            q.dup = each(dup, K.dupcap, s);
+            q.scratch = each(scratch, A1 + 256, s);
+            q.mark = each(mark, A1, s);
+            q.merged = each(merged, W, s);
+            q.mbuf = each(mbuf, static_cast<std::size_t>(mcap) * K.mwords, s);
+            q.mcube = each(mcube, mcap, s);
+            q.tbuf = each(tbuf, tcap, s);
+        }
+        d_slots = dupload(slots, owned);
+        sh = dalloc<dev::Shared>(1, owned);
+        ck(cudaMemset(sh, 0, sizeof(dev::Shared)), "memset");
+        const std::uint32_t gb = grid_blocks ? grid_blocks : 1;
+        partial = dalloc<unsigned long long>(2 * gb, owned);
+        pd = dalloc<double>(gb, owned);
+        pi = dalloc<std::uint32_t>(gb, owned);
+    }
+
+    std::size_t pool_size_ = 0;
+};
+
+std::uint32_t grid_blocks_for(int device) {
+    int sms = 0, per = 0;
+    ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
+    ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, dev::grid_kernel<kGridBS>, kGridBS, 0), "occupancy");
+    if (per < 1) per = 1;
+    return static_cast<std::uint32_t>(sms) * 1u;  // one CTA per SM: cheapest grid barrier
+}
+
+}  // namespace
+
+std::string device_name(int device) {
+    cudaDeviceProp p{};
+    if (cudaGetDeviceProperties(&p, device) != cudaSuccess) return "unavailable";
+    return p.name;
+}
+
+EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, const EngineOptions& opt,
+                          const std::vector<std::int32_t>& cubes, std::uint32_t n_cubes,
+                          std::uint32_t cube_width, const EngineCallbacks& cb) {
+    ck(cudaSetDevice(opt.device), "cudaSetDevice");
+    const auto w0 = std::chrono::steady_clock::now();
+    EngineResult res;
+    Arena ar;
+    ar.pool_size_ = prog.store->pool.size();
+    ar.upload_static(*prog.store, prog.rules, prog.n_prog, cubes);
+    const std::uint32_t gblocks = opt.grid ? grid_blocks_for(opt.device) : 0;
+    const std::uint32_t n_slots = opt.grid ? 1u : std::max<std::uint32_t>(1, std::min(opt.slots, n_cubes));
+    ar.alloc_slots(n_slots, cfg_in.W, opt.lcap, opt.lpool, opt.mcap, opt.tcap, cube_width, gblocks);
+    dev::Config cfg = cfg_in;
+    cfg.n_cubes = n_cubes;
+    cfg.cube_width = cube_width;
+    cfg.slice_ns = static_cast<std::uint64_t>(opt.slice_ms * 1e6);
+
+    cudaEvent_t e0, e1;
+    ck(cudaEventCreate(&e0), "event");
+    ck(cudaEventCreate(&e1), "event");
+    std::vector<dev::Ctl> ctl(n_slots);
+    std::vector<std::uint32_t> mb, mc;
+    bool stop_early = false;
+    for (;;) {
+        ck(cudaEventRecord(e0), "record");
+        if (opt.grid) {
+            void* args[] = {&ar.S, &cfg, &ar.d_slots, &ar.K, &ar.sh, &ar.partial, &ar.pd, &ar.pi};
+            ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::grid_kernel<kGridBS>), dim3(gblocks),
+                                           dim3(kGridBS), args, 0, nullptr),
+               "grid launch");
+        } else {
+            dev::block_kernel<kBlockBS><<<n_slots, kBlockBS>>>(ar.S, cfg, ar.d_slots, ar.K, ar.sh);
+            ck(cudaGetLastError(), "block launch");
+        }
+        ck(cudaEventRecord(e1), "record");
+        ck(cudaEventSynchronize(e1), "kernel");
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        res.device_ms += ms;
+        ++res.launches;
+        ck(cudaMemcpy(ctl.data(), ar.slots[0].ctl, n_slots * sizeof(dev::Ctl), cudaMemcpyDeviceToHost), "ctl");
+        bool more = false;
+        std::uint32_t err = dev::kDone;
+        for (std::uint32_t s = 0; s < n_slots; ++s) {
+            dev::Ctl& c = ctl[s];
+            if (c.n_mbuf) {
+                mb.resize(static_cast<std::size_t>(c.n_mbuf) * ar.K.mwords);
+                mc.resize(c.n_mbuf);
+                ck(cudaMemcpy(mb.data(), ar.slots[s].mbuf, mb.size() * 4, cudaMemcpyDeviceToHost), "models");
+                ck(cudaMemcpy(mc.data(), ar.slots[s].mcube, mc.size() * 4, cudaMemcpyDeviceToHost), "models");
+                for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
+                    EngineModel em;
+                    em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(m) * ar.K.mwords,
+                                   mb.begin() + static_cast<std::ptrdiff_t>(m + 1) * ar.K.mwords);
+                    em.cube = mc[m];
+                    if (cb.on_model && !cb.on_model(em)) stop_early = true;
+                }
+                c.n_mbuf = 0;
+            }
+            if (c.n_trace) {
+                std::vector<uint4> tb(c.n_trace);
+                ck(cudaMemcpy(tb.data(), ar.slots[s].tbuf, tb.size() * sizeof(uint4), cudaMemcpyDeviceToHost), "trace");
+                if (cb.on_trace)
+                    for (const uint4& t : tb) cb.on_trace(t.x, static_cast<std::int32_t>(t.y), t.z, t.w);
+                c.n_trace = 0;
+            }
+            if (c.status == dev::kYield) more = true;
+            else if (c.status != dev::kDone && c.status != dev::kRunning) err = c.status;
+        }
+        if (err != dev::kDone) {
+            res.status = err;
+            break;
+        }
+        if (!more || stop_early) break;
+        ck(cudaMemcpy(ar.slots[0].ctl, ctl.data(), n_slots * sizeof(dev::Ctl), cudaMemcpyHostToDevice), "ctl");
+        ck(cudaMemset(&ar.sh->stop, 0, sizeof(std::uint32_t)), "stop");
+    }
+    dev::Stats tot{};
+    auto add = [](dev::Stats& a, const dev::Stats& b) {
+        const unsigned long long* pb = &b.decisions;
+        unsigned long long* pa = &a.decisions;
+        for (std::size_t i = 0; i < sizeof(dev::Stats) / 8; ++i) pa[i] += pb[i];
+    };
+    for (const dev::Ctl& c : ctl) add(tot, c.st);
+    res.stats = tot;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    res.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+    return res;
+}
+
+// ---------------------------------------------------------------------------
+// Session
+// ---------------------------------------------------------------------------
+struct Session::Impl {
+    Arena ar;
+    dev::Config cfg{};
+    bool grid = false;
+    std::uint32_t gblocks = 0;
+    int device = 0;
+    cudaEvent_t e0{}, e1{};
+};
+
+Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, int device, std::uint32_t lcap,
+                 std::uint32_t lpool)
+    : impl_(new Impl), W_(deps_words) {
+    ck(cudaSetDevice(device), "cudaSetDevice");
+    impl_->device = device;
+    impl_->grid = grid;
+    impl_->ar.pool_size_ = store.pool.size();
+    impl_->ar.upload_static(store, {}, 0, {});
+    impl_->gblocks = grid ? grid_blocks_for(device) : 0;
+    impl_->ar.alloc_slots(1, deps_words, lcap, lpool, 16, 128, 0, impl_->gblocks);
+    dev::Config& c = impl_->cfg;
+    c.W = deps_words;
+    c.decay = 0.95;
+    c.restart_base = 100;
+    c.restart_factor = 1.5;
+    c.fanout = 1;
+    c.learned_capacity = ~0ull;
+    c.n_cubes = 1;
+    ck(cudaEventCreate(&impl_->e0), "event");
+    ck(cudaEventCreate(&impl_->e1), "event");
+    reset();
+}
+
+Session::~Session() {
+    cudaEventDestroy(impl_->e0);
+    cudaEventDestroy(impl_->e1);
+}
+
+namespace {
+void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
+    cudaEventRecord(im.e0);
+    if (im.grid) {
+        dev::OpArgs o = op;
+        void* args[] = {&im.ar.S, &im.cfg, &im.ar.d_slots, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &o};
+        ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::op_grid_kernel<kGridBS>), dim3(im.gblocks),
+                                       dim3(kGridBS), args, 0, nullptr),
+           "op grid launch");
+    } else {
+        dev::op_block_kernel<kBlockBS><<<1, kBlockBS>>>(im.ar.S, im.cfg, im.ar.d_slots, im.ar.K, im.ar.sh, op);
+        ck(cudaGetLastError(), "op launch");
+    }
+    cudaEventRecord(im.e1);
+    ck(cudaEventSynchronize(im.e1), "op kernel");
+    if (ms) cudaEventElapsedTime(ms, im.e0, im.e1);
+}
+}  // namespace
+
+void Session::reset() {
+    dev::OpArgs op{};
+    op.op = dev::kOpReset;
+    run_op(*impl_, op, nullptr);
+}
+
+bool Session::initial_propagation() {
+    dev::OpArgs op{};
+    op.op = dev::kOpInitial;
+    run_op(*impl_, op, &last_ms_);
+    return ctl().b[10] != 0;
+}
+
+bool Session::propagate(std::uint32_t level) {
+    dev::OpArgs op{};
+    op.op = dev::kOpPropagate;
+    op.level = level;
+    run_op(*impl_, op, &last_ms_);
+    return ctl().b[10] != 0;
+}
+
+void Session::push_decision(std::int32_t lit) {
+    dev::OpArgs op{};
+    op.op = dev::kOpDecide;
+    op.lit = lit;
+    run_op(*impl_, op, nullptr);
+}
+
+void Session::assign(const std::vector<std::int32_t>& lits, std::uint32_t level, std::int32_t antecedent,
+                     const std::vector<unsigned long long>& deps, bool ovf) {
+    std::vector<void*> tmp;
+    dev::OpArgs op{};
+    op.op = dev::kOpAssign;
+    op.level = level;
+    op.antecedent = antecedent;
+    op.lits = dupload(lits, tmp);
+    op.n = static_cast<std::uint32_t>(lits.size());
+    std::vector<unsigned long long> d(W_, 0ull);
+    for (std::size_t i = 0; i < deps.size() && i < W_; ++i) d[i] = deps[i];
+    op.deps = dupload(d, tmp);
+    op.ovf = ovf ? 1u : 0u;
+    run_op(*impl_, op, nullptr);
+    for (void* p : tmp) cudaFree(p);
+}
+
+void Session::seed(const std::vector<std::int32_t>& lits) {
+    std::vector<void*> tmp;
+    dev::OpArgs op{};
+    op.op = dev::kOpSeed;
+    op.lits = dupload(lits, tmp);
+    op.n = static_cast<std::uint32_t>(lits.size());
+    run_op(*impl_, op, nullptr);
+    for (void* p : tmp) cudaFree(p);
+}
+
+std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
+    std::vector<void*> tmp;
+    dev::OpArgs op{};
+    op.op = dev::kOpLearn;
+    op.lits = dupload(lits, tmp);
+    op.n = static_cast<std::uint32_t>(lits.size());
+    run_op(*impl_, op, nullptr);
+    for (void* p : tmp) cudaFree(p);
+    return static_cast<std::int32_t>(ctl().b[12]);
+}
+
+dev::Ctl Session::ctl() const {
+    dev::Ctl c{};
+    ck(cudaMemcpy(&c, impl_->ar.slots[0].ctl, sizeof(c), cudaMemcpyDeviceToHost), "ctl");
+    return c;
+}
+
+namespace {
+template <class T>
+std::vector<T> dl(const T* p, std::size_t n) {
+    std::vector<T> v(n);
+    if (n) ck(cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), "download");
+    return v;
+}
+}  // namespace
+
+std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells, impl_->ar.A + 1); }
+std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail, ctl().ts); }
+std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason, impl_->ar.A + 1); }
+std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
+    return dl(impl_->ar.slots[0].deps + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1);
+}
+std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf, impl_->ar.A + 1); }
+std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl, ctl().n_confl); }
+std::vector<std::int32_t> Session::frontier() const {
+    const dev::Ctl c = ctl();
+    return dl(impl_->ar.slots[0].fr[c.cur], c.F);
+}
+
+}  // namespace yas

@@ -1,0 +1,91 @@
+// Program -> completion nogoods -> length-sorted CSR store (host, runs once per
+// solve). Both steps define the nogood ids and auxiliary atom ids that the
+// device engine and every trajectory counter depend on, so they follow the
+// reference's emission order exactly:
+//   compile_completion  /root/reference/proj/src/completion.cpp:60-146
+//   nogood_census       /root/reference/proj/src/completion.cpp:153-173
+//   NogoodStore::build  /root/reference/proj/src/nogood_store.cpp:25-74
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <optional>
+#include <string>
+#include <vector>
+
+#include "program.hpp"
+
+namespace yas {
+
+// Signed literal code: +atom for T atom, -atom for F atom.
+inline AtomId lit_atom(std::int32_t c) { return static_cast<AtomId>(c < 0 ? -c : c); }
+inline std::uint32_t lit_index(std::int32_t c) { return 2u * lit_atom(c) + (c < 0 ? 1u : 0u); }
+
+inline constexpr std::uint32_t kAnyTruth = 0xFFFFFFFFu;
+inline constexpr std::uint32_t kNoTruth = 0u;
+
+enum Origin : std::uint8_t { kCompletion = 0, kConstraint = 1, kLearned = 2 };
+
+struct Nogood {
+    std::vector<std::int32_t> lits;  // sorted by atom, duplicate free
+    std::uint8_t origin = kCompletion;
+    std::uint32_t guard = kAnyTruth;
+
+    /// Canonicalises (sort by atom, drop repeats); nullopt when the set holds
+    /// both signs of one atom. Contract of Nogood::make, nogood.hpp:80-87.
+    static std::optional<Nogood> make(std::vector<std::int32_t> lits, std::uint8_t origin,
+                                      std::uint32_t guard = kAnyTruth);
+    bool may_assert(std::int32_t l) const { return l < 0 || guard == kAnyTruth || guard == lit_atom(l); }
+};
+
+struct RuleAux {
+    AtomId b = 0, t = 0, n = 0;
+    bool vacuous = false;
+};
+
+struct Census {
+    std::size_t rule_nogoods = 0, atom_nogoods = 0, constraint_nogoods = 0;
+    std::size_t total() const { return rule_nogoods + atom_nogoods + constraint_nogoods; }
+};
+
+struct Completion {
+    std::vector<Nogood> nogoods;
+    std::vector<RuleAux> aux;      // per rule
+    std::vector<std::uint32_t> aux_rule;  // aux atom - first_aux -> rule index
+    std::vector<std::uint8_t> aux_kind;   // 0 body, 1 pos test, 2 neg test
+    AtomId first_aux = 0;
+    AtomId total_atoms = 0;
+    Census counts;
+    std::string atom_name(AtomId a, const Program& prog) const;
+};
+
+Completion compile_completion(const Program& prog);
+Census census(const Program& prog);
+std::string dump_nogoods(const Completion& comp, const Program& prog);
+
+/// Static store, laid out for upload. Length-1 nogoods whose complement may be
+/// asserted become `units` (kept in order); everything else is stable-sorted by
+/// length into CSR ids 0..N-1. Occurrence lists are CSR over the key
+/// (2*atom + neg) * 4 + length_class, ids ascending.
+struct StaticStore {
+    AtomId total_atoms = 0;
+    std::vector<std::uint32_t> off{0};
+    std::vector<std::int32_t> pool;
+    std::vector<std::uint32_t> guard;
+    std::vector<std::uint8_t> origin;
+    std::vector<std::int32_t> units;     // literals of the static unit nogoods
+    std::vector<std::int32_t> unit_ids;  // CSR ids of length-1 entries
+    std::vector<std::uint32_t> occ_off;  // (2A+2)*4 + 1
+    std::vector<std::int32_t> occ_ids;
+    std::array<std::uint32_t, 4> bounds{0, 0, 0, 0};
+
+    std::uint32_t size() const { return static_cast<std::uint32_t>(off.size() - 1); }
+    std::uint32_t length(std::uint32_t id) const { return off[id + 1] - off[id]; }
+    std::string dump_csv() const;
+};
+
+inline std::uint32_t length_class(std::uint32_t len) { return len >= 4 ? 3u : len - 1u; }
+
+StaticStore build_store(const std::vector<Nogood>& nogoods, AtomId total_atoms);
+
+}  // namespace yas

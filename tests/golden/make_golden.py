@@ -1,0 +1,107 @@
+"""Regenerate the committed golden fixtures from the UNMODIFIED reference.
+
+Runs oracle/_ref/aspine_ref (built by `make -C oracle ref` from
+/root/reference/proj/src) and stores its outputs as small JSON files here, so
+the parity tests can run on a machine without /root/reference (the GPU box).
+
+    python tests/golden/make_golden.py            # all fixtures
+"""
+from __future__ import annotations
+
+import json
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+REF = os.path.join(ROOT, "oracle", "_ref", "aspine_ref")
+sys.path.insert(0, ROOT)
+
+from paper_1909_01786_b200 import instances as I  # noqa: E402
+
+MODES = [("fwd", "occ"), ("res", "occ"), ("fwd", "jw"), ("res", "jw"), ("fwd", "act"), ("res", "act")]
+
+
+def ref(args, stdin=None):
+    out = subprocess.run([REF] + args, input=stdin, capture_output=True, text=True, check=False)
+    if out.returncode not in (0, 2):
+        raise RuntimeError(out.stderr)
+    return json.loads(out.stdout)
+
+
+def solve_text(text, opts):
+    return ref(["solve", "-"] + opts, stdin=text)
+
+
+def corpus():
+    """Acceptance corpus (acceptance_main.cpp:51-65) with full-enumeration results per mode x heuristic."""
+    progs = ref(["corpus"])
+    for p in progs:
+        runs = {}
+        for mode, heur in MODES:
+            r = solve_text(p["text"], ["-n", "0", "--mode", mode, "--heur", heur, "--verify"])
+            runs[f"{mode}/{heur}"] = {"status": r["status"], "models": r["models"], "stats": r["stats"]}
+        p["runs"] = runs
+    return progs
+
+
+def extras():
+    """Restarts, fanout, deps-words overflow, capacity: small programs x options."""
+    progs = ref(["corpus"])
+    cases = []
+    opts = [
+        ["--restarts", "1:1.5"], ["--restarts", "3:2", "--mode", "res"], ["--fanout", "3"],
+        ["--fanout", "2", "--heur", "act"], ["--deps-words", "1"], ["--mode", "res", "--heur", "act", "--decay", "0.8"],
+    ]
+    for i, p in enumerate(progs):
+        if i % 5:
+            continue
+        for o in opts:
+            r = solve_text(p["text"], ["-n", "0"] + o)
+            cases.append({"name": p["name"], "text": p["text"], "opts": o, "status": r["status"],
+                          "models": r["models"], "stats": r["stats"]})
+    php = I.pigeonhole(3, 2)
+    for o in (["--restarts", "1:1.5"], ["--restarts", "1:1.5", "--mode", "res"], ["--cap", "0"]):
+        r = solve_text(php, ["-n", "0"] + o)
+        cases.append({"name": "php32", "text": php, "opts": o, "status": r["status"], "models": r["models"],
+                      "stats": r["stats"], "error": r["error"]})
+    return cases
+
+
+def configs():
+    out = {}
+    q8 = I.queens(8)
+    for mode, heur in MODES:
+        r = solve_text(q8, ["-n", "0", "--mode", mode, "--heur", heur, "--trace"])
+        out[f"queens8/{mode}/{heur}"] = {"status": r["status"], "models": r["models"], "stats": r["stats"],
+                                         "trace": r["trace"]}
+    for name, text in (("colour2000", I.colouring(2000, 4.0, 3, 1)), ("ham200", I.hamiltonian(200, 1.0, 1))):
+        r = solve_text(text, ["-n", "1", "--no-models"])
+        r1 = solve_text(text, ["-n", "1"])
+        out[f"{name}/fwd/occ"] = {"status": r["status"], "models": r1["models"], "stats": r["stats"]}
+    return out
+
+
+def propstores():
+    return {
+        "test_propagate": ref(["propstores", "0xc105e001", "300", "10", "4"]),
+        "criterion5": ref(["propstores", "0xc7059a7e", "1000", "10", "4"]),
+    }
+
+
+def planted():
+    return [ref(["planted", "20000", "200000", str(p), "0x1b00b5"]) for p in (1, 10, 50, 90)]
+
+
+def main():
+    targets = sys.argv[1:] or ["corpus", "extras", "configs", "propstores", "planted"]
+    for t in targets:
+        data = globals()[t]()
+        with open(os.path.join(HERE, f"{t}.json"), "w") as f:
+            json.dump(data, f, separators=(",", ":"))
+        print(t, "written")
+
+
+if __name__ == "__main__":
+    main()

@@ -73,6 +73,12 @@ uint32_t yas_program_total_atoms(const yas_program* p); /* AuxMap::total_atoms *
 int yas_program_census(const yas_program* p, uint64_t census[3], uint64_t counts[3]);
 /* tp_step (program.hpp:96): interp sorted; out gets up to cap ids; returns count. */
 size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap);
+/* Cube split used by yas_solve when cfg.cube_atoms > 0: the first k choice
+ * atoms (a with "a :- not b." and "b :- not a."), and the cubes of `rank`
+ * (pattern i runs on rank i % world). Each cube is k nogood literals: +a for
+ * ":- a." and -a for ":- not a.". Returns the cube count; host-only. */
+size_t yas_program_cubes(const yas_program* p, uint32_t k, int rank, int world, int32_t* out, size_t cap,
+                         uint32_t* width);
 /* verify_model (solver.hpp:116): 1 when the sorted atom set is an answer set. */
 int yas_verify_model(const yas_program* p, const uint32_t* atom_ids, size_t n);
 

@@ -224,7 +224,9 @@ int cmd_dump(const std::string& file) {
 int cmd_corpus() {
     std::cout << "[";
     bool first = true;
-    auto emit = [&](const std::string& name, const GroundProgram& prog) {
+    auto emit = [&](const std::string& name, const GroundProgram& generated) {
+        // ids of the emitted text (the re-parse relabels atoms in first-occurrence order)
+        const GroundProgram prog = parse_program(print_program(generated));
         auto fam = enumerate_answer_sets(prog);
         std::ostringstream f;
         f << '[';

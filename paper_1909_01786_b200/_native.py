@@ -19,7 +19,7 @@ EXPORTS = [
     "yas_program_rule_count", "yas_program_constraint_count", "yas_program_atom_name", "yas_program_find",
     "yas_program_rule", "yas_program_print", "yas_program_dump_nogoods", "yas_program_store_csv",
     "yas_program_diagnostics", "yas_program_rule_aux", "yas_program_total_atoms", "yas_program_census",
-    "yas_program_tp_step", "yas_verify_model",
+    "yas_program_tp_step", "yas_program_cubes", "yas_verify_model",
     "yas_config_default", "yas_solve", "yas_result_status", "yas_result_model_count", "yas_result_model",
     "yas_result_model_cube", "yas_result_stats", "yas_result_free", "yas_stats_csv_header", "yas_emit_stats",
     "yas_store_build", "yas_store_free", "yas_store_size", "yas_store_total_atoms", "yas_store_dump_csv",
@@ -103,6 +103,7 @@ def lib() -> C.CDLL:
         "yas_program_total_atoms": (U32, [P]),
         "yas_program_census": (C.c_int, [P, pU64, pU64]),
         "yas_program_tp_step": (SZ, [P, pU32, SZ, pU32, SZ]),
+        "yas_program_cubes": (SZ, [P, U32, C.c_int, C.c_int, pI32, SZ, pU32]),
         "yas_verify_model": (C.c_int, [P, pU32, SZ]),
         "yas_config_default": (None, [C.POINTER(yas_config)]),
         "yas_solve": (C.c_int, [P, C.POINTER(yas_config), C.POINTER(P), C.c_char_p, SZ]),

@@ -239,6 +239,26 @@ class GroundProgram:
     def total_atoms(self) -> int:
         return N.lib().yas_program_total_atoms(self._h)
 
+    def _rule(self, r: int):
+        head = C.c_uint32()
+        pos, neg = C.POINTER(C.c_uint32)(), C.POINTER(C.c_uint32)()
+        np_, nn = C.c_uint32(), C.c_uint32()
+        if N.lib().yas_program_rule(self._h, r, C.byref(head), C.byref(pos), C.byref(np_), C.byref(neg),
+                                    C.byref(nn)) != 0:
+            raise IndexError(r)
+        return head.value, list(pos[: np_.value]), list(neg[: nn.value])
+
+    def rules(self):
+        """[(head, pos_body, neg_body)] in rule order (GroundProgram::rules)."""
+        return [self._rule(r) for r in range(self.rule_count())]
+
+    def constraints(self):
+        nr = self.rule_count()
+        return [self._rule(nr + c) for c in range(self.constraint_count())]
+
+    def rules_of(self, atom: int):
+        return [i for i, (h, _, _) in enumerate(self.rules()) if h == atom]
+
     def rule_aux(self, rule: int):
         out = (C.c_uint32 * 4)()
         if N.lib().yas_program_rule_aux(self._h, rule, out) != 0:
@@ -297,6 +317,16 @@ def tp_step(prog: GroundProgram, interp: Sequence[int]) -> List[int]:
     out = (C.c_uint32 * cap)()
     n = N.lib().yas_program_tp_step(prog._h, arr, len(interp), out, cap)
     return list(out[:n])
+
+
+def cubes(prog: GroundProgram, k: int, rank: int = 0, world: int = 1):
+    """Cube split used by solve(cube_atoms=k): list of cubes (nogood literals) of this rank."""
+    width = C.c_uint32(0)
+    n = N.lib().yas_program_cubes(prog._h, k, rank, world, None, 0, C.byref(width))
+    out = (C.c_int32 * max(1, n * max(1, width.value)))()
+    N.lib().yas_program_cubes(prog._h, k, rank, world, out, n * width.value, C.byref(width))
+    w = width.value
+    return [list(out[i * w:(i + 1) * w]) for i in range(n)]
 
 
 def verify_model(prog: GroundProgram, model: Model) -> bool:

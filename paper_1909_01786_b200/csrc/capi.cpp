@@ -101,6 +101,9 @@ int guarded(char* err, std::size_t cap, F&& f) {
     } catch (const VerifyError& e) {
         put_err(err, cap, e.what());
         return YAS_ERR_VERIFY;
+    } catch (const std::invalid_argument& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_ARG;
     } catch (const std::logic_error& e) {
         put_err(err, cap, e.what());
         return YAS_ERR_LOGIC;
@@ -139,6 +142,25 @@ std::vector<AtomId> choice_atoms(const Program& prog, std::uint32_t k) {
         taken[a] = taken[partner[a]] = 1;
     }
     return out;
+}
+
+// Every sign pattern over the first k choice atoms, as integrity constraints
+// (":- a." -> nogood {T a}; ":- not a." -> {F a}); pattern i belongs to rank
+// i % world. Returns the number of cubes of this rank.
+std::uint32_t make_cubes(const Program& prog, std::uint32_t k, int rank, int world, std::vector<std::int32_t>& cubes,
+                         std::uint32_t& width) {
+    const std::vector<AtomId> ca = choice_atoms(prog, std::min<std::uint32_t>(k, 24));
+    width = static_cast<std::uint32_t>(ca.size());
+    const std::uint32_t total = 1u << width;
+    std::uint32_t n = 0;
+    cubes.clear();
+    for (std::uint32_t pat = 0; pat < total; ++pat) {
+        if (static_cast<int>(pat % static_cast<std::uint32_t>(world < 1 ? 1 : world)) != rank) continue;
+        for (std::uint32_t j = 0; j < width; ++j)
+            cubes.push_back(((pat >> j) & 1u) ? -static_cast<std::int32_t>(ca[j]) : static_cast<std::int32_t>(ca[j]));
+        ++n;
+    }
+    return n;
 }
 
 void fill_stats(yas_stats& o, const dev::Stats& s) {
@@ -283,6 +305,17 @@ size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t 
     for (std::size_t i = 0; i < r.size() && i < cap; ++i) out[i] = r[i];
     return r.size();
 }
+size_t yas_program_cubes(const yas_program* p, uint32_t k, int rank, int world, int32_t* out, size_t cap,
+                         uint32_t* width) {
+    if (!p) return 0;
+    std::vector<std::int32_t> cubes;
+    std::uint32_t w = 0;
+    const std::uint32_t n = make_cubes(p->prog, k, rank, world, cubes, w);
+    if (width) *width = w;
+    for (std::size_t i = 0; i < cubes.size() && i < cap; ++i) out[i] = cubes[i];
+    return n;
+}
+
 int yas_verify_model(const yas_program* p, const uint32_t* ids, size_t n) {
     if (!p) return 0;
     return is_answer_set(p->prog, std::vector<AtomId>(ids, ids + n)) ? 1 : 0;
@@ -341,21 +374,10 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         dc.learned_capacity = cfg.learned_capacity;
         dc.trace = cfg.trace ? 1u : 0u;
 
-        // cubes: every sign pattern over the first k choice atoms, as
-        // integrity constraints (":- a." -> nogood {T a}; ":- not a." -> {F a}).
         std::vector<std::int32_t> cubes;
         std::uint32_t width = 0, n_cubes = 1;
         if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
-            const std::vector<AtomId> ca = choice_atoms(prog, std::min<std::uint32_t>(cfg.cube_atoms, 24));
-            width = static_cast<std::uint32_t>(ca.size());
-            const std::uint32_t total = 1u << width;
-            n_cubes = 0;
-            for (std::uint32_t pat = 0; pat < total; ++pat) {
-                if (static_cast<int>(pat % static_cast<std::uint32_t>(cfg.world)) != cfg.rank) continue;
-                for (std::uint32_t k = 0; k < width; ++k)
-                    cubes.push_back(((pat >> k) & 1u) ? -static_cast<std::int32_t>(ca[k]) : static_cast<std::int32_t>(ca[k]));
-                ++n_cubes;
-            }
+            n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.rank, cfg.world, cubes, width);
         } else if (cfg.rank != 0) {
             n_cubes = 0;  // a single search runs on rank 0 only
         }

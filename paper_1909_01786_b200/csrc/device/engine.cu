@@ -267,6 +267,75 @@ struct GridG {
 // ---------------------------------------------------------------------------
 // The search (one instance per group)
 // ---------------------------------------------------------------------------
+// Shared-memory working set of a single-CTA search (all null for GridG).
+struct Sm {
+    unsigned long long* htab;  // claim hash: (id+1) << 32 | min e
+    unsigned long long* wtab;  // win hash:   (atom+1) << 32 | (e << 1 | neg)
+    std::int32_t* pid;
+    std::int32_t* plit;
+    std::uint32_t* pslot;      // claim slot | win slot << 16
+    unsigned long long* pdep;  // Deps word 0 of the proposal (computed at evaluation)
+    std::uint32_t* pmeta;      // overflow << 31 | occurrence total of the proposed literal
+    std::int32_t* litat;
+    std::uint32_t* otat;
+    std::uint32_t* bits;
+    std::int32_t* fr;          // mirror of the current frontier
+    std::uint32_t* froff;      // and of its occurrence offsets
+    std::uint32_t* vasg;       // 2-bit assignment mirror: assigned / true
+    std::uint32_t* vtru;
+    std::uint32_t tcap, hmask, fcap, vwords;
+};
+
+struct SmemCfg {
+    std::uint32_t tcap, hcap, fcap, vwords;
+};
+
+__device__ __forceinline__ std::uint32_t hslot(std::uint32_t key, std::uint32_t mask) { return (key * 2654435761u) & mask; }
+
+__device__ Sm carve_smem(unsigned char* base, const SmemCfg& cfg) {
+    Sm m{};
+    m.tcap = cfg.tcap;
+    m.hmask = cfg.hcap ? cfg.hcap - 1 : 0;
+    m.fcap = cfg.fcap;
+    m.vwords = cfg.vwords;
+    std::size_t o = 0;
+    auto take = [&](std::size_t bytes) {
+        unsigned char* p = base + o;
+        o += (bytes + 15) & ~static_cast<std::size_t>(15);
+        return p;
+    };
+    if (cfg.tcap) {
+        m.htab = reinterpret_cast<unsigned long long*>(take(8ull * cfg.hcap));
+        m.wtab = reinterpret_cast<unsigned long long*>(take(8ull * cfg.hcap));
+        m.pid = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
+        m.plit = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
+        m.pslot = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
+        m.pdep = reinterpret_cast<unsigned long long*>(take(8ull * cfg.tcap));
+        m.pmeta = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
+        m.litat = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
+        m.otat = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
+        m.bits = reinterpret_cast<std::uint32_t*>(take(4ull * ((cfg.tcap + 31) / 32)));
+        m.fr = reinterpret_cast<std::int32_t*>(take(4ull * cfg.fcap));
+        m.froff = reinterpret_cast<std::uint32_t*>(take(4ull * (cfg.fcap + 1)));
+    }
+    if (cfg.vwords) {
+        m.vasg = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.vwords));
+        m.vtru = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.vwords));
+    }
+    return m;
+}
+
+std::size_t smem_bytes(const SmemCfg& cfg) {
+    auto r = [](std::size_t b) { return (b + 15) & ~static_cast<std::size_t>(15); };
+    std::size_t o = 0;
+    if (cfg.tcap)
+        o += 2 * r(8ull * cfg.hcap) + 6 * r(4ull * cfg.tcap) + r(8ull * cfg.tcap) + r(4ull * ((cfg.tcap + 31) / 32)) +
+             r(4ull * cfg.fcap) +
+             r(4ull * (cfg.fcap + 1));
+    if (cfg.vwords) o += 2 * r(4ull * cfg.vwords);
+    return o;
+}
+
 template <class G>
 struct Search {
     G& g;
@@ -277,10 +346,52 @@ struct Search {
     Shared* sh;
     Ctl* c;
     unsigned long long t0;
+    Sm sm;
 
     __device__ Search(G& g_, const Static& s, const Config& cf, const Slot& slot, const Caps& k, Shared* shared,
-                      unsigned long long start)
-        : g(g_), S(s), C(cf), sl(slot), K(k), sh(shared), c(g_.c), t0(start) {}
+                      unsigned long long start, const Sm& smem)
+        : g(g_), S(s), C(cf), sl(slot), K(k), sh(shared), c(g_.c), t0(start), sm(smem) {}
+
+    // ---- assignment access: 2-bit shared mirror when present --------------
+    // sign of the atom's value: 0 unassigned, 1 true, -1 false
+    __device__ int val(std::uint32_t a) const {
+        if (sm.vwords) {
+            const std::uint32_t b = 1u << (a & 31);
+            if (!(sm.vasg[a >> 5] & b)) return 0;
+            return (sm.vtru[a >> 5] & b) ? 1 : -1;
+        }
+        const std::int32_t cv = sl.cells[a];
+        return (cv > 0) - (cv < 0);
+    }
+    __device__ void set_cell(std::uint32_t a, std::int32_t cv) const {
+        sl.cells[a] = cv;
+        if (sm.vwords) {
+            const std::uint32_t b = 1u << (a & 31);
+            if (cv == 0) {
+                atomicAnd(sm.vasg + (a >> 5), ~b);
+                atomicAnd(sm.vtru + (a >> 5), ~b);
+            } else {
+                if (cv > 0) atomicOr(sm.vtru + (a >> 5), b);
+                else atomicAnd(sm.vtru + (a >> 5), ~b);
+                atomicOr(sm.vasg + (a >> 5), b);
+            }
+        }
+    }
+    __device__ void rebuild_mirror() const {
+        if (!sm.vwords) return;
+        for (std::uint32_t w = g.tid(); w < sm.vwords; w += g.size()) {
+            std::uint32_t as = 0, tr = 0;
+            for (std::uint32_t b = 0; b < 32; ++b) {
+                const std::uint32_t a = 32 * w + b;
+                if (a > S.A) break;
+                const std::int32_t cv = sl.cells[a];
+                if (cv != 0) as |= 1u << b;
+                if (cv > 0) tr |= 1u << b;
+            }
+            sm.vasg[w] = as;
+            sm.vtru[w] = tr;
+        }
+    }
 
     // ---- store access ----------------------------------------------------
     __device__ const std::int32_t* lits_of(std::uint32_t id, std::uint32_t& len) const {
@@ -306,16 +417,28 @@ struct Search {
         return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot[li];
     }
     // j-th entry of the literal's occurrence list [static c0, learned c0, ..., static c3, learned c3]
-    __device__ std::int32_t occ_entry(std::uint32_t li, std::uint32_t j) const {
-#pragma unroll 1
-        for (std::uint32_t cl = 0; cl < 4; ++cl) {
-            const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
-            if (j < hi - lo) return __ldg(S.occ_ids + lo + j);
-            j -= hi - lo;
-            const std::uint32_t* h = sl.lhdr + 3 * (li * 4 + cl);
-            const std::uint32_t n = h[1];
-            if (j < n) return sl.larena[h[0] + j];
-            j -= n;
+    // All segment bounds are loaded at once (one memory round trip), then one
+    // dependent load fetches the id.
+    __device__ std::int32_t occ_entry(std::uint32_t li, std::uint32_t j, bool learned) const {
+        const std::uint32_t* oo = S.occ_off + li * 4;
+        std::uint32_t b[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) b[k] = __ldg(oo + k);
+        if (!learned) return __ldg(S.occ_ids + b[0] + j);  // classes are contiguous
+        const std::uint32_t* h = sl.lhdr + 12 * li;
+        std::uint32_t hp[4], hn[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            hp[k] = h[3 * k];
+            hn[k] = h[3 * k + 1];
+        }
+#pragma unroll
+        for (int cl = 0; cl < 4; ++cl) {
+            const std::uint32_t ns = b[cl + 1] - b[cl];
+            if (j < ns) return __ldg(S.occ_ids + b[cl] + j);
+            j -= ns;
+            if (j < hn[cl]) return sl.larena[hp[cl] + j];
+            j -= hn[cl];
         }
         return -1;
     }
@@ -327,8 +450,17 @@ struct Search {
         return sl.deps[static_cast<std::size_t>(w) * (S.A + 1) + a];
     }
     __device__ bool holds(std::int32_t l) const {
-        const std::int32_t cv = sl.cells[atom_of(l)];
-        return cv != 0 && ((cv > 0) == (l > 0));
+        const int v = val(atom_of(l));
+        return v != 0 && ((v > 0) == (l > 0));
+    }
+
+    // phase accounting: cycles since the previous mark go to bucket k
+    __device__ void mark(int k) const {
+        if (g.leader()) {
+            const unsigned long long t = clock64();
+            c->prof[k] += t - c->prof_t;
+            c->prof_t = t;
+        }
     }
 
     __device__ void fail(std::uint32_t status) {
@@ -341,77 +473,108 @@ struct Search {
                                     std::uint32_t level) const {
         const std::uint32_t nw = nwords(level);
         std::uint8_t ovf = 0;
-        for (std::uint32_t w = 0; w < nw; ++w) {
-            unsigned long long acc = 0;
-            for (std::uint32_t k = 0; k < len; ++k) {
-                const std::uint32_t x = atom_of(lit_at(L, k, id));
-                if (x == a) continue;
-                if (lvl_of(sl.cells[x]) <= 1) continue;
-                acc |= dep(w, x);
-                if (w == 0) ovf |= sl.dovf[x];
-            }
-            dep(w, a) = acc;
-        }
+        for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = deps_word(L, len, id, a, w, ovf);
         sl.dovf[a] = ovf;
+    }
+    __device__ unsigned long long deps_word(const std::int32_t* L, std::uint32_t len, std::uint32_t id,
+                                            std::uint32_t a, std::uint32_t w, std::uint8_t& ovf) const {
+        unsigned long long acc = 0;
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::uint32_t x = atom_of(lit_at(L, k, id));
+            const std::int32_t cv = sl.cells[x];
+            const unsigned long long d = dep(w, x);
+            const std::uint8_t o = w == 0 ? sl.dovf[x] : 0;
+            if (x != a && lvl_of(cv) > 1) {
+                acc |= d;
+                ovf |= o;
+            }
+        }
+        return acc;
     }
 
     // ---- group-parallel building blocks -------------------------------------
-    // Exclusive occurrence offsets of the current frontier; sets c->T.
+    // Exclusive occurrence offsets of the current frontier; sets c->T. The
+    // frontier and its offsets are mirrored into shared memory when they fit.
     __device__ void frontier_offsets() {
         const std::uint32_t F = c->F;
         const std::int32_t* fr = sl.fr[c->cur];
+        const bool mirror = sm.tcap && F + 1 <= sm.fcap;
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < F; base += g.size()) {
             const std::uint32_t p = base + g.tid();
-            const unsigned long long v = p < F ? occ_total(lidx(fr[p])) : 0ull;
+            const std::int32_t lit = p < F ? fr[p] : 0;
+            const unsigned long long v = p < F ? occ_total(lidx(lit)) : 0ull;
             unsigned long long tot;
             const unsigned long long pre = g.scan(v, tot) + carry;
-            if (p < F) sl.froff[p] = static_cast<std::uint32_t>(pre);
+            if (p < F) {
+                sl.froff[p] = static_cast<std::uint32_t>(pre);
+                if (mirror) {
+                    sm.froff[p] = static_cast<std::uint32_t>(pre);
+                    sm.fr[p] = lit;
+                }
+            }
             carry += tot;
         }
         g.sync();
         if (g.leader()) {
             sl.froff[F] = static_cast<std::uint32_t>(carry);
+            if (mirror) sm.froff[F] = static_cast<std::uint32_t>(carry);
             c->T = static_cast<std::uint32_t>(carry);
             c->b[11] = 0;
         }
         g.sync();
+        mark(1);
     }
 
     // Winners marked in the bitmap (bits e < T) are written, in e order, to the
     // frontier buffer `dst`, appended to the trail, and the occurrence offsets
     // of that new frontier are produced by the same scan.
-    __device__ void compact(std::uint32_t T, std::uint32_t dst, bool pass) {
+    template <bool SMEM>
+    __device__ void compact(std::uint32_t T, std::uint32_t dst, bool pass, std::uint32_t hsize) {
         const std::uint32_t nw = (T + 31) / 32;
         const std::uint32_t ts0 = c->ts;
         std::int32_t* out = sl.fr[dst];
+        std::uint32_t* bsrc = SMEM ? sm.bits : sl.bitmap;
+        const std::int32_t* lat = SMEM ? sm.litat : sl.litat;
+        const std::uint32_t fcap = sm.tcap ? sm.fcap : 0;
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < nw; base += g.size()) {
             const std::uint32_t wi = base + g.tid();
-            std::uint32_t bits = wi < nw ? sl.bitmap[wi] : 0u;
+            const std::uint32_t bits = wi < nw ? bsrc[wi] : 0u;
             unsigned long long occ = 0;
-            for (std::uint32_t b = bits; b; b &= b - 1) occ += occ_total(lidx(sl.litat[wi * 32 + __ffs(b) - 1]));
+            for (std::uint32_t b = bits; b; b &= b - 1)
+                occ += SMEM ? sm.otat[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lat[wi * 32 + __ffs(b) - 1]));
             const unsigned long long v = (static_cast<unsigned long long>(__popc(bits)) << 32) | occ;
             unsigned long long tot;
             const unsigned long long pre = g.scan(v, tot) + carry;
             std::uint32_t r = static_cast<std::uint32_t>(pre >> 32);
             std::uint32_t o = static_cast<std::uint32_t>(pre);
             for (std::uint32_t b = bits; b; b &= b - 1) {
-                const std::int32_t lit = sl.litat[wi * 32 + __ffs(b) - 1];
+                const std::int32_t lit = lat[wi * 32 + __ffs(b) - 1];
                 out[r] = lit;
                 sl.froff[r] = o;
+                if (r < fcap) {
+                    sm.fr[r] = lit;
+                    sm.froff[r] = o;
+                }
                 sl.trail[ts0 + r] = lit;
                 sl.tpos[atom_of(lit)] = ts0 + r;
-                o += occ_total(lidx(lit));
+                o += SMEM ? sm.otat[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lit));
                 ++r;
             }
-            if (bits) sl.bitmap[wi] = 0u;
+            if (bits) bsrc[wi] = 0u;
             carry += tot;
         }
+        if (SMEM)
+            for (std::uint32_t i = g.tid(); i < hsize; i += g.size()) {
+                sm.htab[i] = 0ull;
+                sm.wtab[i] = 0ull;
+            }
         g.sync();
         if (g.leader()) {
             const std::uint32_t cnt = static_cast<std::uint32_t>(carry >> 32);
             sl.froff[cnt] = static_cast<std::uint32_t>(carry);
+            if (cnt + 1 <= fcap) sm.froff[cnt] = static_cast<std::uint32_t>(carry);
             c->ts = ts0 + cnt;
             c->F = cnt;
             c->T = static_cast<std::uint32_t>(carry);
@@ -429,112 +592,232 @@ struct Search {
 
     // Apply proposals: per atom the smallest key wins (newly_set); an opposite
     // loser turns its nogood into a conflict (assignment.cpp:116-124).
+    template <bool SMEM>
     __device__ void apply(std::uint32_t level, bool unit) {
         const std::uint32_t np = c->n_props;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
         for (std::uint32_t base = g.tid() & ~31u; base < np; base += g.size()) {
             const std::uint32_t i = base + lane_id();
             bool lose = false;
-            int4 p = make_int4(0, 0, 0, 0);
+            std::int32_t id = 0;
             if (i < np) {
-                p = sl.props[i];
-                const std::uint32_t a = atom_of(p.y);
-                const unsigned long long w = sl.win[a];
-                if ((static_cast<std::uint32_t>(w) >> 1) == static_cast<std::uint32_t>(p.z)) {
-                    sl.cells[a] = p.y > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level);
+                std::int32_t lit;
+                std::uint32_t e;
+                unsigned long long w;
+                if (SMEM) {
+                    id = sm.pid[i];
+                    lit = sm.plit[i];
+                    const std::uint32_t ps = sm.pslot[i];
+                    e = static_cast<std::uint32_t>(sm.htab[ps & 0xffffu]);
+                    w = sm.wtab[ps >> 16];
+                } else {
+                    const int4 p = sl.props[i];
+                    id = p.x;
+                    lit = p.y;
+                    e = static_cast<std::uint32_t>(p.z);
+                    w = sl.win[atom_of(lit)];
+                }
+                const std::uint32_t a = atom_of(lit);
+                if ((static_cast<std::uint32_t>(w) >> 1) == e) {
+                    set_cell(a, lit > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
                     if (unit) {
                         sl.reason[a] = kReasonUnit;
                     } else {
-                        sl.reason[a] = p.x;
-                        std::uint32_t len;
-                        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(p.x), len);
-                        write_deps_from(L, len, static_cast<std::uint32_t>(p.x), a, dlev);
+                        sl.reason[a] = id;
+                        if (SMEM && nwords(dlev) == 1) {
+                            dep(0, a) = sm.pdep[i];
+                            sl.dovf[a] = static_cast<std::uint8_t>(sm.pmeta[i] >> 31);
+                        } else {
+                            std::uint32_t len;
+                            const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+                            write_deps_from(L, len, static_cast<std::uint32_t>(id), a, dlev);
+                        }
                     }
-                    atomicOr(sl.bitmap + (p.z >> 5), 1u << (p.z & 31));
-                    sl.litat[p.z] = p.y;
+                    if (SMEM) {
+                        atomicOr(sm.bits + (e >> 5), 1u << (e & 31));
+                        sm.litat[e] = lit;
+                        sm.otat[e] = sm.pmeta[i] & 0x7fffffffu;
+                    } else {
+                        atomicOr(sl.bitmap + (e >> 5), 1u << (e & 31));
+                        sl.litat[e] = lit;
+                    }
                 } else {
-                    lose = (w & 1ull) != (p.y < 0 ? 1ull : 0ull);
+                    lose = (w & 1ull) != (lit < 0 ? 1ull : 0ull);
                 }
             }
             __syncwarp();
             const std::uint32_t slot = warp_append(&c->n_confl, lose);
-            if (lose) sl.confl[slot] = p.x;
+            if (lose) sl.confl[slot] = id;
         }
         g.sync();
+    }
+
+    // Evaluate nogood `id` against the pass-start assignment
+    // (propagate.cpp:86-168 without the watch shortcuts).
+    __device__ void evaluate(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit,
+                             unsigned long long* d0 = nullptr, std::uint32_t* meta = nullptr) const {
+        std::uint32_t len;
+        const std::uint32_t guard = guard_of(static_cast<std::uint32_t>(id));
+        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+        if (len == 1) {
+            conflict = holds(lit_at(L, 0, static_cast<std::uint32_t>(id)));
+            return;
+        }
+        std::uint32_t nfree = 0;
+        std::int32_t u1 = 0;
+        for (std::uint32_t k = 0; k < len; ++k) {
+            const std::int32_t l = lit_at(L, k, static_cast<std::uint32_t>(id));
+            const int v = val(atom_of(l));
+            if (v == 0) {
+                if (nfree == 0) u1 = l;
+                if (++nfree == 2) return;
+            } else if ((v > 0) != (l > 0)) {
+                return;  // a dead literal: satisfied
+            }
+        }
+        if (nfree == 0) conflict = true;
+        else if (may_assert(guard, -u1)) {
+            prop = true;
+            plit = -u1;
+            if (d0) {
+                std::uint8_t ovf = 0;
+                *d0 = deps_word(L, len, static_cast<std::uint32_t>(id), atom_of(u1), 0, ovf);
+                *meta = occ_total(lidx(plit)) | (static_cast<std::uint32_t>(ovf) << 31);
+            }
+        }
+    }
+
+    // One pass with the working set in shared memory (T <= tcap).
+    __device__ void pass_smem(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
+        const bool learned = c->learned_n > 0;
+        std::uint32_t hs = 64;
+        while (hs < 2 * T) hs <<= 1;
+        if (hs > sm.hmask + 1) hs = sm.hmask + 1;
+        const std::uint32_t hm = hs - 1;
+        for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
+            const std::uint32_t e = base + lane_id();
+            bool first = false, conflict = false, prop = false;
+            std::int32_t id = -1, plit = 0;
+            std::uint32_t slot = 0, meta = 0;
+            unsigned long long d0 = 0;
+            if (e < T) {
+                std::uint32_t lo = 0, hi = F;
+                while (hi - lo > 1) {
+                    const std::uint32_t mid = (lo + hi) >> 1;
+                    if (sm.froff[mid] <= e) lo = mid; else hi = mid;
+                }
+                id = occ_entry(lidx(sm.fr[lo]), e - sm.froff[lo], learned);
+                const unsigned long long key = (static_cast<unsigned long long>(id + 1) << 32) | e;
+                for (std::uint32_t h = hslot(static_cast<std::uint32_t>(id), hm);; h = (h + 1) & hm) {
+                    unsigned long long cur_k = sm.htab[h];
+                    if (cur_k == 0ull) {
+                        cur_k = atomicCAS(sm.htab + h, 0ull, key);
+                        if (cur_k == 0ull) { first = true; slot = h; break; }
+                    }
+                    if ((cur_k >> 32) == static_cast<unsigned long long>(id + 1)) {
+                        atomicMin(sm.htab + h, key);
+                        break;
+                    }
+                }
+                if (first) evaluate(id, conflict, prop, plit, &d0, &meta);
+            }
+            __syncwarp();
+            warp_count(&c->st.checks, first);
+            const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+            if (conflict) sl.confl[cs] = id;
+            const std::uint32_t ps = warp_append(&c->n_props, prop);
+            if (prop) {
+                sm.pid[ps] = id;
+                sm.plit[ps] = plit;
+                sm.pslot[ps] = slot;
+                sm.pdep[ps] = d0;
+                sm.pmeta[ps] = meta;
+            }
+        }
+        g.sync();
+        mark(2);
+        const std::uint32_t np = c->n_props;
+        for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
+            const std::uint32_t e = static_cast<std::uint32_t>(sm.htab[sm.pslot[i]]);
+            const std::int32_t lit = sm.plit[i];
+            const std::uint32_t a = atom_of(lit);
+            const unsigned long long key =
+                (static_cast<unsigned long long>(a + 1) << 32) | (static_cast<unsigned long long>(e) << 1) | (lit < 0 ? 1ull : 0ull);
+            for (std::uint32_t h = hslot(a, hm);; h = (h + 1) & hm) {
+                unsigned long long cur_k = sm.wtab[h];
+                if (cur_k == 0ull) {
+                    cur_k = atomicCAS(sm.wtab + h, 0ull, key);
+                    if (cur_k == 0ull) { sm.pslot[i] |= h << 16; break; }
+                }
+                if ((cur_k >> 32) == static_cast<unsigned long long>(a + 1)) {
+                    atomicMin(sm.wtab + h, key);
+                    sm.pslot[i] |= h << 16;
+                    break;
+                }
+            }
+        }
+        g.sync();
+        mark(3);
+        apply<true>(level, false);
+        mark(4);
+        compact<true>(T, cur ^ 1u, true, hs);
+        mark(5);
+    }
+
+    // One pass with the working set in global memory (any size; grid mode).
+    __device__ void pass_global(std::uint32_t F, std::uint32_t T, std::uint32_t gen, std::uint32_t cur,
+                                std::uint32_t level) {
+        const bool learned = c->learned_n > 0;
+        const std::int32_t* fr = sl.fr[cur];
+        for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
+            const std::uint32_t e = base + lane_id();
+            bool first = false, conflict = false, prop = false;
+            std::int32_t id = -1, plit = 0;
+            if (e < T) {
+                std::uint32_t lo = 0, hi = F;  // largest p with froff[p] <= e
+                while (hi - lo > 1) {
+                    const std::uint32_t mid = (lo + hi) >> 1;
+                    if (sl.froff[mid] <= e) lo = mid; else hi = mid;
+                }
+                id = occ_entry(lidx(fr[lo]), e - sl.froff[lo], learned);
+                const unsigned long long old = atomicMin(sl.claim + id, ckey(gen, e));
+                first = static_cast<std::uint32_t>(old >> 32) != ~gen;
+                if (first) evaluate(id, conflict, prop, plit);
+            }
+            __syncwarp();
+            warp_count(&c->st.checks, first);
+            const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+            if (conflict) sl.confl[cs] = id;
+            const std::uint32_t ps = warp_append(&c->n_props, prop);
+            if (prop) sl.props[ps] = make_int4(id, plit, 0, 0);
+        }
+        g.sync();
+        // resolve: final min-e of every proposing nogood, atomicMin per atom
+        const std::uint32_t np = c->n_props;
+        for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
+            int4 p = sl.props[i];
+            const std::uint32_t e = static_cast<std::uint32_t>(sl.claim[p.x]);
+            p.z = static_cast<std::int32_t>(e);
+            sl.props[i] = p;
+            atomicMin(sl.win + atom_of(p.y), wkey(gen, e, p.y < 0));
+        }
+        g.sync();
+        apply<false>(level, false);
+        compact<false>(T, cur ^ 1u, true, 0);
     }
 
     // One propagation call to fixpoint or violation (propagate.cpp:170-205).
     // Returns true when conflicts were found (they are in confl[0..n_confl)).
     __device__ bool propagate(std::uint32_t level) {
+        mark(0);
         frontier_offsets();
         for (;;) {
-            const std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur;
-            if (F == 0) break;
-            const std::int32_t* fr = sl.fr[cur];
-            // expand + claim + evaluate against the pass-start snapshot
-            for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
-                const std::uint32_t e = base + lane_id();
-                bool first = false, conflict = false, prop = false;
-                std::int32_t id = -1, plit = 0;
-                if (e < T) {
-                    std::uint32_t lo = 0, hi = F;  // largest p with froff[p] <= e
-                    while (hi - lo > 1) {
-                        const std::uint32_t mid = (lo + hi) >> 1;
-                        if (sl.froff[mid] <= e) lo = mid; else hi = mid;
-                    }
-                    id = occ_entry(lidx(fr[lo]), e - sl.froff[lo]);
-                    const unsigned long long old = atomicMin(sl.claim + id, ckey(gen, e));
-                    first = static_cast<std::uint32_t>(old >> 32) != ~gen;
-                    if (first) {
-                        std::uint32_t len;
-                        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
-                        if (len == 1) {
-                            conflict = holds(lit_at(L, 0, id));
-                        } else {
-                            std::uint32_t nfree = 0;
-                            std::int32_t u1 = 0;
-                            bool dead = false;
-                            for (std::uint32_t k = 0; k < len; ++k) {
-                                const std::int32_t l = lit_at(L, k, id);
-                                const std::int32_t cv = sl.cells[atom_of(l)];
-                                if (cv == 0) {
-                                    if (nfree == 0) u1 = l;
-                                    if (++nfree == 2) break;
-                                } else if ((cv > 0) != (l > 0)) {
-                                    dead = true;
-                                    break;
-                                }
-                            }
-                            if (!dead) {
-                                if (nfree == 0) conflict = true;
-                                else if (nfree == 1 && may_assert(guard_of(id), -u1)) { prop = true; plit = -u1; }
-                            }
-                        }
-                    }
-                }
-                __syncwarp();
-                warp_count(&c->st.checks, first);
-                const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-                if (conflict) sl.confl[cs] = id;
-                const std::uint32_t ps = warp_append(&c->n_props, prop);
-                if (prop) sl.props[ps] = make_int4(id, plit, 0, 0);
-            }
-            g.sync();
-            // resolve: final min-e of every proposing nogood, atomicMin per atom
-            const std::uint32_t np = c->n_props;
-            for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
-                int4 p = sl.props[i];
-                const std::uint32_t e = static_cast<std::uint32_t>(sl.claim[p.x]);
-                p.z = static_cast<std::int32_t>(e);
-                sl.props[i] = p;
-                atomicMin(sl.win + atom_of(p.y), wkey(gen, e, p.y < 0));
-            }
-            g.sync();
-            apply(level, false);
-            compact(T, cur ^ 1u, true);
-            if (c->b[11]) return true;
+            const std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, viol = c->b[11];
+            if (viol) return true;
+            if (F == 0) return false;
+            if (sm.tcap && T <= sm.tcap && F + 1 <= sm.fcap) pass_smem(F, T, cur, level);
+            else pass_global(F, T, gen, cur, level);
         }
-        return false;
     }
 
     // Initial propagation (propagate.cpp:23-47): static units in compile order
@@ -564,7 +847,7 @@ struct Search {
                 }
                 if (force) {
                     lit = -sigma;
-                    const std::int32_t cv = sl.cells[atom_of(lit)];
+                    const int cv = val(atom_of(lit));
                     if (cv != 0) {
                         conflict = (cv > 0) != (lit > 0);
                     } else {
@@ -592,7 +875,7 @@ struct Search {
                 const std::int32_t sigma = lit_at(L, 0, static_cast<std::uint32_t>(id));
                 if (!may_assert(guard_of(static_cast<std::uint32_t>(id)), -sigma)) {
                     const std::uint32_t a = atom_of(sigma);
-                    const std::int32_t cv = sl.cells[a];
+                    const int cv = val(a);
                     if (cv != 0) {
                         conflict = (cv > 0) == (sigma > 0);
                     } else {
@@ -608,8 +891,8 @@ struct Search {
             if (conflict) sl.confl[cs] = id;
         }
         g.sync();
-        apply(1, true);
-        compact(total, c->cur, false);
+        apply<false>(1, true);
+        compact<false>(total, c->cur, false, 0);
         const bool violated = c->n_confl > 0;
         g.sync();
         if (!keep_conflicts && g.leader()) c->n_confl = 0;
@@ -630,7 +913,7 @@ struct Search {
             const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
             for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
             sl.dovf[a] = 0;
-            sl.cells[a] = 0;
+            set_cell(a, 0);
             sl.tpos[a] = 0;
             sl.reason[a] = kReasonNone;
         }
@@ -731,7 +1014,7 @@ struct Search {
         std::int32_t rem = 0;
         for (std::uint32_t k = 0; k < len; ++k) {
             const std::int32_t l = lit_at(L, k, id);
-            const std::int32_t cv = sl.cells[atom_of(l)];
+            const int cv = val(atom_of(l));
             if (cv == 0) {
                 if (rem != 0) return;
                 rem = l;
@@ -747,7 +1030,7 @@ struct Search {
         const std::int32_t lit = -rem;
         const std::uint32_t a = atom_of(lit), cdl = c->cdl;
         write_deps_from(L, len, id, a, cdl);
-        sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl);
+        set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
         sl.reason[a] = static_cast<std::int32_t>(id);
         sl.tpos[a] = c->ts;
         sl.trail[c->ts++] = lit;
@@ -760,7 +1043,7 @@ struct Search {
         const std::int32_t* L = lits_of(id, len);
         for (std::uint32_t k = 0; k < len; ++k) {
             const std::int32_t l = lit_at(L, k, id);
-            const std::int32_t cv = sl.cells[atom_of(l)];
+            const int cv = val(atom_of(l));
             if (cv == 0) ++nfree;
             else if ((cv > 0) != (l > 0)) return false;
         }
@@ -992,9 +1275,9 @@ struct Search {
             const uint4 ru = __ldg(S.rules + r);
             if (ru.w >> 31) continue;
             const std::uint32_t n = ru.w & 0x7fffffffu;
-            if (sl.cells[ru.x] != 0) continue;
-            if (ru.z != 0 && sl.cells[ru.z] <= 0) continue;
-            if (n != 0 && sl.cells[n] < 0) continue;
+            if (val(ru.x) != 0) continue;
+            if (ru.z != 0 && val(ru.z) <= 0) continue;
+            if (n != 0 && val(n) < 0) continue;
             const double s = score(ru.x);
             if (better(s, r, best, bi)) { best = s; bi = r; }
         }
@@ -1004,7 +1287,7 @@ struct Search {
                 const std::uint32_t b = __ldg(S.rules + bi).y;
                 const std::uint32_t cdl = ++c->cdl;
                 sl.ldec[cdl] = static_cast<std::int32_t>(b);
-                sl.cells[b] = static_cast<std::int32_t>(cdl);
+                set_cell(b, static_cast<std::int32_t>(cdl));
                 sl.tpos[b] = c->ts;
                 sl.trail[c->ts++] = static_cast<std::int32_t>(b);
                 sl.reason[b] = kReasonDecision;
@@ -1026,11 +1309,11 @@ struct Search {
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < np; base += g.size()) {
             const std::uint32_t a = base + g.tid() + 1;
-            const bool open = a <= np && sl.cells[a] == 0;
+            const bool open = a <= np && val(a) == 0;
             unsigned long long tot;
             const std::uint32_t r = static_cast<std::uint32_t>(g.scan(open ? 1ull : 0ull, tot) + carry);
             if (open) {
-                sl.cells[a] = -static_cast<std::int32_t>(cdl);
+                set_cell(a, -static_cast<std::int32_t>(cdl));
                 sl.reason[a] = kReasonCompletion;
                 for (std::uint32_t w = 0; w < nw; ++w) {
                     unsigned long long m = 0;
@@ -1065,7 +1348,7 @@ struct Search {
             std::uint32_t bits = 0;
             for (std::uint32_t b = 0; b < 32; ++b) {
                 const std::uint32_t a = 32 * w + b + 1;
-                if (a <= S.n_prog && sl.cells[a] > 0) bits |= 1u << b;
+                if (a <= S.n_prog && val(a) > 0) bits |= 1u << b;
             }
             sl.mbuf[static_cast<std::size_t>(m) * words + w] = bits;
         }
@@ -1116,7 +1399,7 @@ struct Search {
             bool dead = false;
             for (std::uint32_t k = 0; k < len; ++k) {
                 const std::int32_t l = lit_at(L, k, id);
-                const std::int32_t cv = sl.cells[atom_of(l)];
+                const int cv = val(atom_of(l));
                 if (cv == 0) { ++nfree; open = l; }
                 else if ((cv > 0) == (l > 0)) ++nhold;
                 else dead = true;
@@ -1137,7 +1420,7 @@ struct Search {
             const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
             for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
             sl.dovf[a] = 0;
-            sl.cells[a] = 0;
+            set_cell(a, 0);
             sl.tpos[a] = 0;
             sl.reason[a] = kReasonNone;
         }
@@ -1160,6 +1443,7 @@ struct Search {
             sl.loff[0] = 0;
             c->cube = cube;
             c->epoch += 1;
+            if (c->gen == 0) c->gen = 1;  // claim/win keys of generation 0 equal the all-ones init
             c->pad0 = 0;
             c->restart_threshold = C.restart_base;
             c->conflicts_at_restart = c->st.conflicts;
@@ -1234,7 +1518,10 @@ struct Search {
                 conflicted = true;
             }
             if (conflicted) {
-                if (!handle_conflicts()) {
+                mark(0);
+                const bool go_on = handle_conflicts();
+                mark(7);
+                if (!go_on) {
                     if (c->status != kRunning) return;
                     if (g.leader()) c->phase = kFinished;
                     g.sync();
@@ -1247,7 +1534,9 @@ struct Search {
                 if (c->status != kRunning) return;
             }
             if (c->ts != S.A) {
+                mark(0);
                 decide_or_complete();
+                mark(6);
                 continue;
             }
             record_model(c->cube);
@@ -1261,9 +1550,25 @@ struct Search {
 // Kernels
 // ---------------------------------------------------------------------------
 template <class G>
-__device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh) {
+__device__ void init_smem(G& g, Search<G>& s) {
+    const Sm& m = s.sm;
+    if (m.tcap) {
+        for (std::uint32_t i = g.tid(); i <= m.hmask; i += g.size()) {
+            m.htab[i] = 0ull;
+            m.wtab[i] = 0ull;
+        }
+        for (std::uint32_t i = g.tid(); i < (m.tcap + 31) / 32; i += g.size()) m.bits[i] = 0u;
+    }
+    s.rebuild_mirror();
+    g.sync();
+}
+
+template <class G>
+__device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh,
+                          const Sm& sm) {
     const unsigned long long t0 = gtimer();
-    Search<G> s(g, S, C, sl, K, sh, t0);
+    Search<G> s(g, S, C, sl, K, sh, t0, sm);
+    init_smem(g, s);
     for (;;) {
         g.sync();
         if (g.c->status != kRunning) return;
@@ -1288,7 +1593,8 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl
 
 template <int BS>
 __global__ void __launch_bounds__(BS) block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                   Shared* sh) {
+                                                   Shared* sh, SmemCfg smc) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ Ctl ctl;
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
@@ -1302,7 +1608,7 @@ __global__ void __launch_bounds__(BS) block_kernel(Static S, Config C, const Slo
     __syncthreads();
     if (threadIdx.x == 0 && ctl.status == kYield) ctl.status = kRunning;
     BlockG<BS> g{&ctl, sbuf, sd, si};
-    slot_loop(g, S, C, sl, K, sh);
+    slot_loop(g, S, C, sl, K, sh, carve_smem(dsm, smc));
     __syncthreads();
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
@@ -1322,7 +1628,7 @@ __global__ void __launch_bounds__(BS) grid_kernel(Static S, Config C, const Slot
     GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
     if (g.leader() && sl.ctl->status == kYield) sl.ctl->status = kRunning;
     g.sync();
-    slot_loop(g, S, C, sl, K, sh);
+    slot_loop(g, S, C, sl, K, sh, Sm{});
 }
 
 // Low-level operations on one slot (Propagator-style API for tests and the
@@ -1342,8 +1648,9 @@ struct OpArgs {
 
 template <class G>
 __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh,
-                      const OpArgs& op) {
-    Search<G> s(g, S, C, sl, K, sh, 0);
+                      const OpArgs& op, const Sm& sm) {
+    Search<G> s(g, S, C, sl, K, sh, 0, sm);
+    init_smem(g, s);
     Ctl* c = g.c;
     switch (op.op) {
         case kOpReset:
@@ -1373,7 +1680,7 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
                 const std::uint32_t a = atom_of(lit);
                 const std::uint32_t cdl = ++c->cdl;
                 sl.ldec[cdl] = lit;
-                sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl);
+                s.set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
                 sl.tpos[a] = c->ts;
                 sl.trail[c->ts++] = lit;
                 sl.reason[a] = kReasonDecision;
@@ -1388,8 +1695,8 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
                 for (std::uint32_t k = 0; k < op.n; ++k) {
                     const std::int32_t lit = op.lits[k];
                     const std::uint32_t a = atom_of(lit);
-                    if (sl.cells[a] != 0) continue;
-                    sl.cells[a] = lit > 0 ? static_cast<std::int32_t>(op.level) : -static_cast<std::int32_t>(op.level);
+                    if (s.val(a) != 0) continue;
+                    s.set_cell(a, lit > 0 ? static_cast<std::int32_t>(op.level) : -static_cast<std::int32_t>(op.level));
                     sl.tpos[a] = c->ts;
                     sl.trail[c->ts++] = lit;
                     sl.reason[a] = op.antecedent;
@@ -1421,7 +1728,8 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
 
 template <int BS>
 __global__ void __launch_bounds__(BS) op_block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                      Shared* sh, OpArgs op) {
+                                                      Shared* sh, OpArgs op, SmemCfg smc) {
+    extern __shared__ __align__(16) unsigned char dsm[];
     __shared__ Ctl ctl;
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
@@ -1434,7 +1742,7 @@ __global__ void __launch_bounds__(BS) op_block_kernel(Static S, Config C, const 
     }
     __syncthreads();
     BlockG<BS> g{&ctl, sbuf, sd, si};
-    do_op(g, S, C, sl, K, sh, op);
+    do_op(g, S, C, sl, K, sh, op, carve_smem(dsm, smc));
     __syncthreads();
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
@@ -1452,7 +1760,7 @@ __global__ void __launch_bounds__(BS) op_grid_kernel(Static S, Config C, const S
     __shared__ std::uint32_t si[BS / 32];
     const Slot sl = slots[0];
     GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
-    do_op(g, S, C, sl, K, sh, op);
+    do_op(g, S, C, sl, K, sh, op, Sm{});
 }
 
 }  // namespace yas::dev

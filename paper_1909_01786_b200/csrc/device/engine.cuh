@@ -86,6 +86,8 @@ struct Ctl {
     double act_inc;
     std::uint32_t b[16];  // leader -> group broadcast scratch
     Stats st;
+    unsigned long long prof[10];  // clock64 cycles per phase (leader view, after barriers)
+    unsigned long long prof_t;
 };
 
 struct Caps {

@@ -1,6 +1,7 @@
 // Host side of the engine: uploads, per-slot arenas, the launch/drain loop.
 // Included at the end of engine.cu (needs the kernel templates).
 #include <chrono>
+#include <cstdlib>
 
 namespace yas {
 
@@ -192,6 +193,22 @@ struct Arena {
     std::size_t pool_size_ = 0;
 };
 
+// Shared-memory working set of a single-CTA search: pass scratch for up to
+// tcap expansion entries plus the 2-bit assignment mirror, within `budget`.
+dev::SmemCfg plan_smem(std::uint32_t atoms, std::size_t budget) {
+    dev::SmemCfg c{};
+    const std::uint32_t vw = (atoms + 1 + 31) / 32;
+    if (2ull * 4 * vw + 64 <= budget / 2) c.vwords = vw;
+    for (std::uint32_t t = 16384; t >= 128; t /= 2) {
+        dev::SmemCfg x = c;
+        x.tcap = t;
+        x.hcap = 2 * t;
+        x.fcap = t + 1;
+        if (dev::smem_bytes(x) <= budget) return x;
+    }
+    return c;
+}
+
 std::uint32_t grid_blocks_for(int device) {
     int sms = 0, per = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
@@ -230,6 +247,20 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     ck(cudaEventCreate(&e1), "event");
     std::vector<dev::Ctl> ctl(n_slots);
     std::vector<std::uint32_t> mb, mc;
+    dev::SmemCfg smc{};
+    std::size_t smem = 0;
+    if (!opt.grid) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
+        const std::uint32_t per_sm = std::min<std::uint32_t>(4, (n_slots + sms - 1) / sms);
+        // keep most of the unified L1 for the (read-only) static store
+        const std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
+        smc = plan_smem(ar.A, budget);
+        smem = dev::smem_bytes(smc);
+        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)),
+           "smem attribute");
+    }
     bool stop_early = false;
     for (;;) {
         ck(cudaEventRecord(e0), "record");
@@ -239,7 +270,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            dev::block_kernel<kBlockBS><<<n_slots, kBlockBS>>>(ar.S, cfg, ar.d_slots, ar.K, ar.sh);
+            dev::block_kernel<kBlockBS><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.d_slots, ar.K, ar.sh, smc);
             ck(cudaGetLastError(), "block launch");
         }
         ck(cudaEventRecord(e1), "record");
@@ -293,6 +324,16 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     };
     for (const dev::Ctl& c : ctl) add(tot, c.st);
     res.stats = tot;
+    if (std::getenv("YAS_PROFILE")) {
+        static const char* names[10] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
+                                        "conflict", "-", "-"};
+        unsigned long long p[10] = {0};
+        for (const dev::Ctl& c : ctl)
+            for (int k = 0; k < 10; ++k) p[k] += c.prof[k];
+        std::fprintf(stderr, "[yas profile] passes=%llu", static_cast<unsigned long long>(tot.passes));
+        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s=%.1fMcyc", names[k], p[k] / 1e6);
+        std::fprintf(stderr, "\n");
+    }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     res.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
@@ -304,6 +345,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
 // ---------------------------------------------------------------------------
 struct Session::Impl {
     Arena ar;
+    dev::SmemCfg smc{};
+    std::size_t smem = 0;
     dev::Config cfg{};
     bool grid = false;
     std::uint32_t gblocks = 0;
@@ -321,6 +364,13 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     impl_->ar.upload_static(store, {}, 0, {});
     impl_->gblocks = grid ? grid_blocks_for(device) : 0;
     impl_->ar.alloc_slots(1, deps_words, lcap, lpool, 16, 128, 0, impl_->gblocks);
+    if (!grid) {
+        impl_->smc = plan_smem(impl_->ar.A, 96u * 1024u);
+        impl_->smem = dev::smem_bytes(impl_->smc);
+        ck(cudaFuncSetAttribute(dev::op_block_kernel<kBlockBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(impl_->smem)),
+           "smem attribute");
+    }
     dev::Config& c = impl_->cfg;
     c.W = deps_words;
     c.decay = 0.95;
@@ -349,7 +399,8 @@ void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
                                        dim3(kGridBS), args, 0, nullptr),
            "op grid launch");
     } else {
-        dev::op_block_kernel<kBlockBS><<<1, kBlockBS>>>(im.ar.S, im.cfg, im.ar.d_slots, im.ar.K, im.ar.sh, op);
+        dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem>>>(im.ar.S, im.cfg, im.ar.d_slots, im.ar.K, im.ar.sh, op,
+                                                                im.smc);
         ck(cudaGetLastError(), "op launch");
     }
     cudaEventRecord(im.e1);

@@ -90,12 +90,26 @@ def propstores():
     }
 
 
+def dumps():
+    """compile_completion + NogoodStore::build goldens for the corpus and the config instances."""
+    progs = ref(["corpus"])
+    texts = [(p["name"], p["text"]) for p in progs]
+    texts += [("queens8", I.queens(8)), ("queens5", I.queens(5)), ("ham12", I.hamiltonian(12, 1.0, 3)),
+              ("colour30", I.colouring(30, 4.0, 3, 7)), ("php43", I.pigeonhole(4, 3))]
+    out = []
+    for name, text in texts:
+        d = ref(["dump", "-"], stdin=text)
+        d["name"], d["text"] = name, text
+        out.append(d)
+    return out
+
+
 def planted():
     return [ref(["planted", "20000", "200000", str(p), "0x1b00b5"]) for p in (1, 10, 50, 90)]
 
 
 def main():
-    targets = sys.argv[1:] or ["corpus", "extras", "configs", "propstores", "planted"]
+    targets = sys.argv[1:] or ["corpus", "extras", "configs", "propstores", "planted", "dumps"]
     for t in targets:
         data = globals()[t]()
         with open(os.path.join(HERE, f"{t}.json"), "w") as f:

@@ -1,0 +1,146 @@
+"""Propagation on the device vs the reference Propagator (P/tests/test_propagate.cpp),
+through the C-ABI. Both engines: one CTA per search ("block") and whole grid ("grid")."""
+import pytest
+
+import paper_1909_01786_b200 as Y
+
+from _util import golden
+
+pytestmark = pytest.mark.gpu
+ENGINES = ["block", "grid"]
+
+
+def fnv(trail):
+    h = 0xcbf29ce484222325
+    for c in trail:
+        h = ((h ^ (c & 0xFFFFFFFF)) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_initial_propagation_forces_unit_complements(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1], [2]], 2), 1, engine)
+    o = p.initial_propagation()
+    assert not o.violated and p.cells()[1:] == [-1, -1] and o.propagations == 2 and len(p.frontier()) == 2
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_inconsistent_units_violate_with_pseudo_id(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1], [-1]], 1), 1, engine)
+    o = p.initial_propagation()
+    assert o.violated and len(o.conflicts) == 1 and o.conflicts[0] < 0
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_learned_units_replayed(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2]], 3), 1, engine)
+    lid = p.add_learned([3])
+    assert lid == 1
+    o = p.initial_propagation()
+    assert not o.violated and p.cells()[3] == -1
+    again = p.initial_propagation()
+    assert not again.violated and p.frontier() == []
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_unit_propagation_copies_deps(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2]], 2), 2, engine)
+    p.push_decision(1)
+    p.seed([1])
+    o = p.propagate_and_check(2)
+    assert not o.violated and p.cells()[2] == -2 and p.reasons()[2] == 0 and o.propagations == 1
+    d, _ = p.deps(0)
+    assert d[1] == d[2] == 0b10
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_race_first_in_item_order_wins(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2], [1, -2]], 2), 1, engine)
+    p.push_decision(1)
+    p.seed([1])
+    o = p.propagate_and_check(2)
+    assert o.violated and p.cells()[2] == -2 and o.conflicts == [1]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_violation_and_chain(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2, 3]], 3), 1, engine)
+    p.push_decision(1)
+    p.push_decision(2)
+    p.assign_propagated([3], 3, [0b100])
+    p.seed([3])
+    o = p.propagate_and_check(3)
+    assert o.violated and o.conflicts == [0]
+    q = Y.Propagator(Y.NogoodStore.build([[1, 2], [-2, -3], [3, 4]], 4), 1, engine)
+    q.push_decision(1)
+    q.seed([1])
+    o = q.propagate_and_check(2)
+    assert not o.violated and o.propagations == 3 and o.passes >= 3
+    assert q.cells()[2:] == [-2, 2, -2]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+@pytest.mark.parametrize("key", ["test_propagate", "criterion5"])
+def test_random_stores_match_reference(engine, key):
+    """300 + 1000 random stores: outcome, cells, trail order, reasons and Deps."""
+    for st in golden("propstores")[key]:
+        p = Y.Propagator(Y.NogoodStore.build(st["nogoods"], 10), 1, engine)
+        o = p.initial_propagation()
+        assert o.violated == bool(st["init_violated"])
+        assert sorted(o.conflicts) == sorted(st["init_conflicts"]) and o.propagations == st["init_props"]
+        if not o.violated:
+            o = p.propagate_and_check(1)
+            assert (o.violated, o.propagations, o.passes) == (bool(st["l1_violated"]), st["l1_props"], st["l1_passes"])
+            assert sorted(o.conflicts) == sorted(st["l1_conflicts"])
+            if not o.violated and st["decision"]:
+                p.push_decision(st["decision"])
+                p.seed([st["decision"]])
+                o = p.propagate_and_check(2)
+                assert (o.violated, o.propagations, o.passes) == (bool(st["l2_violated"]), st["l2_props"],
+                                                                  st["l2_passes"])
+                assert sorted(o.conflicts) == sorted(st["l2_conflicts"])
+        assert p.cells() == st["cells"] and p.trail() == st["trail"] and p.reasons() == st["reasons"]
+        d, ov = p.deps(0)
+        assert [x | (1 << 63 if v else 0) for x, v in zip(d, ov)] == st["deps"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_planted_fixpoint_matches_reference(engine):
+    """200k-nogood planted stores (App. C recipe) at 1/10/50/90 % seeds: identical
+    propagation count, pass count and trail (FNV digest of the literal sequence)."""
+    for exp in golden("planted"):
+        s, seeded, dec = Y.NogoodStore.planted(exp["atoms"], exp["nogoods"], exp["pct"])
+        p = Y.Propagator(s, 16, engine)
+        p.push_decision(dec)
+        p.assign_propagated(seeded, 2)
+        p.seed([dec] + seeded)
+        o = p.propagate_and_check(2)
+        tr = p.trail()
+        assert not o.violated
+        assert (o.propagations, o.passes, len(tr)) == (exp["propagations"], exp["passes"], exp["trail"])
+        assert fnv(tr) == exp["trail_digest"]
+
+
+def test_planted_1m_properties():
+    """Full-size config 4b (1M nogoods, 100k atoms, 50 % seed): size-independent
+    properties — H satisfies every nogood, so no conflict may appear, every
+    propagated literal agrees with the planted assignment, and the fixpoint is
+    closed (re-propagating the whole trail derives nothing new)."""
+    s, seeded, dec = Y.NogoodStore.planted(100_000, 1_000_000, 50)
+    p = Y.Propagator(s, 16, "grid")
+    p.push_decision(dec)
+    p.assign_propagated(seeded, 2)
+    p.seed([dec] + seeded)
+    o = p.propagate_and_check(2)
+    assert not o.violated and o.checks > 500_000
+    tr = p.trail()
+    H = {abs(l): l for l in [dec] + seeded}
+    cells = p.cells()
+    # every assignment is consistent with H where H is known
+    for lit in tr:
+        if abs(lit) in H:
+            assert H[abs(lit)] == lit
+    before = len(tr)
+    p.seed(tr)
+    o2 = p.propagate_and_check(2)
+    assert not o2.violated and o2.propagations == 0 and len(p.trail()) == before

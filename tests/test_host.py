@@ -1,0 +1,145 @@
+"""Host side of the drop-in boundary (CPU only): parser, completion compiler and
+store builder must produce exactly the reference's atom ids, nogood ids, CSR
+layout, guards and unit lists."""
+import pytest
+
+import paper_1909_01786_b200 as Y
+from paper_1909_01786_b200 import aspine as A
+from paper_1909_01786_b200 import instances as I
+
+from _util import golden
+
+
+# ---- parser: P/tests/test_program.cpp ----------------------------------------
+def test_parses_facts_rules_constraints():
+    p = Y.parse_program("a.\nb :- a, not c.\n:- b, c.")
+    assert p.atom_count() == 3 and p.rule_count() == 2 and p.constraint_count() == 1
+    (h0, p0, n0), (h1, p1, n1) = p.rules()
+    assert (h0, p0, n0) == (1, [], [])
+    assert h1 == p.find("b") and p1 == [p.find("a")] and n1 == [p.find("c")]
+    assert p.constraints()[0][1] == [p.find("b"), p.find("c")]
+
+
+def test_interning_order_and_duplicates():
+    p = Y.parse_program("x :- y, not z.\ny.\n")
+    assert (p.find("x"), p.find("y"), p.find("z")) == (1, 2, 3)
+    q = Y.parse_program("a :- b, b, not c, not c.")
+    assert q.rules()[0][1:] == ([2], [3])
+    s = Y.parse_program("a :- not a.")
+    assert s.rules() == [(1, [], [1])]
+
+
+def test_comments_blank_lines_and_parenthesised_names():
+    p = Y.parse_program("% a comment line\n\nat(1,2) :- step(1), not wall(1,2).  % trailing comment\n")
+    assert p.atom_count() == 3 and p.find("at(1,2)") == 1 and p.find("wall(1,2)") == 3
+
+
+@pytest.mark.parametrize("text,line", [
+    ("a.\nb :- \nc.", 2), ("a.\nb :- ,c.\n", 2), ("a. b.", 1), ("a :- not .", 1), ("a :- b", 1),
+    ("p(1 :- q.", 1), ("x(a b).", 1), (":- .", 1), ("ok.\n\n% c\nbad :- x,", 4)])
+def test_syntax_errors_carry_line_numbers(text, line):
+    with pytest.raises(Y.ParseError) as e:
+        Y.parse_program(text)
+    assert e.value.line == line
+    assert str(e.value).startswith(f"line {line}: ")
+
+
+def test_tp_step_and_validate():
+    p = Y.parse_program("a.\nb :- a.")
+    assert Y.tp_step(p, []) == [1] and Y.tp_step(p, [1]) == [1, 2]
+    q = Y.parse_program("a :- not b.\nb :- not a.")
+    assert Y.tp_step(q, [1]) == [1]
+    assert Y.validate(Y.parse_program("b :- a.")) == ["atom a has no rules"]
+    assert "rule 1 body is inconsistent" in Y.validate(Y.parse_program("a :- b, not b."))
+    assert Y.validate(Y.parse_program("a.")) == []
+    assert Y.validate(Y.parse_program("")) == ["empty program"]
+
+
+def test_print_matches_reference_and_round_trips():
+    """print_program(parse_program(text)) equals the reference's output; a second
+    round trip is a fixpoint (test_program.cpp print/parse round-trip)."""
+    for d in golden("dumps"):
+        p = Y.parse_program(d["text"])
+        printed = Y.print_program(p)
+        assert printed == d["printed"], d["name"]
+        assert Y.print_program(Y.parse_program(printed)) == printed
+
+
+# ---- completion + store goldens: test_completion.cpp:19-37, test_store.cpp:62 --
+def test_completion_golden_dump():
+    p = Y.parse_program("a :- b, not c.")
+    assert p.rule_aux(0) == {"b": 4, "t": 5, "n": 6, "vacuous": False}
+    assert p.total_atoms() == 6
+    assert Y.dump_nogoods(p) == (
+        "{F b_r(1), T t_r(1), T n_r(1)} completion\n{T b_r(1), F t_r(1)} completion\n"
+        "{T b_r(1), F n_r(1)} completion\n{F b, T t_r(1)} completion\n{T b, F t_r(1)} completion\n"
+        "{T c, T n_r(1)} completion\n{F c, F n_r(1)} completion\n{F a, T b_r(1)} completion\n"
+        "{T a, F b_r(1)} completion\n{T b} completion\n{T c} completion\n")
+    assert p.census() == ((7, 4, 0), (7, 4, 0))
+
+
+def test_store_golden_csv():
+    s = Y.NogoodStore.build([[1, 2, 3], [-4], [1, -2], [-3, 5]], 5)
+    assert s.dump_csv() == "offsets,0,2,4,7\npool,1,-2,-3,5,1,2,3\n"
+    assert s.static_units() == [-4] and s.static_class_bounds() == [0, 2, 3, 3]
+    e = Y.NogoodStore.build([], 3)
+    assert e.dump_csv() == "offsets,0\npool\n" and e.size() == 0
+
+
+def test_vacuous_nogood_rejected():
+    with pytest.raises(ValueError):
+        Y.NogoodStore.build([[1, -1]], 2)
+
+
+def test_dumps_match_reference_for_corpus_and_instances():
+    """Every program: aux ids, census, dump_nogoods text and the CSR store."""
+    for d in golden("dumps"):
+        p = Y.parse_program(d["text"])
+        assert p.atom_count() == d["atoms"] and p.total_atoms() == d["total_atoms"], d["name"]
+        assert [list(p.rule_aux(r).values()) for r in range(p.rule_count())] == [
+            [b, t, n, bool(v)] for b, t, n, v in d["aux"]], d["name"]
+        census, counts = p.census()
+        assert list(census) == d["census"] and list(counts) == d["counts"], d["name"]
+        assert Y.dump_nogoods(p) == d["dump"], d["name"]
+        assert Y.store_csv(p) == d["csv"], d["name"]
+
+
+def test_store_units_guards_and_occurrences():
+    """Static units, unit ids, class bounds and occurrence lists vs the reference build."""
+    for d in golden("dumps")[::7]:
+        p = Y.parse_program(d["text"])
+        # rebuild the store through the low-level API from the compiled nogoods
+        csv = d["csv"].splitlines()
+        offs = [int(x) for x in csv[0].split(",")[1:]]
+        pool = [int(x) for x in csv[1].split(",")[1:]] if "," in csv[1] else []
+        ngs = [pool[offs[i]:offs[i + 1]] for i in range(len(offs) - 1)]
+        s = Y.NogoodStore.build(ngs, d["total_atoms"], guards=d["store_guards"])
+        assert s.dump_csv() == d["csv"]
+        assert s.static_class_bounds()[:3] == d["bounds"][:3]
+        ids = set()
+        for a in range(1, d["total_atoms"] + 1):
+            for lit in (a, -a):
+                for c in range(4):
+                    occ = s.occurrences(lit, c)
+                    assert occ == sorted(occ)
+                    for i in occ:
+                        assert lit in ngs[i] and min(len(ngs[i]), 4) - 1 == c
+                        ids.add((lit, i))
+        assert len(ids) == len(pool)
+
+
+def test_planted_store_matches_reference_generator():
+    for exp in golden("planted"):
+        s, seeded, dec = Y.NogoodStore.planted(exp["atoms"], exp["nogoods"], exp["pct"])
+        assert s.size() + len(s.static_units()) == exp["nogoods"] and len(seeded) == exp["seeded"]
+        assert abs(dec) == 1
+
+
+def test_cube_partition_covers_all_patterns():
+    p = Y.parse_program(I.queens(6))
+    full = A.cubes(p, 5)
+    assert len(full) == 32 and len({tuple(c) for c in full}) == 32
+    parts = [A.cubes(p, 5, r, 3) for r in range(3)]
+    assert sorted(tuple(c) for part in parts for c in part) == sorted(tuple(c) for c in full)
+    atoms = {abs(x) for c in full for x in c}
+    assert atoms == {p.find(f"q(1,{j})") for j in range(1, 6)}  # partners nq(.) are skipped

@@ -73,12 +73,16 @@ uint32_t yas_program_total_atoms(const yas_program* p); /* AuxMap::total_atoms *
 int yas_program_census(const yas_program* p, uint64_t census[3], uint64_t counts[3]);
 /* tp_step (program.hpp:96): interp sorted; out gets up to cap ids; returns count. */
 size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap);
-/* Cube split used by yas_solve when cfg.cube_atoms > 0: the first k choice
- * atoms (a with "a :- not b." and "b :- not a."), and the cubes of `rank`
- * (pattern i runs on rank i % world). Each cube is k nogood literals: +a for
- * ":- a." and -a for ":- not a.". Returns the cube count; host-only. */
-size_t yas_program_cubes(const yas_program* p, uint32_t k, int rank, int world, int32_t* out, size_t cap,
-                         uint32_t* width);
+/* Cube split used by yas_solve when cfg.cube_atoms > 0. Choice atoms are
+ * atoms a whose only rule is "a :- not b." with "b :- not a." present. The
+ * first depth*k of them form `depth` nested ladders of width k: per level a
+ * cube fixes (F a_0..F a_{i-1}, T a_i) or all F, so the (k+1)^depth cubes
+ * partition the answer sets. depth 0 = smallest depth with >= want cubes.
+ * Cube c runs on rank c % world. Each cube is width = depth*k unit-nogood
+ * literals (0 = none): +a (":- a.") or +b (":- b.", i.e. T a). Returns this
+ * rank's cube count; host-only. */
+size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
+                         int32_t* out, size_t cap, uint32_t* width);
 /* verify_model (solver.hpp:116): 1 when the sorted atom set is an answer set. */
 int yas_verify_model(const yas_program* p, const uint32_t* atom_ids, size_t n);
 
@@ -112,7 +116,8 @@ typedef struct yas_config {
     /* device extensions */
     int device;          /* CUDA ordinal */
     int engine;          /* 0 auto, 1 one CTA per search, 2 whole-grid search */
-    uint32_t cube_atoms; /* enumeration split over the first k choice atoms (0 = single search) */
+    uint32_t cube_atoms; /* enumeration split: ladder width k over choice atoms (0 = single search) */
+    uint32_t cube_depth; /* ladder levels (0 = auto: enough cubes for every search slot) */
     uint32_t slots;      /* concurrent searches per GPU for cubes (0 = auto) */
     int rank, world;     /* cube partition across processes/GPUs: cube i runs on rank i % world */
 } yas_config;

@@ -48,7 +48,8 @@ class yas_config(C.Structure):
         ("max_models", C.c_uint64), ("deps_words", C.c_uint32), ("conflict_fanout", C.c_uint32),
         ("seed", C.c_uint64), ("verify", C.c_int), ("debug_validate", C.c_int),
         ("learned_capacity", C.c_uint64), ("trace", TRACE_FN), ("trace_user", C.c_void_p),
-        ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("slots", C.c_uint32),
+        ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("cube_depth", C.c_uint32),
+        ("slots", C.c_uint32),
         ("rank", C.c_int), ("world", C.c_int),
     ]
 
@@ -103,7 +104,7 @@ def lib() -> C.CDLL:
         "yas_program_total_atoms": (U32, [P]),
         "yas_program_census": (C.c_int, [P, pU64, pU64]),
         "yas_program_tp_step": (SZ, [P, pU32, SZ, pU32, SZ]),
-        "yas_program_cubes": (SZ, [P, U32, C.c_int, C.c_int, pI32, SZ, pU32]),
+        "yas_program_cubes": (SZ, [P, U32, U32, U32, C.c_int, C.c_int, pI32, SZ, pU32]),
         "yas_verify_model": (C.c_int, [P, pU32, SZ]),
         "yas_config_default": (None, [C.POINTER(yas_config)]),
         "yas_solve": (C.c_int, [P, C.POINTER(yas_config), C.POINTER(P), C.c_char_p, SZ]),

@@ -128,6 +128,7 @@ class SolverConfig:
     device: int = 0
     engine: str = "auto"  # "auto" | "block" | "grid"
     cube_atoms: int = 0
+    cube_depth: int = 0
     slots: int = 0
     rank: int = 0
     world: int = 1
@@ -319,12 +320,12 @@ def tp_step(prog: GroundProgram, interp: Sequence[int]) -> List[int]:
     return list(out[:n])
 
 
-def cubes(prog: GroundProgram, k: int, rank: int = 0, world: int = 1):
-    """Cube split used by solve(cube_atoms=k): list of cubes (nogood literals) of this rank."""
+def cubes(prog: GroundProgram, k: int, depth: int = 1, rank: int = 0, world: int = 1, want: int = 0):
+    """Cube split used by solve(cube_atoms=k, cube_depth=depth): this rank's cubes (unit nogood literals)."""
     width = C.c_uint32(0)
-    n = N.lib().yas_program_cubes(prog._h, k, rank, world, None, 0, C.byref(width))
+    n = N.lib().yas_program_cubes(prog._h, k, depth, want, rank, world, None, 0, C.byref(width))
     out = (C.c_int32 * max(1, n * max(1, width.value)))()
-    N.lib().yas_program_cubes(prog._h, k, rank, world, out, n * width.value, C.byref(width))
+    N.lib().yas_program_cubes(prog._h, k, depth, want, rank, world, out, n * width.value, C.byref(width))
     w = width.value
     return [list(out[i * w:(i + 1) * w]) for i in range(n)]
 
@@ -354,6 +355,7 @@ def _config(cfg: SolverConfig) -> N.yas_config:
     c.device = cfg.device
     c.engine = {"auto": 0, "block": 1, "grid": 2}[cfg.engine]
     c.cube_atoms = cfg.cube_atoms
+    c.cube_depth = cfg.cube_depth
     c.slots = cfg.slots
     c.rank = cfg.rank
     c.world = cfg.world

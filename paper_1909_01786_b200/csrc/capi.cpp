@@ -119,45 +119,74 @@ int guarded(char* err, std::size_t cap, F&& f) {
     }
 }
 
-// Choice atoms: a with rules "a :- not b." and "b :- not a." (the even-loop
-// choice encoding). The first k of them, partners skipped, define the cubes.
-std::vector<AtomId> choice_atoms(const Program& prog, std::uint32_t k) {
-    std::vector<AtomId> partner(prog.atom_count() + 1, 0);
-    for (const Rule& r : prog.rules())
-        if (r.pos_body.empty() && r.neg_body.size() == 1) {
-            const AtomId a = r.head, b = r.neg_body[0];
-            for (std::uint32_t ri : prog.rules_of(b)) {
-                const Rule& s = prog.rules()[ri];
-                if (s.pos_body.empty() && s.neg_body.size() == 1 && s.neg_body[0] == a) {
-                    partner[a] = b;
-                    break;
-                }
-            }
-        }
-    std::vector<AtomId> out;
+// Choice atoms: a whose only rule is "a :- not b." where b has the rule
+// "b :- not a." (the even-loop choice encoding). For such an atom
+//   T a  <=>  F b   and the constraint ":- not a." is equivalent to ":- b.",
+// so both cube polarities can be stated as *forcing* unit nogoods: F a as
+// {T a}, T a as {T b}. Partners are skipped (b is determined by a).
+struct Choice {
+    AtomId a, b;
+};
+
+std::vector<Choice> choice_atoms(const Program& prog) {
+    std::vector<Choice> out;
     std::vector<char> taken(prog.atom_count() + 1, 0);
-    for (AtomId a = 1; a <= prog.atom_count() && out.size() < k; ++a) {
-        if (!partner[a] || taken[a]) continue;
-        out.push_back(a);
-        taken[a] = taken[partner[a]] = 1;
+    for (AtomId a = 1; a <= prog.atom_count(); ++a) {
+        if (taken[a] || prog.rules_of(a).size() != 1) continue;
+        const Rule& r = prog.rules()[prog.rules_of(a)[0]];
+        if (!r.pos_body.empty() || r.neg_body.size() != 1 || r.neg_body[0] == a) continue;
+        const AtomId b = r.neg_body[0];
+        bool pair = false;
+        for (std::uint32_t ri : prog.rules_of(b)) {
+            const Rule& q = prog.rules()[ri];
+            pair |= q.pos_body.empty() && q.neg_body.size() == 1 && q.neg_body[0] == a;
+        }
+        if (!pair) continue;
+        out.push_back({a, b});
+        taken[a] = taken[b] = 1;
     }
     return out;
 }
 
-// Every sign pattern over the first k choice atoms, as integrity constraints
-// (":- a." -> nogood {T a}; ":- not a." -> {F a}); pattern i belongs to rank
-// i % world. Returns the number of cubes of this rank.
-std::uint32_t make_cubes(const Program& prog, std::uint32_t k, int rank, int world, std::vector<std::int32_t>& cubes,
-                         std::uint32_t& width) {
-    const std::vector<AtomId> ca = choice_atoms(prog, std::min<std::uint32_t>(k, 24));
-    width = static_cast<std::uint32_t>(ca.size());
-    const std::uint32_t total = 1u << width;
-    std::uint32_t n = 0;
+// Nested "ladder" cubes over windows of L choice atoms: at each of d levels the
+// cube picks i in [0, L]: i < L means (F a_0, ..., F a_{i-1}, T a_i) and i = L
+// means all F. The (L+1)^d cubes partition the answer sets exactly. Cube c
+// belongs to rank c % world. Returns this rank's cube count.
+std::uint32_t make_cubes(const Program& prog, std::uint32_t L, std::uint32_t depth, std::uint32_t want, int rank,
+                         int world, std::vector<std::int32_t>& cubes, std::uint32_t& width) {
+    const std::vector<Choice> ch = choice_atoms(prog);
     cubes.clear();
-    for (std::uint32_t pat = 0; pat < total; ++pat) {
-        if (static_cast<int>(pat % static_cast<std::uint32_t>(world < 1 ? 1 : world)) != rank) continue;
-        for (std::uint32_t j = 0; j < width; ++j)
-            cubes.push_back(((pat >> j) & 1u) ? -static_cast<std::int32_t>(ca[j]) : static_cast<std::int32_t>(ca[j]));
+    width = 0;
+    if (world < 1) world = 1;
+    if (L == 0 || ch.empty()) return rank == 0 ? 1u : 0u;
+    L = std::min<std::uint32_t>(L, static_cast<std::uint32_t>(ch.size()));
+    std::uint32_t maxd = static_cast<std::uint32_t>(ch.size()) / L;
+    if (depth == 0) {  // smallest depth giving `want` cubes, at most 2^17 cubes
+        depth = 1;
+        std::uint64_t n = L + 1;
+        while (n < want && depth < maxd && n * (L + 1) <= (1u << 17)) {
+            n *= L + 1;
+            ++depth;
+        }
+    }
+    depth = std::max<std::uint32_t>(1, std::min(depth, maxd));
+    width = depth * L;
+    std::uint64_t total = 1;
+    for (std::uint32_t j = 0; j < depth; ++j) total *= L + 1;
+    std::uint32_t n = 0;
+    for (std::uint64_t cube = 0; cube < total; ++cube) {
+        if (static_cast<int>(cube % static_cast<std::uint64_t>(world)) != rank) continue;
+        std::uint64_t digits = cube;
+        for (std::uint32_t j = 0; j < depth; ++j) {
+            const std::uint32_t pick = static_cast<std::uint32_t>(digits % (L + 1));
+            digits /= L + 1;
+            for (std::uint32_t i = 0; i < L; ++i) {
+                const Choice& c = ch[j * L + i];
+                if (i < pick) cubes.push_back(static_cast<std::int32_t>(c.a));        // F a: nogood {T a}
+                else if (i == pick) cubes.push_back(static_cast<std::int32_t>(c.b));  // T a: nogood {T b}
+                else cubes.push_back(0);
+            }
+        }
         ++n;
     }
     return n;
@@ -305,12 +334,12 @@ size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t 
     for (std::size_t i = 0; i < r.size() && i < cap; ++i) out[i] = r[i];
     return r.size();
 }
-size_t yas_program_cubes(const yas_program* p, uint32_t k, int rank, int world, int32_t* out, size_t cap,
-                         uint32_t* width) {
+size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
+                         int32_t* out, size_t cap, uint32_t* width) {
     if (!p) return 0;
     std::vector<std::int32_t> cubes;
     std::uint32_t w = 0;
-    const std::uint32_t n = make_cubes(p->prog, k, rank, world, cubes, w);
+    const std::uint32_t n = make_cubes(p->prog, k, depth, want ? want : 2368, rank, world, cubes, w);
     if (width) *width = w;
     for (std::size_t i = 0; i < cubes.size() && i < cap; ++i) out[i] = cubes[i];
     return n;
@@ -376,8 +405,12 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
 
         std::vector<std::int32_t> cubes;
         std::uint32_t width = 0, n_cubes = 1;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
+        const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * 4;
         if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
-            n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.rank, cfg.world, cubes, width);
+            n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * static_cast<std::uint32_t>(cfg.world),
+                                 cfg.rank, cfg.world, cubes, width);
         } else if (cfg.rank != 0) {
             n_cubes = 0;  // a single search runs on rank 0 only
         }
@@ -386,13 +419,12 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         eo.device = cfg.device;
         const bool wide = cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0);
         eo.grid = wide;
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
-        eo.slots = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * 4;
+        eo.slots = slots_per_gpu;
         const bool many = width > 0;
         const std::uint64_t cap = cfg.learned_capacity;
-        eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, many ? (1u << 14) : (1u << 18)));
-        eo.lpool = many ? (1u << 20) : (1u << 22);
+        eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, many ? (1u << 13) : (1u << 18)));
+        eo.lpool = many ? (1u << 16) : (1u << 22);
+        eo.slice_ms = 500.0;
 
         auto res = std::make_unique<yas_result>();
         for (int attempt = 0;; ++attempt) {

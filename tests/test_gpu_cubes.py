@@ -10,20 +10,21 @@ from _util import golden
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("k", [1, 4, 8, 12])
-def test_queens8_cube_split_model_set(k):
+@pytest.mark.parametrize("k,depth", [(1, 1), (4, 2), (8, 1), (8, 2), (8, 3), (5, 0)])
+def test_queens8_cube_split_model_set(k, depth):
     exp = golden("configs")["queens8/fwd/occ"]["models"]
-    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=0, cube_atoms=k))
+    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=0, cube_atoms=k, cube_depth=depth))
     got = sorted(m.atom_ids for m in r.models)
     assert got == sorted(exp) and len(got) == 92
-    assert r.stats.searches == 2 ** min(k, 64)
+    if depth:
+        assert r.stats.searches == (k + 1) ** depth
 
 
 def test_cube_split_by_rank_partitions_models():
     exp = sorted(golden("configs")["queens8/fwd/occ"]["models"])
     parts = []
     for rank in range(3):
-        r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=0, cube_atoms=6, rank=rank, world=3))
+        r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=0, cube_atoms=8, cube_depth=2, rank=rank, world=3))
         parts.append(sorted(m.atom_ids for m in r.models))
     allm = sorted(m for p in parts for m in p)
     assert allm == exp
@@ -31,12 +32,12 @@ def test_cube_split_by_rank_partitions_models():
 
 def test_corpus_cube_split_matches_families():
     for prog in golden("corpus")[::5]:
-        r = Y.solve(Y.parse_program(prog["text"]), Y.SolverConfig(max_models=0, cube_atoms=3))
+        r = Y.solve(Y.parse_program(prog["text"]), Y.SolverConfig(max_models=0, cube_atoms=3, cube_depth=2))
         assert sorted(m.atom_ids for m in r.models) == sorted(prog["family"]), prog["name"]
 
 
 def test_queens10_count():
-    r = Y.solve(Y.parse_program(I.queens(10)), Y.SolverConfig(max_models=0, cube_atoms=10))
+    r = Y.solve(Y.parse_program(I.queens(10)), Y.SolverConfig(max_models=0, cube_atoms=10, cube_depth=2))
     assert len(r.models) == 724 and len({tuple(m.atom_ids) for m in r.models}) == 724
     for m in r.models[:50]:
         assert Y.verify_model(Y.parse_program(I.queens(10)), m)

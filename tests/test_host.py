@@ -135,11 +135,16 @@ def test_planted_store_matches_reference_generator():
         assert abs(dec) == 1
 
 
-def test_cube_partition_covers_all_patterns():
+def test_ladder_cubes_partition_and_encoding():
     p = Y.parse_program(I.queens(6))
-    full = A.cubes(p, 5)
-    assert len(full) == 32 and len({tuple(c) for c in full}) == 32
-    parts = [A.cubes(p, 5, r, 3) for r in range(3)]
-    assert sorted(tuple(c) for part in parts for c in part) == sorted(tuple(c) for c in full)
-    atoms = {abs(x) for c in full for x in c}
-    assert atoms == {p.find(f"q(1,{j})") for j in range(1, 6)}  # partners nq(.) are skipped
+    one = A.cubes(p, 6, 1)
+    assert len(one) == 7
+    names = [[p.name(x) for x in c if x] for c in one]
+    # cube i: F q(1,1..i-1) as ":- q(1,j).", T q(1,i) as ":- nq(1,i)."; last cube: all F
+    assert names[0] == ["nq(1,1)"] and names[2] == ["q(1,1)", "q(1,2)", "nq(1,3)"]
+    assert names[6] == [f"q(1,{j})" for j in range(1, 7)]
+    two = A.cubes(p, 6, 2)
+    assert len(two) == 49 and len({tuple(c) for c in two}) == 49
+    parts = [A.cubes(p, 6, 2, r, 3) for r in range(3)]
+    assert sorted(tuple(c) for part in parts for c in part) == sorted(tuple(c) for c in two)
+    assert len(A.cubes(p, 6, 0, want=300)) == 343

@@ -28,7 +28,7 @@ def _worker(rank, world, port, q):
     from paper_1909_01786_b200 import aspine as A
     from paper_1909_01786_b200 import instances as I
     p = Y.parse_program(I.queens(6))
-    mine = A.cubes(p, 6, rank, world)
+    mine = A.cubes(p, 6, 2, rank, world)
     n = torch.tensor([len(mine)], dtype=torch.int64)
     dist.all_reduce(n)
     gathered = [None] * world
@@ -49,7 +49,7 @@ def test_cube_partition_allreduce_world2():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    assert total == 64
+    assert total == 49
     cubes = [c for part in gathered for c in part]
-    assert len(cubes) == 64 and len(set(cubes)) == 64
+    assert len(cubes) == 49 and len(set(cubes)) == 49
     assert not set(gathered[0]) & set(gathered[1])

@@ -1,0 +1,332 @@
+"""yasmin-b200 benchmark (driver contract: one JSON line from rank 0).
+
+Headline metric (BASELINE.json): nogood checks/s of propagation-to-fixpoint on
+the synthetic 1M-nogood / 100k-atom planted store (config 4b),
+with the HBM roofline of the propagation kernel; the same line carries the
+enumeration result (12-queens, all 14,200 answer sets, cube-split over the N
+GPUs) and the first-model configurations, each next to the reference CPU solver
+timed on this host.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl yasmin|reference]
+
+A "step" is one propagate_and_check call to fixpoint over the planted store.
+The propagation path does not shard (one fixpoint), so with N > 1 every rank
+runs a replica ("weak" scaling); enumeration cubes are partitioned over ranks
+and only the model count / time are all-reduced (NCCL).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PLANTED = dict(atoms=100_000, nogoods=1_000_000, pct=50, seed=0x1B00B5)
+WORKLOAD = "planted store: 1M nogoods, 100k atoms, len U[2,6], 50% of H seeded at level 2 (SURVEY.md App. C, 4b)"
+REF_BIN = os.path.join(ROOT, "oracle", "_ref", "aspine_ref")
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def allreduce(vals, op="max", world=1):
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def run_reference_planted(reps):
+    """Unmodified reference (oracle/_ref): Propagator::propagate_and_check on the same store."""
+    out = subprocess.run([REF_BIN, "planted", str(PLANTED["atoms"]), str(PLANTED["nogoods"]), str(PLANTED["pct"]),
+                          hex(PLANTED["seed"]), str(reps)], capture_output=True, text=True, check=True)
+    return json.loads(out.stdout)
+
+
+def planted_checks():
+    from oracle import port  # the count of items is a property of the workload
+    return port.planted(PLANTED["atoms"], PLANTED["nogoods"], PLANTED["pct"], PLANTED["seed"])
+
+
+def reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    reps = args.warmup + args.steps
+    if os.path.exists(REF_BIN):
+        ref = run_reference_planted(reps)
+        times = ref["prop_ms"][args.warmup:]
+        kind = "reference"
+    else:  # restatement of the reference algorithm (oracle port), timed in-process
+        from oracle import port
+        times = []
+        for i in range(reps):
+            t = time.perf_counter()
+            port.planted(PLANTED["atoms"], PLANTED["nogoods"], PLANTED["pct"], PLANTED["seed"])
+            if i >= args.warmup:
+                times.append((time.perf_counter() - t) * 1e3)
+        kind = "port"
+    checks = planted_checks()["checks"]
+    ms = statistics.mean(times)
+    value = checks / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": "nogood checks/sec", "value": value, "unit": "checks/s", "n_gpus": 0,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "solver": "aspine Propagator workers=1"},
+        "cpu_baseline": {"value": value, "unit": "checks/s", "cores": 1, "kind": kind,
+                         "sample": f"{args.steps} full propagate_and_check calls ({checks} checks each)"},
+        "e2e": {"value": value, "unit": "checks/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="yasmin", choices=["yasmin", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="skip enumeration / first-model sections")
+    args = ap.parse_args()
+    rank, world, local = dist_setup(args.gpus)
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+
+    import torch
+    import paper_1909_01786_b200 as Y
+    from paper_1909_01786_b200 import instances as I
+
+    torch.cuda.set_device(local)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+
+    store, seeded, dec = Y.NogoodStore.planted(**PLANTED)
+    prop = Y.Propagator(store, 16, engine="grid", device=local)
+
+    def prepare():
+        prop.reset()
+        prop.push_decision(dec)
+        prop.assign_propagated(seeded, 2)
+        prop.seed([dec] + seeded)
+
+    for _ in range(args.warmup):
+        prepare()
+        flush.zero_()
+        torch.cuda.synchronize()
+        o = prop.propagate_and_check(2)
+    barrier(world)
+    torch.cuda.synchronize()
+    dev_ms, checks, lits, launches = [], 0, 0, 0
+    t0 = time.perf_counter()
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            prepare()
+            flush.zero_()  # L2 flushed between timed iterations
+            torch.cuda.synchronize()
+            o = prop.propagate_and_check(2)  # one kernel launch: all passes to fixpoint
+            launches += 1
+            dev_ms.append(o.device_ms)
+            checks += o.checks
+            lits += o.checked_lits
+            assert not o.violated
+    torch.cuda.synchronize()
+    barrier(world)
+    wall = time.perf_counter() - t0
+    total_ms = allreduce([sum(dev_ms)], "max", world)[0]
+    all_checks = allreduce([float(checks)], "sum", world)[0]
+    value = all_checks / (total_ms / 1e3)
+    avg_ms = statistics.mean(dev_ms)
+    algo_bytes = (12 * checks + 4 * lits) / args.steps  # per launch, SURVEY.md §8(d)
+    peak, peak_kind = peaks()
+    achieved = algo_bytes / (avg_ms / 1e3) / 1e9
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "planted_grid_dram.json")
+    if os.path.exists(prof_json):
+        with open(prof_json) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # ---- e2e through the public API with host buffers ----------------------
+    e2e_ms = []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        prepare()  # H2D: decision + seeded assignment + frontier
+        o = prop.propagate_and_check(2)
+        tr = prop.trail()  # D2H: the fixpoint trail
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+    e2e_max = allreduce([statistics.mean(e2e_ms)], "max", world)[0]
+    h2d = 4 * (1 + len(seeded)) + 4 * (1 + len(seeded)) + 8 * 16
+    d2h = 4 * len(tr)
+
+    line = {
+        "metric": "nogood checks/sec", "value": value, "unit": "checks/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world} (propagation does not shard)",
+                   "engine": "grid (1 CTA/SM, cooperative)", "l2": "flushed between steps (512 MiB write)",
+                   "timed": "propagate_and_check kernel, CUDA events on its stream"},
+        "checks_per_step": checks / args.steps, "passes_per_step": o.passes,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": algo_bytes,
+                     "bytes_model": "12 B/check (occurrence + offset + guard) + 4 B/literal of checked nogoods"},
+        "e2e": {"value": (all_checks / args.steps) / (e2e_max / 1e3), "unit": "checks/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max},
+        "clocks": clk.summary(), "gpu_launches": launches, "bracket_wall_s": wall,
+    }
+
+    if rank == 0:
+        try:
+            if os.path.exists(REF_BIN):
+                ref = run_reference_planted(3)
+                cpu_ms = statistics.mean(ref["prop_ms"])
+                kind = "reference"
+            else:
+                from oracle import port
+                t = time.perf_counter()
+                port.planted(**PLANTED)
+                cpu_ms = (time.perf_counter() - t) * 1e3
+                kind = "port"
+            line["cpu_baseline"] = {"value": checks / args.steps / (cpu_ms / 1e3), "unit": "checks/s", "cores": 1,
+                                    "kind": kind, "sample": "3 full propagate_and_check calls on the same store "
+                                                            "(workers=1, the reference's fastest setting)",
+                                    "ms_per_call": cpu_ms}
+        except Exception as e:  # never let the baseline break the line
+            line["cpu_baseline"] = {"value": None, "unit": "checks/s", "cores": 1, "kind": "reference",
+                                    "sample": f"failed: {e}"}
+
+    if not args.no_extras:
+        line["enumeration"] = enumeration(Y, I, rank, world, local)
+        if rank == 0:
+            line["first_model"] = first_model(Y, I, local)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def enumeration(Y, I, rank, world, local):
+    """12-queens, all answer sets: ladder cubes over the choice atoms, partitioned
+    over the ranks; model count all-reduced (SUM), time max over ranks."""
+    text = I.queens(12)
+    cfg = Y.SolverConfig(max_models=0, cube_atoms=12, rank=rank, world=world, device=local)
+    Y.solve(Y.parse_program(text), cfg)  # warm-up (module load, allocations)
+    barrier(world)
+    t = time.perf_counter()
+    prog = Y.parse_program(text)
+    r = Y.solve(prog, cfg)
+    wall = (time.perf_counter() - t) * 1e3
+    n_models, cubes = allreduce([float(len(r.models)), float(r.stats.cubes)], "sum", world)
+    wall_max, dev_max = allreduce([wall, r.stats.device_ms], "max", world)
+    out = {"instance": "queens12 (all answer sets)", "models": int(n_models), "expected_models": 14200,
+           "wall_ms": wall_max, "device_ms": dev_max, "cubes": int(cubes), "n_gpus": world,
+           "passes_rank0": r.stats.passes}
+    if rank == 0 and os.path.exists(REF_BIN):
+        # bounded CPU sample: the reference's first 1000 models of the same enumeration
+        p = subprocess.run([REF_BIN, "solve", "-", "-n", "1000", "--no-models"], input=text, capture_output=True,
+                           text=True, check=True)
+        ref = json.loads(p.stdout)
+        rate = ref["stats"]["models"] / (ref["run_ms"][0] / 1e3)
+        out["cpu_reference"] = {"sample": "queens12, first 1000 models, workers=1", "models_per_s": rate,
+                                "extrapolated_all_models_s": 14200 / rate}
+        out["models_per_s"] = n_models / (wall_max / 1e3)
+    return out
+
+
+def first_model(Y, I, local):
+    out = {}
+    for name, text in (("colour2000", I.colouring(2000, 4.0, 3, 1)), ("ham200", I.hamiltonian(200, 1.0, 1))):
+        prog = Y.parse_program(text)
+        Y.solve(prog, Y.SolverConfig(device=local))
+        t = time.perf_counter()
+        r = Y.solve(prog, Y.SolverConfig(device=local))
+        entry = {"status": r.status.name, "wall_ms": (time.perf_counter() - t) * 1e3, "device_ms": r.stats.device_ms,
+                 "decisions": r.stats.decisions, "passes": r.stats.passes}
+        if os.path.exists(REF_BIN):
+            p = subprocess.run([REF_BIN, "solve", "-", "-n", "1", "--no-models", "--reps", "3"], input=text,
+                               capture_output=True, text=True, check=True)
+            ref = json.loads(p.stdout)
+            entry["cpu_reference_run_ms"] = statistics.mean(ref["run_ms"])
+            entry["same_trajectory"] = all(getattr(r.stats, k) == ref["stats"][k]
+                                           for k in ("decisions", "propagations", "conflicts", "passes"))
+        out[name] = entry
+    return out
+
+
+if __name__ == "__main__":
+    main()

@@ -136,6 +136,7 @@ typedef struct yas_stats {
     uint64_t launches; /* kernel launches */
     double device_ms;  /* kernel time, CUDA events */
     uint64_t cubes;    /* cubes assigned to this rank */
+    uint64_t checked_lits; /* literals of the checked nogoods (algorithmic traffic) */
 } yas_stats;
 
 int yas_solve(const yas_program* p, const yas_config* cfg, yas_result** out, char* err, size_t err_cap);
@@ -176,7 +177,7 @@ void yas_free_ints(int32_t* p);
 /* ---- low level: Propagator (propagate.hpp:54-97) over one device search -- */
 typedef struct yas_outcome {
     int violated;
-    uint64_t propagations, passes, checks;
+    uint64_t propagations, passes, checks, checked_lits;
     uint32_t n_conflicts;
     float device_ms;
 } yas_outcome; /* PropagationOutcome (+ device extras) */

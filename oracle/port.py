@@ -26,6 +26,8 @@ def lib():
                                 C.c_uint64, C.c_double, C.c_uint32, C.c_uint64, C.c_double]
         L.ora_propstore.restype = C.c_void_p
         L.ora_propstore.argtypes = [C.POINTER(C.c_int32), C.POINTER(C.c_uint32), C.c_size_t, C.c_uint32, C.c_uint32]
+        L.ora_planted.restype = C.c_void_p
+        L.ora_planted.argtypes = [C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint64]
         L.ora_free.argtypes = [C.c_void_p]
         _lib = L
     return _lib
@@ -54,3 +56,8 @@ def propstore(nogoods, atoms: int, deps_words: int = 1) -> dict:
     L = (C.c_int32 * max(1, len(lits)))(*lits)
     O = (C.c_uint32 * len(offs))(*offs)
     return _take(lib().ora_propstore(L, O, len(nogoods), atoms, deps_words))
+
+
+def planted(atoms: int, nogoods: int, pct: int, seed: int = 0x1B00B5) -> dict:
+    """Planted-store propagation (config 4b): checks/passes/propagations + trail digest."""
+    return _take(lib().ora_planted(atoms, nogoods, pct, seed))

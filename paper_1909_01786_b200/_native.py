@@ -60,12 +60,13 @@ class yas_stats(C.Structure):
         ("wall_ms", C.c_double)] + [(n, C.c_uint64) for n in (
         "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods", "res_learned", "fwd_learned",
         "fwd_fallbacks", "uip_check_failures", "fwd_decision_only_failures", "asserting_failures", "checks",
-        "searches", "launches")] + [("device_ms", C.c_double), ("cubes", C.c_uint64)]
+        "searches", "launches")] + [("device_ms", C.c_double), ("cubes", C.c_uint64), ("checked_lits", C.c_uint64)]
 
 
 class yas_outcome(C.Structure):
     _fields_ = [("violated", C.c_int), ("propagations", C.c_uint64), ("passes", C.c_uint64),
-                ("checks", C.c_uint64), ("n_conflicts", C.c_uint32), ("device_ms", C.c_float)]
+                ("checks", C.c_uint64), ("checked_lits", C.c_uint64), ("n_conflicts", C.c_uint32),
+                ("device_ms", C.c_float)]
 
 
 _lib = None

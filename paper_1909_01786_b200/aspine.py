@@ -138,7 +138,7 @@ _STAT_FIELDS = ["decisions", "propagations", "conflicts", "learned_count", "lear
                 "models", "wall_ms", "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods",
                 "res_learned", "fwd_learned", "fwd_fallbacks", "uip_check_failures",
                 "fwd_decision_only_failures", "asserting_failures", "checks", "searches", "launches",
-                "device_ms", "cubes"]
+                "device_ms", "cubes", "checked_lits"]
 
 
 @dataclass
@@ -166,6 +166,7 @@ class SolveStats:
     launches: int = 0
     device_ms: float = 0.0
     cubes: int = 0
+    checked_lits: int = 0
 
     def avg_learned_len(self) -> float:
         return 0.0 if self.learned_count == 0 else self.learned_length_sum / self.learned_count
@@ -517,6 +518,7 @@ class PropagationOutcome:
     passes: int
     checks: int
     device_ms: float
+    checked_lits: int = 0
 
 
 REASON_NONE, REASON_DECISION, REASON_UNIT, REASON_COMPLETION = -1, -2, -3, -4
@@ -544,7 +546,8 @@ class Propagator:
             self._h = C.c_void_p(0)
 
     def _outcome(self, o: N.yas_outcome) -> PropagationOutcome:
-        return PropagationOutcome(bool(o.violated), self.conflicts(), o.propagations, o.passes, o.checks, o.device_ms)
+        return PropagationOutcome(bool(o.violated), self.conflicts(), o.propagations, o.passes, o.checks, o.device_ms,
+                                  o.checked_lits)
 
     def reset(self):
         N.lib().yas_propagator_reset(self._h)

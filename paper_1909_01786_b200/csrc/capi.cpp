@@ -212,6 +212,7 @@ void fill_stats(yas_stats& o, const dev::Stats& s) {
     o.asserting_failures = s.asserting_failures;
     o.checks = s.checks;
     o.searches = s.searches;
+    o.checked_lits = s.checked_lits;
 }
 
 }  // namespace
@@ -654,6 +655,7 @@ static void outcome_from(yas_propagator* p, bool violated, const dev::Ctl& befor
     o->propagations = c.st.propagations - before.st.propagations;
     o->passes = c.st.passes - before.st.passes;
     o->checks = c.st.checks - before.st.checks;
+    o->checked_lits = c.st.checked_lits - before.st.checked_lits;
     o->n_conflicts = c.n_confl;
     o->device_ms = p->s->last_ms();
 }

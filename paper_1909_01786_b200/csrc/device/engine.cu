@@ -75,6 +75,11 @@ __device__ __forceinline__ void warp_count(unsigned long long* ctr, bool pred) {
     if (b && lane_id() == static_cast<std::uint32_t>(__ffs(b) - 1)) atomicAdd(ctr, static_cast<unsigned long long>(__popc(b)));
 }
 
+__device__ __forceinline__ void warp_sum(unsigned long long* ctr, std::uint32_t v) {
+    const std::uint32_t t = __reduce_add_sync(0xffffffffu, v);
+    if (lane_id() == 0 && t) atomicAdd(ctr, static_cast<unsigned long long>(t));
+}
+
 __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -654,9 +659,8 @@ struct Search {
 
     // Evaluate nogood `id` against the pass-start assignment
     // (propagate.cpp:86-168 without the watch shortcuts).
-    __device__ void evaluate(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit,
+    __device__ void evaluate(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
                              unsigned long long* d0 = nullptr, std::uint32_t* meta = nullptr) const {
-        std::uint32_t len;
         const std::uint32_t guard = guard_of(static_cast<std::uint32_t>(id));
         const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
         if (len == 1) {
@@ -698,7 +702,7 @@ struct Search {
             const std::uint32_t e = base + lane_id();
             bool first = false, conflict = false, prop = false;
             std::int32_t id = -1, plit = 0;
-            std::uint32_t slot = 0, meta = 0;
+            std::uint32_t slot = 0, meta = 0, clen = 0;
             unsigned long long d0 = 0;
             if (e < T) {
                 std::uint32_t lo = 0, hi = F;
@@ -719,10 +723,11 @@ struct Search {
                         break;
                     }
                 }
-                if (first) evaluate(id, conflict, prop, plit, &d0, &meta);
+                if (first) evaluate(id, conflict, prop, plit, clen, &d0, &meta);
             }
             __syncwarp();
             warp_count(&c->st.checks, first);
+            warp_sum(&c->st.checked_lits, clen);
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
             if (conflict) sl.confl[cs] = id;
             const std::uint32_t ps = warp_append(&c->n_props, prop);
@@ -773,6 +778,7 @@ struct Search {
             const std::uint32_t e = base + lane_id();
             bool first = false, conflict = false, prop = false;
             std::int32_t id = -1, plit = 0;
+            std::uint32_t clen = 0;
             if (e < T) {
                 std::uint32_t lo = 0, hi = F;  // largest p with froff[p] <= e
                 while (hi - lo > 1) {
@@ -782,10 +788,11 @@ struct Search {
                 id = occ_entry(lidx(fr[lo]), e - sl.froff[lo], learned);
                 const unsigned long long old = atomicMin(sl.claim + id, ckey(gen, e));
                 first = static_cast<std::uint32_t>(old >> 32) != ~gen;
-                if (first) evaluate(id, conflict, prop, plit);
+                if (first) evaluate(id, conflict, prop, plit, clen);
             }
             __syncwarp();
             warp_count(&c->st.checks, first);
+            warp_sum(&c->st.checked_lits, clen);
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
             if (conflict) sl.confl[cs] = id;
             const std::uint32_t ps = warp_append(&c->n_props, prop);
@@ -1690,22 +1697,32 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
             }
             g.sync();
             break;
-        case kOpAssign:  // assign_propagated for a bulk of literals (assignment.cpp:135-144)
-            if (g.leader()) {
-                for (std::uint32_t k = 0; k < op.n; ++k) {
-                    const std::int32_t lit = op.lits[k];
-                    const std::uint32_t a = atom_of(lit);
-                    if (s.val(a) != 0) continue;
+        case kOpAssign: {  // assign_propagated for a bulk of distinct atoms (assignment.cpp:135-144);
+                           // already assigned atoms are left alone (agreed / conflict)
+            const std::uint32_t ts0 = c->ts;
+            unsigned long long carry = 0;
+            for (std::uint32_t base = 0; base < op.n; base += g.size()) {
+                const std::uint32_t k = base + g.tid();
+                const std::int32_t lit = k < op.n ? op.lits[k] : 0;
+                const std::uint32_t a = atom_of(lit);
+                const bool fresh = k < op.n && s.val(a) == 0;
+                unsigned long long tot;
+                const std::uint32_t r = static_cast<std::uint32_t>(g.scan(fresh ? 1ull : 0ull, tot) + carry);
+                if (fresh) {
                     s.set_cell(a, lit > 0 ? static_cast<std::int32_t>(op.level) : -static_cast<std::int32_t>(op.level));
-                    sl.tpos[a] = c->ts;
-                    sl.trail[c->ts++] = lit;
+                    sl.tpos[a] = ts0 + r;
+                    sl.trail[ts0 + r] = lit;
                     sl.reason[a] = op.antecedent;
                     for (std::uint32_t w = 0; w < C.W; ++w) s.dep(w, a) = op.deps ? op.deps[w] : 0ull;
                     sl.dovf[a] = static_cast<std::uint8_t>(op.ovf);
                 }
+                carry += tot;
             }
             g.sync();
+            if (g.leader()) c->ts = ts0 + static_cast<std::uint32_t>(carry);
+            g.sync();
             break;
+        }
         case kOpSeed:  // frontier.last.push_back for a bulk of literals
             for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr[c->cur][c->F + k] = op.lits[k];
             g.sync();

@@ -72,7 +72,7 @@ struct Stats {
     unsigned long long decisions, propagations, conflicts, learned_count, learned_length_sum,
         restarts, models, passes, duplicate_learned, blocking_nogoods, res_learned, fwd_learned,
         fwd_fallbacks, uip_check_failures, fwd_decision_only_failures, asserting_failures,
-        checks, searches;
+        checks, searches, checked_lits;
 };
 
 // Per-slot control block. Mirrored into shared memory by single-CTA searches.

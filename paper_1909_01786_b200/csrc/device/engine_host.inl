@@ -437,8 +437,19 @@ void Session::push_decision(std::int32_t lit) {
     run_op(*impl_, op, nullptr);
 }
 
-void Session::assign(const std::vector<std::int32_t>& lits, std::uint32_t level, std::int32_t antecedent,
+void Session::assign(const std::vector<std::int32_t>& lits_in, std::uint32_t level, std::int32_t antecedent,
                      const std::vector<unsigned long long>& deps, bool ovf) {
+    // the device op takes distinct atoms (a repeated atom would be agreed or a
+    // conflict in try_set, i.e. no change): keep the first occurrence only
+    std::vector<std::int32_t> lits;
+    lits.reserve(lits_in.size());
+    std::vector<char> seen(impl_->ar.A + 1, 0);
+    for (std::int32_t l : lits_in) {
+        const std::uint32_t a = static_cast<std::uint32_t>(l < 0 ? -l : l);
+        if (a > impl_->ar.A || seen[a]) continue;
+        seen[a] = 1;
+        lits.push_back(l);
+    }
     std::vector<void*> tmp;
     dev::OpArgs op{};
     op.op = dev::kOpAssign;

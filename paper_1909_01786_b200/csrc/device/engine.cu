@@ -272,73 +272,76 @@ struct GridG {
 // ---------------------------------------------------------------------------
 // The search (one instance per group)
 // ---------------------------------------------------------------------------
-// Shared-memory working set of a single-CTA search (all null for GridG).
-struct Sm {
-    unsigned long long* htab;  // claim hash: (id+1) << 32 | min e
-    unsigned long long* wtab;  // win hash:   (atom+1) << 32 | (e << 1 | neg)
-    std::int32_t* pid;
-    std::int32_t* plit;
-    std::uint32_t* pslot;      // claim slot | win slot << 16
-    unsigned long long* pdep;  // Deps word 0 of the proposal (computed at evaluation)
-    std::uint32_t* pmeta;      // overflow << 31 | occurrence total of the proposed literal
-    std::int32_t* litat;
-    std::uint32_t* otat;
-    std::uint32_t* bits;
-    std::int32_t* fr;          // mirror of the current frontier
-    std::uint32_t* froff;      // and of its occurrence offsets
-    std::uint32_t* vasg;       // 2-bit assignment mirror: assigned / true
-    std::uint32_t* vtru;
-    std::uint32_t tcap, hmask, fcap, vwords;
-};
-
+// Shared-memory working set of a single-CTA search. Offsets are computed on
+// the host (plan_smem) and passed as a __grid_constant__ kernel parameter, so
+// every array address is "dynamic-smem base + constant".
 struct SmemCfg {
     std::uint32_t tcap, hcap, fcap, vwords;
+    std::uint32_t o_htab, o_wtab, o_pid, o_plit, o_pslot, o_pdep, o_pmeta, o_litat, o_otat, o_bits, o_fr, o_froff,
+        o_vasg, o_vtru, bytes;
+};
+
+extern __shared__ __align__(16) unsigned char yas_dsm[];
+
+struct Sm {
+    const SmemCfg* cfg;
+    template <class T>
+    __device__ __forceinline__ T* at(std::uint32_t off) const { return reinterpret_cast<T*>(yas_dsm + off); }
+    __device__ __forceinline__ unsigned long long* htab() const { return at<unsigned long long>(cfg->o_htab); }  // (id+1)<<32 | min e
+    __device__ __forceinline__ unsigned long long* wtab() const { return at<unsigned long long>(cfg->o_wtab); }  // (atom+1)<<32 | e<<1|neg
+    __device__ __forceinline__ std::int32_t* pid() const { return at<std::int32_t>(cfg->o_pid); }
+    __device__ __forceinline__ std::int32_t* plit() const { return at<std::int32_t>(cfg->o_plit); }
+    __device__ __forceinline__ std::uint32_t* pslot() const { return at<std::uint32_t>(cfg->o_pslot); }  // claim | win << 16
+    __device__ __forceinline__ unsigned long long* pdep() const { return at<unsigned long long>(cfg->o_pdep); }  // Deps word 0
+    __device__ __forceinline__ std::uint32_t* pmeta() const { return at<std::uint32_t>(cfg->o_pmeta); }  // ovf<<31 | occ total
+    __device__ __forceinline__ std::int32_t* litat() const { return at<std::int32_t>(cfg->o_litat); }
+    __device__ __forceinline__ std::uint32_t* otat() const { return at<std::uint32_t>(cfg->o_otat); }
+    __device__ __forceinline__ std::uint32_t* bits() const { return at<std::uint32_t>(cfg->o_bits); }
+    __device__ __forceinline__ std::int32_t* fr() const { return at<std::int32_t>(cfg->o_fr); }  // frontier mirror
+    __device__ __forceinline__ std::uint32_t* froff() const { return at<std::uint32_t>(cfg->o_froff); }
+    __device__ __forceinline__ std::uint32_t* vasg() const { return at<std::uint32_t>(cfg->o_vasg); }  // assigned bits
+    __device__ __forceinline__ std::uint32_t* vtru() const { return at<std::uint32_t>(cfg->o_vtru); }  // true bits
+    __device__ __forceinline__ std::uint32_t tcap() const { return cfg->tcap; }
+    __device__ __forceinline__ std::uint32_t hmask() const { return cfg->hcap ? cfg->hcap - 1 : 0; }
+    __device__ __forceinline__ std::uint32_t fcap() const { return cfg->fcap; }
+    __device__ __forceinline__ std::uint32_t vwords() const { return cfg->vwords; }
 };
 
 __device__ __forceinline__ std::uint32_t hslot(std::uint32_t key, std::uint32_t mask) { return (key * 2654435761u) & mask; }
 
-__device__ Sm carve_smem(unsigned char* base, const SmemCfg& cfg) {
-    Sm m{};
-    m.tcap = cfg.tcap;
-    m.hmask = cfg.hcap ? cfg.hcap - 1 : 0;
-    m.fcap = cfg.fcap;
-    m.vwords = cfg.vwords;
-    std::size_t o = 0;
-    auto take = [&](std::size_t bytes) {
-        unsigned char* p = base + o;
-        o += (bytes + 15) & ~static_cast<std::size_t>(15);
-        return p;
+// Host: lay out the shared-memory arrays for a given capacity.
+SmemCfg smem_layout(std::uint32_t tcap, std::uint32_t vwords) {
+    SmemCfg c{};
+    c.tcap = tcap;
+    c.hcap = tcap ? 2 * tcap : 0;
+    c.fcap = tcap ? tcap + 1 : 0;
+    c.vwords = vwords;
+    std::uint32_t o = 0;
+    auto take = [&](std::uint32_t bytes) {
+        const std::uint32_t at = o;
+        o += (bytes + 15u) & ~15u;
+        return at;
     };
-    if (cfg.tcap) {
-        m.htab = reinterpret_cast<unsigned long long*>(take(8ull * cfg.hcap));
-        m.wtab = reinterpret_cast<unsigned long long*>(take(8ull * cfg.hcap));
-        m.pid = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
-        m.plit = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
-        m.pslot = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
-        m.pdep = reinterpret_cast<unsigned long long*>(take(8ull * cfg.tcap));
-        m.pmeta = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
-        m.litat = reinterpret_cast<std::int32_t*>(take(4ull * cfg.tcap));
-        m.otat = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.tcap));
-        m.bits = reinterpret_cast<std::uint32_t*>(take(4ull * ((cfg.tcap + 31) / 32)));
-        m.fr = reinterpret_cast<std::int32_t*>(take(4ull * cfg.fcap));
-        m.froff = reinterpret_cast<std::uint32_t*>(take(4ull * (cfg.fcap + 1)));
+    if (tcap) {
+        c.o_htab = take(8u * c.hcap);
+        c.o_wtab = take(8u * c.hcap);
+        c.o_pdep = take(8u * tcap);
+        c.o_pid = take(4u * tcap);
+        c.o_plit = take(4u * tcap);
+        c.o_pslot = take(4u * tcap);
+        c.o_pmeta = take(4u * tcap);
+        c.o_litat = take(4u * tcap);
+        c.o_otat = take(4u * tcap);
+        c.o_bits = take(4u * ((tcap + 31) / 32));
+        c.o_fr = take(4u * c.fcap);
+        c.o_froff = take(4u * (c.fcap + 1));
     }
-    if (cfg.vwords) {
-        m.vasg = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.vwords));
-        m.vtru = reinterpret_cast<std::uint32_t*>(take(4ull * cfg.vwords));
+    if (vwords) {
+        c.o_vasg = take(4u * vwords);
+        c.o_vtru = take(4u * vwords);
     }
-    return m;
-}
-
-std::size_t smem_bytes(const SmemCfg& cfg) {
-    auto r = [](std::size_t b) { return (b + 15) & ~static_cast<std::size_t>(15); };
-    std::size_t o = 0;
-    if (cfg.tcap)
-        o += 2 * r(8ull * cfg.hcap) + 6 * r(4ull * cfg.tcap) + r(8ull * cfg.tcap) + r(4ull * ((cfg.tcap + 31) / 32)) +
-             r(4ull * cfg.fcap) +
-             r(4ull * (cfg.fcap + 1));
-    if (cfg.vwords) o += 2 * r(4ull * cfg.vwords);
-    return o;
+    c.bytes = o;
+    return c;
 }
 
 template <class G>
@@ -346,55 +349,55 @@ struct Search {
     G& g;
     const Static& S;
     const Config& C;
-    const Slot& sl;
+    Slot sl;
     const Caps& K;
     Shared* sh;
     Ctl* c;
     unsigned long long t0;
     Sm sm;
 
-    __device__ Search(G& g_, const Static& s, const Config& cf, const Slot& slot, const Caps& k, Shared* shared,
+    __device__ Search(G& g_, const Static& s, const Config& cf, Slot slot, const Caps& k, Shared* shared,
                       unsigned long long start, const Sm& smem)
         : g(g_), S(s), C(cf), sl(slot), K(k), sh(shared), c(g_.c), t0(start), sm(smem) {}
 
     // ---- assignment access: 2-bit shared mirror when present --------------
     // sign of the atom's value: 0 unassigned, 1 true, -1 false
     __device__ int val(std::uint32_t a) const {
-        if (sm.vwords) {
+        if (sm.vwords()) {
             const std::uint32_t b = 1u << (a & 31);
-            if (!(sm.vasg[a >> 5] & b)) return 0;
-            return (sm.vtru[a >> 5] & b) ? 1 : -1;
+            if (!(sm.vasg()[a >> 5] & b)) return 0;
+            return (sm.vtru()[a >> 5] & b) ? 1 : -1;
         }
-        const std::int32_t cv = sl.cells[a];
+        const std::int32_t cv = sl.cells()[a];
         return (cv > 0) - (cv < 0);
     }
     __device__ void set_cell(std::uint32_t a, std::int32_t cv) const {
-        sl.cells[a] = cv;
-        if (sm.vwords) {
+        sl.cells()[a] = cv;
+        if (sm.vwords()) {
             const std::uint32_t b = 1u << (a & 31);
             if (cv == 0) {
-                atomicAnd(sm.vasg + (a >> 5), ~b);
-                atomicAnd(sm.vtru + (a >> 5), ~b);
+                atomicAnd(sm.vasg() + (a >> 5), ~b);
+                atomicAnd(sm.vtru() + (a >> 5), ~b);
             } else {
-                if (cv > 0) atomicOr(sm.vtru + (a >> 5), b);
-                else atomicAnd(sm.vtru + (a >> 5), ~b);
-                atomicOr(sm.vasg + (a >> 5), b);
+                if (cv > 0) atomicOr(sm.vtru() + (a >> 5), b);
+                else atomicAnd(sm.vtru() + (a >> 5), ~b);
+                atomicOr(sm.vasg() + (a >> 5), b);
             }
         }
     }
     __device__ void rebuild_mirror() const {
-        if (!sm.vwords) return;
-        for (std::uint32_t w = g.tid(); w < sm.vwords; w += g.size()) {
+        if (!sm.vwords()) return;
+        for (std::uint32_t w = g.tid(); w < sm.vwords(); w += g.size()) {
             std::uint32_t as = 0, tr = 0;
             for (std::uint32_t b = 0; b < 32; ++b) {
                 const std::uint32_t a = 32 * w + b;
                 if (a > S.A) break;
-                const std::int32_t cv = sl.cells[a];
+                const std::int32_t cv = sl.cells()[a];
                 if (cv != 0) as |= 1u << b;
                 if (cv > 0) tr |= 1u << b;
             }
-            sm.vasg[w] = as;
-            sm.vtru[w] = tr;
+            sm.vasg()[w] = as;
+            sm.vtru()[w] = tr;
         }
     }
 
@@ -406,20 +409,20 @@ struct Search {
             return S.pool + lo;
         }
         const std::uint32_t k = id - S.N;
-        const std::uint32_t lo = sl.loff[k];
-        len = sl.loff[k + 1] - lo;
-        return sl.lpool + lo;
+        const std::uint32_t lo = sl.loff()[k];
+        len = sl.loff()[k + 1] - lo;
+        return sl.lpool() + lo;
     }
     __device__ std::int32_t lit_at(const std::int32_t* p, std::uint32_t k, std::uint32_t id) const {
         return id < S.N ? __ldg(p + k) : p[k];
     }
     __device__ std::uint32_t length_of(std::uint32_t id) const {
         if (id < S.N) return __ldg(S.off + id + 1) - __ldg(S.off + id);
-        return sl.loff[id - S.N + 1] - sl.loff[id - S.N];
+        return sl.loff()[id - S.N + 1] - sl.loff()[id - S.N];
     }
     __device__ std::uint32_t guard_of(std::uint32_t id) const { return id < S.N ? __ldg(S.guard + id) : kNone; }
     __device__ std::uint32_t occ_total(std::uint32_t li) const {
-        return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot[li];
+        return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot()[li];
     }
     // j-th entry of the literal's occurrence list [static c0, learned c0, ..., static c3, learned c3]
     // All segment bounds are loaded at once (one memory round trip), then one
@@ -430,7 +433,7 @@ struct Search {
 #pragma unroll
         for (int k = 0; k < 5; ++k) b[k] = __ldg(oo + k);
         if (!learned) return __ldg(S.occ_ids + b[0] + j);  // classes are contiguous
-        const std::uint32_t* h = sl.lhdr + 12 * li;
+        const std::uint32_t* h = sl.lhdr() + 12 * li;
         std::uint32_t hp[4], hn[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -442,7 +445,7 @@ struct Search {
             const std::uint32_t ns = b[cl + 1] - b[cl];
             if (j < ns) return __ldg(S.occ_ids + b[cl] + j);
             j -= ns;
-            if (j < hn[cl]) return sl.larena[hp[cl] + j];
+            if (j < hn[cl]) return sl.larena()[hp[cl] + j];
             j -= hn[cl];
         }
         return -1;
@@ -452,7 +455,7 @@ struct Search {
         return nw < C.W ? nw : C.W;
     }
     __device__ unsigned long long& dep(std::uint32_t w, std::uint32_t a) const {
-        return sl.deps[static_cast<std::size_t>(w) * (S.A + 1) + a];
+        return sl.deps()[static_cast<std::size_t>(w) * (S.A + 1) + a];
     }
     __device__ bool holds(std::int32_t l) const {
         const int v = val(atom_of(l));
@@ -479,16 +482,16 @@ struct Search {
         const std::uint32_t nw = nwords(level);
         std::uint8_t ovf = 0;
         for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = deps_word(L, len, id, a, w, ovf);
-        sl.dovf[a] = ovf;
+        sl.dovf()[a] = ovf;
     }
     __device__ unsigned long long deps_word(const std::int32_t* L, std::uint32_t len, std::uint32_t id,
                                             std::uint32_t a, std::uint32_t w, std::uint8_t& ovf) const {
         unsigned long long acc = 0;
         for (std::uint32_t k = 0; k < len; ++k) {
             const std::uint32_t x = atom_of(lit_at(L, k, id));
-            const std::int32_t cv = sl.cells[x];
+            const std::int32_t cv = sl.cells()[x];
             const unsigned long long d = dep(w, x);
-            const std::uint8_t o = w == 0 ? sl.dovf[x] : 0;
+            const std::uint8_t o = w == 0 ? sl.dovf()[x] : 0;
             if (x != a && lvl_of(cv) > 1) {
                 acc |= d;
                 ovf |= o;
@@ -502,8 +505,8 @@ struct Search {
     // frontier and its offsets are mirrored into shared memory when they fit.
     __device__ void frontier_offsets() {
         const std::uint32_t F = c->F;
-        const std::int32_t* fr = sl.fr[c->cur];
-        const bool mirror = sm.tcap && F + 1 <= sm.fcap;
+        const std::int32_t* fr = sl.fr(c->cur);
+        const bool mirror = sm.tcap() && F + 1 <= sm.fcap();
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < F; base += g.size()) {
             const std::uint32_t p = base + g.tid();
@@ -512,18 +515,18 @@ struct Search {
             unsigned long long tot;
             const unsigned long long pre = g.scan(v, tot) + carry;
             if (p < F) {
-                sl.froff[p] = static_cast<std::uint32_t>(pre);
+                sl.froff()[p] = static_cast<std::uint32_t>(pre);
                 if (mirror) {
-                    sm.froff[p] = static_cast<std::uint32_t>(pre);
-                    sm.fr[p] = lit;
+                    sm.froff()[p] = static_cast<std::uint32_t>(pre);
+                    sm.fr()[p] = lit;
                 }
             }
             carry += tot;
         }
         g.sync();
         if (g.leader()) {
-            sl.froff[F] = static_cast<std::uint32_t>(carry);
-            if (mirror) sm.froff[F] = static_cast<std::uint32_t>(carry);
+            sl.froff()[F] = static_cast<std::uint32_t>(carry);
+            if (mirror) sm.froff()[F] = static_cast<std::uint32_t>(carry);
             c->T = static_cast<std::uint32_t>(carry);
             c->b[11] = 0;
         }
@@ -538,17 +541,17 @@ struct Search {
     __device__ void compact(std::uint32_t T, std::uint32_t dst, bool pass, std::uint32_t hsize) {
         const std::uint32_t nw = (T + 31) / 32;
         const std::uint32_t ts0 = c->ts;
-        std::int32_t* out = sl.fr[dst];
-        std::uint32_t* bsrc = SMEM ? sm.bits : sl.bitmap;
-        const std::int32_t* lat = SMEM ? sm.litat : sl.litat;
-        const std::uint32_t fcap = sm.tcap ? sm.fcap : 0;
+        std::int32_t* out = sl.fr(dst);
+        std::uint32_t* bsrc = SMEM ? sm.bits() : sl.bitmap();
+        const std::int32_t* lat = SMEM ? sm.litat() : sl.litat();
+        const std::uint32_t fcap = sm.tcap() ? sm.fcap() : 0;
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < nw; base += g.size()) {
             const std::uint32_t wi = base + g.tid();
             const std::uint32_t bits = wi < nw ? bsrc[wi] : 0u;
             unsigned long long occ = 0;
             for (std::uint32_t b = bits; b; b &= b - 1)
-                occ += SMEM ? sm.otat[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lat[wi * 32 + __ffs(b) - 1]));
+                occ += SMEM ? sm.otat()[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lat[wi * 32 + __ffs(b) - 1]));
             const unsigned long long v = (static_cast<unsigned long long>(__popc(bits)) << 32) | occ;
             unsigned long long tot;
             const unsigned long long pre = g.scan(v, tot) + carry;
@@ -557,14 +560,14 @@ struct Search {
             for (std::uint32_t b = bits; b; b &= b - 1) {
                 const std::int32_t lit = lat[wi * 32 + __ffs(b) - 1];
                 out[r] = lit;
-                sl.froff[r] = o;
+                sl.froff()[r] = o;
                 if (r < fcap) {
-                    sm.fr[r] = lit;
-                    sm.froff[r] = o;
+                    sm.fr()[r] = lit;
+                    sm.froff()[r] = o;
                 }
-                sl.trail[ts0 + r] = lit;
-                sl.tpos[atom_of(lit)] = ts0 + r;
-                o += SMEM ? sm.otat[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lit));
+                sl.trail()[ts0 + r] = lit;
+                sl.tpos()[atom_of(lit)] = ts0 + r;
+                o += SMEM ? sm.otat()[wi * 32 + __ffs(b) - 1] : occ_total(lidx(lit));
                 ++r;
             }
             if (bits) bsrc[wi] = 0u;
@@ -572,14 +575,14 @@ struct Search {
         }
         if (SMEM)
             for (std::uint32_t i = g.tid(); i < hsize; i += g.size()) {
-                sm.htab[i] = 0ull;
-                sm.wtab[i] = 0ull;
+                sm.htab()[i] = 0ull;
+                sm.wtab()[i] = 0ull;
             }
         g.sync();
         if (g.leader()) {
             const std::uint32_t cnt = static_cast<std::uint32_t>(carry >> 32);
-            sl.froff[cnt] = static_cast<std::uint32_t>(carry);
-            if (cnt + 1 <= fcap) sm.froff[cnt] = static_cast<std::uint32_t>(carry);
+            sl.froff()[cnt] = static_cast<std::uint32_t>(carry);
+            if (cnt + 1 <= fcap) sm.froff()[cnt] = static_cast<std::uint32_t>(carry);
             c->ts = ts0 + cnt;
             c->F = cnt;
             c->T = static_cast<std::uint32_t>(carry);
@@ -610,28 +613,28 @@ struct Search {
                 std::uint32_t e;
                 unsigned long long w;
                 if (SMEM) {
-                    id = sm.pid[i];
-                    lit = sm.plit[i];
-                    const std::uint32_t ps = sm.pslot[i];
-                    e = static_cast<std::uint32_t>(sm.htab[ps & 0xffffu]);
-                    w = sm.wtab[ps >> 16];
+                    id = sm.pid()[i];
+                    lit = sm.plit()[i];
+                    const std::uint32_t ps = sm.pslot()[i];
+                    e = static_cast<std::uint32_t>(sm.htab()[ps & 0xffffu]);
+                    w = sm.wtab()[ps >> 16];
                 } else {
-                    const int4 p = sl.props[i];
+                    const int4 p = sl.props()[i];
                     id = p.x;
                     lit = p.y;
                     e = static_cast<std::uint32_t>(p.z);
-                    w = sl.win[atom_of(lit)];
+                    w = sl.win()[atom_of(lit)];
                 }
                 const std::uint32_t a = atom_of(lit);
                 if ((static_cast<std::uint32_t>(w) >> 1) == e) {
                     set_cell(a, lit > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
                     if (unit) {
-                        sl.reason[a] = kReasonUnit;
+                        sl.reason()[a] = kReasonUnit;
                     } else {
-                        sl.reason[a] = id;
+                        sl.reason()[a] = id;
                         if (SMEM && nwords(dlev) == 1) {
-                            dep(0, a) = sm.pdep[i];
-                            sl.dovf[a] = static_cast<std::uint8_t>(sm.pmeta[i] >> 31);
+                            dep(0, a) = sm.pdep()[i];
+                            sl.dovf()[a] = static_cast<std::uint8_t>(sm.pmeta()[i] >> 31);
                         } else {
                             std::uint32_t len;
                             const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
@@ -639,12 +642,12 @@ struct Search {
                         }
                     }
                     if (SMEM) {
-                        atomicOr(sm.bits + (e >> 5), 1u << (e & 31));
-                        sm.litat[e] = lit;
-                        sm.otat[e] = sm.pmeta[i] & 0x7fffffffu;
+                        atomicOr(sm.bits() + (e >> 5), 1u << (e & 31));
+                        sm.litat()[e] = lit;
+                        sm.otat()[e] = sm.pmeta()[i] & 0x7fffffffu;
                     } else {
-                        atomicOr(sl.bitmap + (e >> 5), 1u << (e & 31));
-                        sl.litat[e] = lit;
+                        atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
+                        sl.litat()[e] = lit;
                     }
                 } else {
                     lose = (w & 1ull) != (lit < 0 ? 1ull : 0ull);
@@ -652,7 +655,7 @@ struct Search {
             }
             __syncwarp();
             const std::uint32_t slot = warp_append(&c->n_confl, lose);
-            if (lose) sl.confl[slot] = id;
+            if (lose) sl.confl()[slot] = id;
         }
         g.sync();
     }
@@ -696,7 +699,7 @@ struct Search {
         const bool learned = c->learned_n > 0;
         std::uint32_t hs = 64;
         while (hs < 2 * T) hs <<= 1;
-        if (hs > sm.hmask + 1) hs = sm.hmask + 1;
+        if (hs > sm.hmask() + 1) hs = sm.hmask() + 1;
         const std::uint32_t hm = hs - 1;
         for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
             const std::uint32_t e = base + lane_id();
@@ -708,18 +711,18 @@ struct Search {
                 std::uint32_t lo = 0, hi = F;
                 while (hi - lo > 1) {
                     const std::uint32_t mid = (lo + hi) >> 1;
-                    if (sm.froff[mid] <= e) lo = mid; else hi = mid;
+                    if (sm.froff()[mid] <= e) lo = mid; else hi = mid;
                 }
-                id = occ_entry(lidx(sm.fr[lo]), e - sm.froff[lo], learned);
+                id = occ_entry(lidx(sm.fr()[lo]), e - sm.froff()[lo], learned);
                 const unsigned long long key = (static_cast<unsigned long long>(id + 1) << 32) | e;
                 for (std::uint32_t h = hslot(static_cast<std::uint32_t>(id), hm);; h = (h + 1) & hm) {
-                    unsigned long long cur_k = sm.htab[h];
+                    unsigned long long cur_k = sm.htab()[h];
                     if (cur_k == 0ull) {
-                        cur_k = atomicCAS(sm.htab + h, 0ull, key);
+                        cur_k = atomicCAS(sm.htab() + h, 0ull, key);
                         if (cur_k == 0ull) { first = true; slot = h; break; }
                     }
                     if ((cur_k >> 32) == static_cast<unsigned long long>(id + 1)) {
-                        atomicMin(sm.htab + h, key);
+                        atomicMin(sm.htab() + h, key);
                         break;
                     }
                 }
@@ -729,34 +732,34 @@ struct Search {
             warp_count(&c->st.checks, first);
             warp_sum(&c->st.checked_lits, clen);
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-            if (conflict) sl.confl[cs] = id;
+            if (conflict) sl.confl()[cs] = id;
             const std::uint32_t ps = warp_append(&c->n_props, prop);
             if (prop) {
-                sm.pid[ps] = id;
-                sm.plit[ps] = plit;
-                sm.pslot[ps] = slot;
-                sm.pdep[ps] = d0;
-                sm.pmeta[ps] = meta;
+                sm.pid()[ps] = id;
+                sm.plit()[ps] = plit;
+                sm.pslot()[ps] = slot;
+                sm.pdep()[ps] = d0;
+                sm.pmeta()[ps] = meta;
             }
         }
         g.sync();
         mark(2);
         const std::uint32_t np = c->n_props;
         for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
-            const std::uint32_t e = static_cast<std::uint32_t>(sm.htab[sm.pslot[i]]);
-            const std::int32_t lit = sm.plit[i];
+            const std::uint32_t e = static_cast<std::uint32_t>(sm.htab()[sm.pslot()[i]]);
+            const std::int32_t lit = sm.plit()[i];
             const std::uint32_t a = atom_of(lit);
             const unsigned long long key =
                 (static_cast<unsigned long long>(a + 1) << 32) | (static_cast<unsigned long long>(e) << 1) | (lit < 0 ? 1ull : 0ull);
             for (std::uint32_t h = hslot(a, hm);; h = (h + 1) & hm) {
-                unsigned long long cur_k = sm.wtab[h];
+                unsigned long long cur_k = sm.wtab()[h];
                 if (cur_k == 0ull) {
-                    cur_k = atomicCAS(sm.wtab + h, 0ull, key);
-                    if (cur_k == 0ull) { sm.pslot[i] |= h << 16; break; }
+                    cur_k = atomicCAS(sm.wtab() + h, 0ull, key);
+                    if (cur_k == 0ull) { sm.pslot()[i] |= h << 16; break; }
                 }
                 if ((cur_k >> 32) == static_cast<unsigned long long>(a + 1)) {
-                    atomicMin(sm.wtab + h, key);
-                    sm.pslot[i] |= h << 16;
+                    atomicMin(sm.wtab() + h, key);
+                    sm.pslot()[i] |= h << 16;
                     break;
                 }
             }
@@ -773,7 +776,7 @@ struct Search {
     __device__ void pass_global(std::uint32_t F, std::uint32_t T, std::uint32_t gen, std::uint32_t cur,
                                 std::uint32_t level) {
         const bool learned = c->learned_n > 0;
-        const std::int32_t* fr = sl.fr[cur];
+        const std::int32_t* fr = sl.fr(cur);
         for (std::uint32_t base = g.tid() & ~31u; base < T; base += g.size()) {
             const std::uint32_t e = base + lane_id();
             bool first = false, conflict = false, prop = false;
@@ -783,10 +786,10 @@ struct Search {
                 std::uint32_t lo = 0, hi = F;  // largest p with froff[p] <= e
                 while (hi - lo > 1) {
                     const std::uint32_t mid = (lo + hi) >> 1;
-                    if (sl.froff[mid] <= e) lo = mid; else hi = mid;
+                    if (sl.froff()[mid] <= e) lo = mid; else hi = mid;
                 }
-                id = occ_entry(lidx(fr[lo]), e - sl.froff[lo], learned);
-                const unsigned long long old = atomicMin(sl.claim + id, ckey(gen, e));
+                id = occ_entry(lidx(fr[lo]), e - sl.froff()[lo], learned);
+                const unsigned long long old = atomicMin(sl.claim() + id, ckey(gen, e));
                 first = static_cast<std::uint32_t>(old >> 32) != ~gen;
                 if (first) evaluate(id, conflict, prop, plit, clen);
             }
@@ -794,19 +797,19 @@ struct Search {
             warp_count(&c->st.checks, first);
             warp_sum(&c->st.checked_lits, clen);
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-            if (conflict) sl.confl[cs] = id;
+            if (conflict) sl.confl()[cs] = id;
             const std::uint32_t ps = warp_append(&c->n_props, prop);
-            if (prop) sl.props[ps] = make_int4(id, plit, 0, 0);
+            if (prop) sl.props()[ps] = make_int4(id, plit, 0, 0);
         }
         g.sync();
         // resolve: final min-e of every proposing nogood, atomicMin per atom
         const std::uint32_t np = c->n_props;
         for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
-            int4 p = sl.props[i];
-            const std::uint32_t e = static_cast<std::uint32_t>(sl.claim[p.x]);
+            int4 p = sl.props()[i];
+            const std::uint32_t e = static_cast<std::uint32_t>(sl.claim()[p.x]);
             p.z = static_cast<std::int32_t>(e);
-            sl.props[i] = p;
-            atomicMin(sl.win + atom_of(p.y), wkey(gen, e, p.y < 0));
+            sl.props()[i] = p;
+            atomicMin(sl.win() + atom_of(p.y), wkey(gen, e, p.y < 0));
         }
         g.sync();
         apply<false>(level, false);
@@ -822,7 +825,7 @@ struct Search {
             const std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, viol = c->b[11];
             if (viol) return true;
             if (F == 0) return false;
-            if (sm.tcap && T <= sm.tcap && F + 1 <= sm.fcap) pass_smem(F, T, cur, level);
+            if (sm.tcap() && T <= sm.tcap() && F + 1 <= sm.fcap()) pass_smem(F, T, cur, level);
             else pass_global(F, T, gen, cur, level);
         }
     }
@@ -846,7 +849,7 @@ struct Search {
                     id = -static_cast<std::int32_t>(e) - 1;
                 } else {
                     const std::uint32_t m = e - n1;
-                    id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits[m - S.n_uids];
+                    id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits()[m - S.n_uids];
                     std::uint32_t len;
                     const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
                     sigma = lit_at(L, 0, static_cast<std::uint32_t>(id));
@@ -859,15 +862,15 @@ struct Search {
                         conflict = (cv > 0) != (lit > 0);
                     } else {
                         prop = true;
-                        atomicMin(sl.win + atom_of(lit), wkey(gen, e, lit < 0));
+                        atomicMin(sl.win() + atom_of(lit), wkey(gen, e, lit < 0));
                     }
                 }
             }
             __syncwarp();
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-            if (conflict) sl.confl[cs] = id;
+            if (conflict) sl.confl()[cs] = id;
             const std::uint32_t ps = warp_append(&c->n_props, prop);
-            if (prop) sl.props[ps] = make_int4(id, lit, static_cast<std::int32_t>(e), 0);
+            if (prop) sl.props()[ps] = make_int4(id, lit, static_cast<std::int32_t>(e), 0);
         }
         g.sync();
         // passive unit entries see the assignments made before them in order
@@ -876,7 +879,7 @@ struct Search {
             bool conflict = false;
             std::int32_t id = 0;
             if (m < n2) {
-                id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits[m - S.n_uids];
+                id = m < S.n_uids ? __ldg(S.uids + m) : sl.lunits()[m - S.n_uids];
                 std::uint32_t len;
                 const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
                 const std::int32_t sigma = lit_at(L, 0, static_cast<std::uint32_t>(id));
@@ -886,7 +889,7 @@ struct Search {
                     if (cv != 0) {
                         conflict = (cv > 0) == (sigma > 0);
                     } else {
-                        const unsigned long long w = sl.win[a];
+                        const unsigned long long w = sl.win()[a];
                         conflict = static_cast<std::uint32_t>(w >> 32) == ~gen &&
                                    (static_cast<std::uint32_t>(w) >> 1) < n1 + m &&
                                    ((w & 1ull) != 0) == (sigma < 0);
@@ -895,7 +898,7 @@ struct Search {
             }
             __syncwarp();
             const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-            if (conflict) sl.confl[cs] = id;
+            if (conflict) sl.confl()[cs] = id;
         }
         g.sync();
         apply<false>(1, true);
@@ -911,18 +914,18 @@ struct Search {
     __device__ void backjump(std::uint32_t target) {
         if (g.leader()) {
             const std::uint32_t cdl = c->cdl;
-            c->b[8] = target < cdl ? sl.tpos[atom_of(sl.ldec[target + 1])] : c->ts;
+            c->b[8] = target < cdl ? sl.tpos()[atom_of(sl.ldec()[target + 1])] : c->ts;
         }
         g.sync();
         const std::uint32_t from = c->b[8], to = c->ts;
         for (std::uint32_t i = from + g.tid(); i < to; i += g.size()) {
-            const std::uint32_t a = atom_of(sl.trail[i]);
-            const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
+            const std::uint32_t a = atom_of(sl.trail()[i]);
+            const std::uint32_t nw = nwords(lvl_of(sl.cells()[a]));
             for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
-            sl.dovf[a] = 0;
+            sl.dovf()[a] = 0;
             set_cell(a, 0);
-            sl.tpos[a] = 0;
-            sl.reason[a] = kReasonNone;
+            sl.tpos()[a] = 0;
+            sl.reason()[a] = kReasonNone;
         }
         g.sync();
         if (g.leader() && target < c->cdl) {
@@ -969,15 +972,15 @@ struct Search {
         const std::uint32_t mask = K.dupcap - 1;
         const unsigned long long tag = static_cast<unsigned long long>(c->epoch) << 32;
         for (std::uint32_t at = static_cast<std::uint32_t>(h ^ (h >> 32)) & mask;; at = (at + 1) & mask) {
-            const unsigned long long ent = sl.dup[at];
+            const unsigned long long ent = sl.dup()[at];
             if ((ent >> 32) != c->epoch || ent == 0) {
-                sl.dup[at] = tag | (c->learned_n + 1);
+                sl.dup()[at] = tag | (c->learned_n + 1);
                 break;
             }
             const std::uint32_t other = static_cast<std::uint32_t>(ent) - 1;
-            const std::uint32_t olo = sl.loff[other], olen = sl.loff[other + 1] - olo;
+            const std::uint32_t olo = sl.loff()[other], olen = sl.loff()[other + 1] - olo;
             bool same = olen == len;
-            for (std::uint32_t k = 0; same && k < len; ++k) same = sl.lpool[olo + k] == lits[k];
+            for (std::uint32_t k = 0; same && k < len; ++k) same = sl.lpool()[olo + k] == lits[k];
             if (same) {
                 c->st.duplicate_learned += 1;
                 break;
@@ -986,13 +989,13 @@ struct Search {
         const std::uint32_t k = c->learned_n;
         const std::uint32_t id = S.N + k;
         const std::uint32_t lo = c->lpool_used;
-        for (std::uint32_t j = 0; j < len; ++j) sl.lpool[lo + j] = lits[j];
-        sl.loff[k + 1] = lo + len;
+        for (std::uint32_t j = 0; j < len; ++j) sl.lpool()[lo + j] = lits[j];
+        sl.loff()[k + 1] = lo + len;
         c->lpool_used = lo + len;
         const std::uint32_t cls = len >= 4 ? 3u : len - 1u;
         for (std::uint32_t j = 0; j < len; ++j) {
             const std::uint32_t li = lidx(lits[j]);
-            std::uint32_t* h3 = sl.lhdr + 3 * (li * 4 + cls);
+            std::uint32_t* h3 = sl.lhdr() + 3 * (li * 4 + cls);
             if (h3[1] == h3[2]) {
                 const std::uint32_t ncap = h3[2] ? 2 * h3[2] : 4u;
                 if (c->locc_used + ncap > K.larena) {
@@ -1000,16 +1003,16 @@ struct Search {
                     return -1;
                 }
                 const std::uint32_t np = c->locc_used;
-                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena[np + q] = sl.larena[h3[0] + q];
+                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena()[np + q] = sl.larena()[h3[0] + q];
                 h3[0] = np;
                 h3[2] = ncap;
                 c->locc_used = np + ncap;
             }
-            sl.larena[h3[0] + h3[1]] = static_cast<std::int32_t>(id);
+            sl.larena()[h3[0] + h3[1]] = static_cast<std::int32_t>(id);
             h3[1] += 1;
-            sl.ltot[li] += 1;
+            sl.ltot()[li] += 1;
         }
-        if (len == 1) sl.lunits[c->lunits_n++] = static_cast<std::int32_t>(id);
+        if (len == 1) sl.lunits()[c->lunits_n++] = static_cast<std::int32_t>(id);
         c->learned_n = k + 1;
         return static_cast<std::int32_t>(id);
     }
@@ -1030,7 +1033,7 @@ struct Search {
             }
         }
         if (rem == 0) {
-            sl.pending[c->n_pending++] = static_cast<std::int32_t>(id);
+            sl.pending()[c->n_pending++] = static_cast<std::int32_t>(id);
             return;
         }
         if (!may_assert(guard_of(id), -rem)) return;
@@ -1038,10 +1041,10 @@ struct Search {
         const std::uint32_t a = atom_of(lit), cdl = c->cdl;
         write_deps_from(L, len, id, a, cdl);
         set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
-        sl.reason[a] = static_cast<std::int32_t>(id);
-        sl.tpos[a] = c->ts;
-        sl.trail[c->ts++] = lit;
-        sl.fr[c->cur][c->F++] = lit;
+        sl.reason()[a] = static_cast<std::int32_t>(id);
+        sl.tpos()[a] = c->ts;
+        sl.trail()[c->ts++] = lit;
+        sl.fr(c->cur)[c->F++] = lit;
         c->st.propagations += 1;
     }
 
@@ -1065,9 +1068,9 @@ struct Search {
         std::uint32_t cl = 0;
         for (std::uint32_t k = 0; k < len; ++k) {
             const std::uint32_t a = atom_of(lit_at(L, k, delta));
-            const std::uint32_t lv = lvl_of(sl.cells[a]);
+            const std::uint32_t lv = lvl_of(sl.cells()[a]);
             cl = lv > cl ? lv : cl;
-            if (sl.dovf[a]) return 0xffffffffu;
+            if (sl.dovf()[a]) return 0xffffffffu;
         }
         const std::uint32_t nw = nwords(c->cdl);
         std::uint32_t n = 0;
@@ -1076,11 +1079,11 @@ struct Search {
             unsigned long long m = 0;
             for (std::uint32_t k = 0; k < len; ++k) {
                 const std::uint32_t a = atom_of(lit_at(L, k, delta));
-                if (lvl_of(sl.cells[a]) > 1) m |= dep(w, a);
+                if (lvl_of(sl.cells()[a]) > 1) m |= dep(w, a);
             }
             for (unsigned long long b = m; b; b &= b - 1) {
                 const std::uint32_t level = 64 * w + static_cast<std::uint32_t>(__ffsll(static_cast<long long>(b))) ;
-                out[n++] = sl.ldec[level];
+                out[n++] = sl.ldec()[level];
                 if (level < cl && level > target) target = level;
             }
         }
@@ -1091,7 +1094,7 @@ struct Search {
 
     // res_learning (learn.cpp:53-104): resolve until a positive UIP.
     __device__ std::uint32_t res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
-        std::uint32_t* mark = sl.mark;
+        std::uint32_t* mark = sl.mark();
         const std::uint32_t stamp = ++c->stamp;
         std::uint32_t len;
         const std::int32_t* L = lits_of(delta, len);
@@ -1104,22 +1107,22 @@ struct Search {
         for (;;) {
             std::uint32_t si = 0;
             for (std::uint32_t k = 1; k < n; ++k)
-                if (sl.tpos[out[k]] > sl.tpos[out[si]]) si = k;
+                if (sl.tpos()[out[k]] > sl.tpos()[out[si]]) si = k;
             const std::uint32_t sa = static_cast<std::uint32_t>(out[si]);
-            const std::uint32_t slev = lvl_of(sl.cells[sa]);
+            const std::uint32_t slev = lvl_of(sl.cells()[sa]);
             std::uint32_t kappa = 0;
             for (std::uint32_t k = 0; k < n; ++k)
-                if (k != si) { const std::uint32_t lv = lvl_of(sl.cells[out[k]]); kappa = lv > kappa ? lv : kappa; }
-            if (kappa != slev && sl.cells[sa] > 0) {
+                if (k != si) { const std::uint32_t lv = lvl_of(sl.cells()[out[k]]); kappa = lv > kappa ? lv : kappa; }
+            if (kappa != slev && sl.cells()[sa] > 0) {
                 target = kappa > 1 ? kappa : 1;
                 for (std::uint32_t k = 0; k < n; ++k) {
                     const std::int32_t a = out[k];
-                    out[k] = sl.cells[a] > 0 ? a : -a;
+                    out[k] = sl.cells()[a] > 0 ? a : -a;
                 }
                 sort_by_atom(out, n);
                 return n;
             }
-            const std::int32_t r = sl.reason[sa];
+            const std::int32_t r = sl.reason()[sa];
             out[si] = out[--n];
             mark[sa] = 0;
             if (r >= 0) {
@@ -1133,7 +1136,7 @@ struct Search {
                 }
             } else if (r == kReasonCompletion) {
                 for (std::uint32_t lv = 2; lv <= c->cdl; ++lv) {
-                    const std::uint32_t a = atom_of(sl.ldec[lv]);
+                    const std::uint32_t a = atom_of(sl.ldec()[lv]);
                     if (a == sa || mark[a] == stamp) continue;
                     mark[a] = stamp;
                     out[n++] = static_cast<std::int32_t>(a);
@@ -1147,7 +1150,7 @@ struct Search {
 
     __device__ void bump_activity(const std::int32_t* lits, std::uint32_t n) {
         if (C.heur != 2) return;
-        for (std::uint32_t k = 0; k < n; ++k) sl.act[atom_of(lits[k])] += c->act_inc;
+        for (std::uint32_t k = 0; k < n; ++k) sl.act()[atom_of(lits[k])] += c->act_inc;
     }
 
     // Driver::handle_conflicts (solver.cpp:161-214), leader part. Returns
@@ -1159,9 +1162,9 @@ struct Search {
         const std::uint32_t nc = c->n_confl;
         // select conflicts: min (length, id); fanout K in fwd mode (learn.cpp:148-157)
         const std::uint32_t K2 = (C.mode == 0 && C.fanout > 1) ? C.fanout : 1u;
-        std::int32_t* added = sl.scratch;            // ids of added nogoods
-        std::int32_t* levels = sl.scratch + 64;      // their backjump levels
-        std::int32_t* buf = sl.scratch + 128;        // learned literal buffer
+        std::int32_t* added = sl.scratch();            // ids of added nogoods
+        std::int32_t* levels = sl.scratch() + 64;      // their backjump levels
+        std::int32_t* buf = sl.scratch() + 128;        // learned literal buffer
         std::uint32_t n_sel = 0;
         unsigned long long prev = 0;
         bool have_prev = false;
@@ -1169,7 +1172,7 @@ struct Search {
         while (n_sel < K2) {
             unsigned long long best = ~0ull;
             for (std::uint32_t i = 0; i < nc; ++i) {
-                const std::uint32_t id = static_cast<std::uint32_t>(sl.confl[i]);
+                const std::uint32_t id = static_cast<std::uint32_t>(sl.confl()[i]);
                 const unsigned long long key = (static_cast<unsigned long long>(length_of(id)) << 32) | id;
                 if ((!have_prev || key > prev) && key < best) best = key;
             }
@@ -1190,14 +1193,14 @@ struct Search {
             // structural self-checks (solver.cpp:171-186)
             if (used == 1) {
                 std::uint32_t cl = 0, at = 0;
-                for (std::uint32_t k = 0; k < n; ++k) { const std::uint32_t lv = lvl_of(sl.cells[atom_of(buf[k])]); cl = lv > cl ? lv : cl; }
-                for (std::uint32_t k = 0; k < n; ++k) at += lvl_of(sl.cells[atom_of(buf[k])]) == cl;
+                for (std::uint32_t k = 0; k < n; ++k) { const std::uint32_t lv = lvl_of(sl.cells()[atom_of(buf[k])]); cl = lv > cl ? lv : cl; }
+                for (std::uint32_t k = 0; k < n; ++k) at += lvl_of(sl.cells()[atom_of(buf[k])]) == cl;
                 if (at != 1) c->st.uip_check_failures += 1;
                 c->st.res_learned += 1;
                 if (C.mode == 0) c->st.fwd_fallbacks += 1;
             } else {
                 for (std::uint32_t k = 0; k < n; ++k)
-                    if (sl.reason[atom_of(buf[k])] != kReasonDecision) c->st.fwd_decision_only_failures += 1;
+                    if (sl.reason()[atom_of(buf[k])] != kReasonDecision) c->st.fwd_decision_only_failures += 1;
                 c->st.fwd_learned += 1;
             }
             const std::int32_t id = add_learned(buf, n);
@@ -1210,13 +1213,13 @@ struct Search {
             c->st.learned_length_sum += n;
             bump_activity(buf, n);
             if (C.trace && c->n_trace < K.tcap)
-                sl.tbuf[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
+                sl.tbuf()[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
         }
         // Heuristic::on_conflict (decide.cpp:34-41)
         if (C.heur == 2) {
             c->act_inc /= C.decay;
             if (c->act_inc > 1e100) {
-                for (std::uint32_t a = 0; a <= S.A; ++a) sl.act[a] *= 1e-100;
+                for (std::uint32_t a = 0; a <= S.A; ++a) sl.act()[a] *= 1e-100;
                 c->act_inc *= 1e-100;
             }
         }
@@ -1246,8 +1249,8 @@ struct Search {
         if (restart) initial_propagation(false);
         if (g.leader()) {
             const std::uint32_t n_sel = c->b[3];
-            const std::int32_t* added = sl.scratch;
-            const std::int32_t* levels = sl.scratch + 64;
+            const std::int32_t* added = sl.scratch();
+            const std::int32_t* levels = sl.scratch() + 64;
             if (!restart)
                 for (std::uint32_t i = 0; i < n_sel; ++i)
                     if (static_cast<std::uint32_t>(levels[i]) == target && !is_unit_now(static_cast<std::uint32_t>(added[i])))
@@ -1259,7 +1262,7 @@ struct Search {
     }
 
     __device__ double score(std::uint32_t head) const {
-        if (C.heur == 2) return sl.act[head];
+        if (C.heur == 2) return sl.act()[head];
         if (C.heur == 0) return static_cast<double>(occ_total(2 * head) + occ_total(2 * head + 1));
         double s = 0.0;  // Jeroslow-Wang, summed in the reference's list order
         for (std::uint32_t li = 2 * head; li <= 2 * head + 1; ++li)
@@ -1267,9 +1270,9 @@ struct Search {
                 const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
                 for (std::uint32_t j = lo; j < hi; ++j)
                     s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ_ids + j)))));
-                const std::uint32_t* h = sl.lhdr + 3 * (li * 4 + cl);
+                const std::uint32_t* h = sl.lhdr() + 3 * (li * 4 + cl);
                 for (std::uint32_t j = 0; j < h[1]; ++j)
-                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena[h[0] + j]))));
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena()[h[0] + j]))));
             }
         return s;
     }
@@ -1293,16 +1296,16 @@ struct Search {
             if (g.leader()) {
                 const std::uint32_t b = __ldg(S.rules + bi).y;
                 const std::uint32_t cdl = ++c->cdl;
-                sl.ldec[cdl] = static_cast<std::int32_t>(b);
+                sl.ldec()[cdl] = static_cast<std::int32_t>(b);
                 set_cell(b, static_cast<std::int32_t>(cdl));
-                sl.tpos[b] = c->ts;
-                sl.trail[c->ts++] = static_cast<std::int32_t>(b);
-                sl.reason[b] = kReasonDecision;
+                sl.tpos()[b] = c->ts;
+                sl.trail()[c->ts++] = static_cast<std::int32_t>(b);
+                sl.reason()[b] = kReasonDecision;
                 const std::uint32_t bit = cdl - 1;
-                if (bit >= 64 * C.W) sl.dovf[b] = 1;
+                if (bit >= 64 * C.W) sl.dovf()[b] = 1;
                 else dep(bit / 64, b) |= 1ull << (bit % 64);
                 c->st.decisions += 1;
-                sl.fr[c->cur][0] = static_cast<std::int32_t>(b);
+                sl.fr(c->cur)[0] = static_cast<std::int32_t>(b);
                 c->F = 1;
             }
             g.sync();
@@ -1321,7 +1324,7 @@ struct Search {
             const std::uint32_t r = static_cast<std::uint32_t>(g.scan(open ? 1ull : 0ull, tot) + carry);
             if (open) {
                 set_cell(a, -static_cast<std::int32_t>(cdl));
-                sl.reason[a] = kReasonCompletion;
+                sl.reason()[a] = kReasonCompletion;
                 for (std::uint32_t w = 0; w < nw; ++w) {
                     unsigned long long m = 0;
                     if (cdl >= 2) {
@@ -1334,10 +1337,10 @@ struct Search {
                     }
                     dep(w, a) = m;
                 }
-                sl.dovf[a] = ovf;
-                sl.tpos[a] = ts0 + r;
-                sl.trail[ts0 + r] = -static_cast<std::int32_t>(a);
-                sl.fr[cur][r] = -static_cast<std::int32_t>(a);
+                sl.dovf()[a] = ovf;
+                sl.tpos()[a] = ts0 + r;
+                sl.trail()[ts0 + r] = -static_cast<std::int32_t>(a);
+                sl.fr(cur)[r] = -static_cast<std::int32_t>(a);
             }
             carry += tot;
         }
@@ -1357,11 +1360,11 @@ struct Search {
                 const std::uint32_t a = 32 * w + b + 1;
                 if (a <= S.n_prog && val(a) > 0) bits |= 1u << b;
             }
-            sl.mbuf[static_cast<std::size_t>(m) * words + w] = bits;
+            sl.mbuf()[static_cast<std::size_t>(m) * words + w] = bits;
         }
         g.sync();
         if (g.leader()) {
-            sl.mcube[m] = cube;
+            sl.mcube()[m] = cube;
             c->n_mbuf = m + 1;
             c->st.models += 1;
             c->pad0 += 1;  // models of this search
@@ -1375,8 +1378,8 @@ struct Search {
             c->b[0] = 0;
             const std::uint32_t cdl = c->cdl;
             if (cdl > 1) {
-                std::int32_t* buf = sl.scratch + 128;
-                for (std::uint32_t lv = 2; lv <= cdl; ++lv) buf[lv - 2] = sl.ldec[lv];
+                std::int32_t* buf = sl.scratch() + 128;
+                for (std::uint32_t lv = 2; lv <= cdl; ++lv) buf[lv - 2] = sl.ldec()[lv];
                 sort_by_atom(buf, cdl - 1);
                 const std::int32_t id = add_learned(buf, cdl - 1);
                 if (id >= 0) {
@@ -1423,21 +1426,21 @@ struct Search {
     __device__ void begin_search(std::uint32_t cube) {
         const std::uint32_t ts = c->ts;
         for (std::uint32_t i = g.tid(); i < ts; i += g.size()) {
-            const std::uint32_t a = atom_of(sl.trail[i]);
-            const std::uint32_t nw = nwords(lvl_of(sl.cells[a]));
+            const std::uint32_t a = atom_of(sl.trail()[i]);
+            const std::uint32_t nw = nwords(lvl_of(sl.cells()[a]));
             for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
-            sl.dovf[a] = 0;
+            sl.dovf()[a] = 0;
             set_cell(a, 0);
-            sl.tpos[a] = 0;
-            sl.reason[a] = kReasonNone;
+            sl.tpos()[a] = 0;
+            sl.reason()[a] = kReasonNone;
         }
         const std::uint32_t keys = (2 * S.A + 2) * 4;
         if (c->learned_n > 0 || c->epoch == 0) {
-            for (std::uint32_t i = g.tid(); i < 3 * keys; i += g.size()) sl.lhdr[i] = 0;
-            for (std::uint32_t i = g.tid(); i < 2 * S.A + 2; i += g.size()) sl.ltot[i] = 0;
+            for (std::uint32_t i = g.tid(); i < 3 * keys; i += g.size()) sl.lhdr()[i] = 0;
+            for (std::uint32_t i = g.tid(); i < 2 * S.A + 2; i += g.size()) sl.ltot()[i] = 0;
         }
         if (C.heur == 2)
-            for (std::uint32_t i = g.tid(); i <= S.A; i += g.size()) sl.act[i] = 0.0;
+            for (std::uint32_t i = g.tid(); i <= S.A; i += g.size()) sl.act()[i] = 0.0;
         g.sync();
         if (g.leader()) {
             c->cdl = 1;
@@ -1447,7 +1450,7 @@ struct Search {
             c->T = 0;
             c->n_props = c->n_confl = c->n_pending = 0;
             c->learned_n = c->lpool_used = c->locc_used = c->lunits_n = 0;
-            sl.loff[0] = 0;
+            sl.loff()[0] = 0;
             c->cube = cube;
             c->epoch += 1;
             if (c->gen == 0) c->gen = 1;  // claim/win keys of generation 0 equal the all-ones init
@@ -1517,7 +1520,7 @@ struct Search {
                 conflicted = propagate(c->cdl);
             } else {
                 if (g.leader()) {
-                    for (std::uint32_t i = 0; i < c->n_pending; ++i) sl.confl[i] = sl.pending[i];
+                    for (std::uint32_t i = 0; i < c->n_pending; ++i) sl.confl()[i] = sl.pending()[i];
                     c->n_confl = c->n_pending;
                     c->n_pending = 0;
                 }
@@ -1559,19 +1562,19 @@ struct Search {
 template <class G>
 __device__ void init_smem(G& g, Search<G>& s) {
     const Sm& m = s.sm;
-    if (m.tcap) {
-        for (std::uint32_t i = g.tid(); i <= m.hmask; i += g.size()) {
-            m.htab[i] = 0ull;
-            m.wtab[i] = 0ull;
+    if (m.tcap()) {
+        for (std::uint32_t i = g.tid(); i <= m.hmask(); i += g.size()) {
+            m.htab()[i] = 0ull;
+            m.wtab()[i] = 0ull;
         }
-        for (std::uint32_t i = g.tid(); i < (m.tcap + 31) / 32; i += g.size()) m.bits[i] = 0u;
+        for (std::uint32_t i = g.tid(); i < (m.tcap() + 31) / 32; i += g.size()) m.bits()[i] = 0u;
     }
     s.rebuild_mirror();
     g.sync();
 }
 
 template <class G>
-__device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh,
+__device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const Caps& K, Shared* sh,
                           const Sm& sm) {
     const unsigned long long t0 = gtimer();
     Search<G> s(g, S, C, sl, K, sh, t0, sm);
@@ -1598,44 +1601,49 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, const Slot& sl
     }
 }
 
-template <int BS>
-__global__ void __launch_bounds__(BS) block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                   Shared* sh, SmemCfg smc) {
-    extern __shared__ __align__(16) unsigned char dsm[];
+// One CTA per search slot; slot k = blockIdx.x. MINB = resident CTAs per SM the
+// register budget is planned for (1: single search, 4: cube enumeration).
+template <int BS, int MINB>
+__global__ void __launch_bounds__(BS, MINB)
+    block_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
+                 const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
+                 const __grid_constant__ SmemCfg smc) {
     __shared__ Ctl ctl;
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
-    const Slot sl = slots[blockIdx.x];
+    const Slot sl{L.base + static_cast<unsigned long long>(blockIdx.x) * L.bytes, &L};
     {
-        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl);
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl());
         std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&ctl);
         for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
     }
     __syncthreads();
     if (threadIdx.x == 0 && ctl.status == kYield) ctl.status = kRunning;
     BlockG<BS> g{&ctl, sbuf, sd, si};
-    slot_loop(g, S, C, sl, K, sh, carve_smem(dsm, smc));
+    slot_loop(g, S, C, sl, K, sh, Sm{&smc});
     __syncthreads();
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
-        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl());
         for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
     }
 }
 
+// Every CTA of a cooperative grid works on slot 0.
 template <int BS>
-__global__ void __launch_bounds__(BS) grid_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                  Shared* sh, unsigned long long* partial, double* pd,
-                                                  std::uint32_t* pi) {
+__global__ void __launch_bounds__(BS, 1)
+    grid_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
+                const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
+                unsigned long long* partial, double* pd, std::uint32_t* pi, const __grid_constant__ SmemCfg smc) {
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
-    const Slot sl = slots[0];
-    GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
-    if (g.leader() && sl.ctl->status == kYield) sl.ctl->status = kRunning;
+    const Slot sl{L.base, &L};
+    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u};
+    if (g.leader() && sl.ctl()->status == kYield) sl.ctl()->status = kRunning;
     g.sync();
-    slot_loop(g, S, C, sl, K, sh, Sm{});
+    slot_loop(g, S, C, sl, K, sh, Sm{&smc});
 }
 
 // Low-level operations on one slot (Propagator-style API for tests and the
@@ -1654,7 +1662,7 @@ struct OpArgs {
 };
 
 template <class G>
-__device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, const Caps& K, Shared* sh,
+__device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Caps& K, Shared* sh,
                       const OpArgs& op, const Sm& sm) {
     Search<G> s(g, S, C, sl, K, sh, 0, sm);
     init_smem(g, s);
@@ -1686,13 +1694,13 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
                 const std::int32_t lit = op.lit;
                 const std::uint32_t a = atom_of(lit);
                 const std::uint32_t cdl = ++c->cdl;
-                sl.ldec[cdl] = lit;
+                sl.ldec()[cdl] = lit;
                 s.set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
-                sl.tpos[a] = c->ts;
-                sl.trail[c->ts++] = lit;
-                sl.reason[a] = kReasonDecision;
+                sl.tpos()[a] = c->ts;
+                sl.trail()[c->ts++] = lit;
+                sl.reason()[a] = kReasonDecision;
                 const std::uint32_t bit = cdl - 1;
-                if (bit >= 64 * C.W) sl.dovf[a] = 1;
+                if (bit >= 64 * C.W) sl.dovf()[a] = 1;
                 else s.dep(bit / 64, a) |= 1ull << (bit % 64);
             }
             g.sync();
@@ -1710,11 +1718,11 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
                 const std::uint32_t r = static_cast<std::uint32_t>(g.scan(fresh ? 1ull : 0ull, tot) + carry);
                 if (fresh) {
                     s.set_cell(a, lit > 0 ? static_cast<std::int32_t>(op.level) : -static_cast<std::int32_t>(op.level));
-                    sl.tpos[a] = ts0 + r;
-                    sl.trail[ts0 + r] = lit;
-                    sl.reason[a] = op.antecedent;
+                    sl.tpos()[a] = ts0 + r;
+                    sl.trail()[ts0 + r] = lit;
+                    sl.reason()[a] = op.antecedent;
                     for (std::uint32_t w = 0; w < C.W; ++w) s.dep(w, a) = op.deps ? op.deps[w] : 0ull;
-                    sl.dovf[a] = static_cast<std::uint8_t>(op.ovf);
+                    sl.dovf()[a] = static_cast<std::uint8_t>(op.ovf);
                 }
                 carry += tot;
             }
@@ -1724,14 +1732,14 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
             break;
         }
         case kOpSeed:  // frontier.last.push_back for a bulk of literals
-            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr[c->cur][c->F + k] = op.lits[k];
+            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr(c->cur)[c->F + k] = op.lits[k];
             g.sync();
             if (g.leader()) c->F += op.n;
             g.sync();
             break;
         case kOpLearn:  // NogoodStore::add_learned (kNoTruth guard)
             if (g.leader()) {
-                std::int32_t* buf = sl.scratch + 128;
+                std::int32_t* buf = sl.scratch() + 128;
                 for (std::uint32_t k = 0; k < op.n; ++k) buf[k] = op.lits[k];
                 s.sort_by_atom(buf, op.n);
                 c->b[12] = static_cast<std::uint32_t>(s.add_learned(buf, op.n));
@@ -1744,40 +1752,53 @@ __device__ void do_op(G& g, const Static& S, const Config& C, const Slot& sl, co
 }
 
 template <int BS>
-__global__ void __launch_bounds__(BS) op_block_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                      Shared* sh, OpArgs op, SmemCfg smc) {
-    extern __shared__ __align__(16) unsigned char dsm[];
+__global__ void __launch_bounds__(BS, 1)
+    op_block_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
+                    const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh, OpArgs op,
+                    const __grid_constant__ SmemCfg smc) {
     __shared__ Ctl ctl;
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
-    const Slot sl = slots[0];
+    const Slot sl{L.base, &L};
     {
-        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl);
+        const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl());
         std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&ctl);
         for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
     }
     __syncthreads();
     BlockG<BS> g{&ctl, sbuf, sd, si};
-    do_op(g, S, C, sl, K, sh, op, carve_smem(dsm, smc));
+    do_op(g, S, C, sl, K, sh, op, Sm{&smc});
     __syncthreads();
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
-        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl);
+        std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(sl.ctl());
         for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
     }
 }
 
 template <int BS>
-__global__ void __launch_bounds__(BS) op_grid_kernel(Static S, Config C, const Slot* __restrict__ slots, Caps K,
-                                                     Shared* sh, unsigned long long* partial, double* pd,
-                                                     std::uint32_t* pi, OpArgs op) {
+__global__ void __launch_bounds__(BS, 1)
+    op_grid_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
+                   const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
+                   unsigned long long* partial, double* pd, std::uint32_t* pi, OpArgs op,
+                   const __grid_constant__ SmemCfg smc) {
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
-    const Slot sl = slots[0];
-    GridG<BS> g{sl.ctl, sh, partial, pd, pi, sbuf, sd, si, 0u};
-    do_op(g, S, C, sl, K, sh, op, Sm{});
+    const Slot sl{L.base, &L};
+    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u};
+    do_op(g, S, C, sl, K, sh, op, Sm{&smc});
+}
+
+// Per-slot initial values that are not zero.
+__global__ void init_slots(const __grid_constant__ SlotLayout L, std::uint32_t A1, std::uint32_t items) {
+    const Slot sl{L.base + static_cast<unsigned long long>(blockIdx.x) * L.bytes, &L};
+    for (std::uint32_t i = threadIdx.x; i < items; i += blockDim.x) sl.claim()[i] = ~0ull;
+    for (std::uint32_t i = threadIdx.x; i < A1; i += blockDim.x) {
+        sl.win()[i] = ~0ull;
+        sl.reason()[i] = kReasonNone;
+    }
 }
 
 }  // namespace yas::dev

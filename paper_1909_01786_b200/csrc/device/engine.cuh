@@ -102,38 +102,59 @@ struct Caps {
     std::uint32_t mwords;  // words per model bitset
 };
 
+// All mutable state of one search lives in one contiguous chunk of device
+// memory; slot k starts at base + k * bytes. Arrays are addressed as
+// chunk + constant offset, so kernels never load per-slot pointers.
+struct SlotLayout {
+    char* base;
+    unsigned long long bytes;
+    unsigned long long o_ctl, o_cells, o_tpos, o_reason, o_deps, o_dovf, o_trail, o_ldec, o_fr0, o_fr1, o_froff,
+        o_claim, o_win, o_props, o_confl, o_pending, o_bitmap, o_litat, o_loff, o_lpool, o_lhdr, o_larena,
+        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf;
+};
+
+#if defined(__CUDACC__)
+#define YAS_HD __host__ __device__ __forceinline__
+#else
+#define YAS_HD inline
+#endif
+
 struct Slot {
-    Ctl* ctl;
-    std::int32_t* cells;
-    std::uint32_t* tpos;
-    std::int32_t* reason;
-    unsigned long long* deps;  // word-major: deps[w*(A+1) + atom]
-    std::uint8_t* dovf;
-    std::int32_t* trail;
-    std::int32_t* ldec;
-    std::int32_t* fr[2];
-    std::uint32_t* froff;
-    unsigned long long* claim;  // per nogood id: (~gen << 32) | min expansion index
-    unsigned long long* win;    // per atom: (~gen << 32) | (e << 1) | negative
-    int4* props;                // (id, lit, e, -)
-    std::int32_t* confl;
-    std::int32_t* pending;
-    std::uint32_t* bitmap;
-    std::int32_t* litat;
-    std::uint32_t* loff;     // lcap+1
-    std::int32_t* lpool;
-    std::uint32_t* lhdr;     // (2A+2)*4 * {ptr,size,cap}
-    std::int32_t* larena;
-    std::int32_t* lunits;
-    std::uint32_t* ltot;     // per literal index: learned occurrences
-    double* act;
-    unsigned long long* dup;
-    std::int32_t* scratch;   // >= 2*(A+2) ints
-    std::uint32_t* mark;     // A+1
-    unsigned long long* merged;  // W words
-    std::uint32_t* mbuf;     // mcap * mwords
-    std::uint32_t* mcube;    // mcap
-    uint4* tbuf;             // tcap trace records (mode, conflict id, len, backjump)
+    char* b;
+    const SlotLayout* L;
+    template <class T>
+    YAS_HD T* at(unsigned long long off) const { return reinterpret_cast<T*>(b + off); }
+    YAS_HD Ctl* ctl() const { return at<Ctl>(L->o_ctl); }
+    YAS_HD std::int32_t* cells() const { return at<std::int32_t>(L->o_cells); }
+    YAS_HD std::uint32_t* tpos() const { return at<std::uint32_t>(L->o_tpos); }
+    YAS_HD std::int32_t* reason() const { return at<std::int32_t>(L->o_reason); }
+    YAS_HD unsigned long long* deps() const { return at<unsigned long long>(L->o_deps); }  // word-major
+    YAS_HD std::uint8_t* dovf() const { return at<std::uint8_t>(L->o_dovf); }
+    YAS_HD std::int32_t* trail() const { return at<std::int32_t>(L->o_trail); }
+    YAS_HD std::int32_t* ldec() const { return at<std::int32_t>(L->o_ldec); }
+    YAS_HD std::int32_t* fr(std::uint32_t k) const { return at<std::int32_t>(k ? L->o_fr1 : L->o_fr0); }
+    YAS_HD std::uint32_t* froff() const { return at<std::uint32_t>(L->o_froff); }
+    YAS_HD unsigned long long* claim() const { return at<unsigned long long>(L->o_claim); }  // (~gen<<32)|min e
+    YAS_HD unsigned long long* win() const { return at<unsigned long long>(L->o_win); }  // (~gen<<32)|(e<<1)|neg
+    YAS_HD int4* props() const { return at<int4>(L->o_props); }  // (id, lit, e, -)
+    YAS_HD std::int32_t* confl() const { return at<std::int32_t>(L->o_confl); }
+    YAS_HD std::int32_t* pending() const { return at<std::int32_t>(L->o_pending); }
+    YAS_HD std::uint32_t* bitmap() const { return at<std::uint32_t>(L->o_bitmap); }
+    YAS_HD std::int32_t* litat() const { return at<std::int32_t>(L->o_litat); }
+    YAS_HD std::uint32_t* loff() const { return at<std::uint32_t>(L->o_loff); }
+    YAS_HD std::int32_t* lpool() const { return at<std::int32_t>(L->o_lpool); }
+    YAS_HD std::uint32_t* lhdr() const { return at<std::uint32_t>(L->o_lhdr); }  // (2A+2)*4 * {ptr,size,cap}
+    YAS_HD std::int32_t* larena() const { return at<std::int32_t>(L->o_larena); }
+    YAS_HD std::int32_t* lunits() const { return at<std::int32_t>(L->o_lunits); }
+    YAS_HD std::uint32_t* ltot() const { return at<std::uint32_t>(L->o_ltot); }
+    YAS_HD double* act() const { return at<double>(L->o_act); }
+    YAS_HD unsigned long long* dup() const { return at<unsigned long long>(L->o_dup); }
+    YAS_HD std::int32_t* scratch() const { return at<std::int32_t>(L->o_scratch); }
+    YAS_HD std::uint32_t* mark() const { return at<std::uint32_t>(L->o_mark); }
+    YAS_HD unsigned long long* merged() const { return at<unsigned long long>(L->o_merged); }
+    YAS_HD std::uint32_t* mbuf() const { return at<std::uint32_t>(L->o_mbuf); }
+    YAS_HD std::uint32_t* mcube() const { return at<std::uint32_t>(L->o_mcube); }
+    YAS_HD uint4* tbuf() const { return at<uint4>(L->o_tbuf); }
 };
 
 struct Shared {  // global (all-slot) coordination

@@ -40,8 +40,8 @@ struct Arena {
     std::vector<void*> owned;
     dev::Static S{};
     dev::Caps K{};
+    dev::SlotLayout L{};
     std::vector<dev::Slot> slots;
-    dev::Slot* d_slots = nullptr;
     dev::Shared* sh = nullptr;
     unsigned long long* partial = nullptr;
     double* pd = nullptr;
@@ -88,100 +88,57 @@ struct Arena {
         K.mcap = mcap;
         K.tcap = tcap;
         K.mwords = (S.n_prog + 31) / 32 ? (S.n_prog + 31) / 32 : 1;
-        slots.resize(n_slots);
-        auto each = [&](auto* base, std::size_t per, std::uint32_t s) { return base + per * s; };
-        // per-array bases for all slots
-        const std::size_t ns = n_slots;
-        auto* ctl = dalloc<dev::Ctl>(ns, owned);
-        auto* cells = dalloc<std::int32_t>(ns * A1, owned);
-        auto* tpos = dalloc<std::uint32_t>(ns * A1, owned);
-        auto* reason = dalloc<std::int32_t>(ns * A1, owned);
-        auto* deps = dalloc<unsigned long long>(ns * W * A1, owned);
-        auto* dovf = dalloc<std::uint8_t>(ns * A1, owned);
-        auto* trail = dalloc<std::int32_t>(ns * A1, owned);
-        auto* ldec = dalloc<std::int32_t>(ns * (A1 + 1), owned);
-        auto* fr0 = dalloc<std::int32_t>(ns * A1, owned);
-        auto* fr1 = dalloc<std::int32_t>(ns * A1, owned);
-        auto* froff = dalloc<std::uint32_t>(ns * (A1 + 1), owned);
-        auto* claim = dalloc<unsigned long long>(ns * K.items, owned);
-        auto* win = dalloc<unsigned long long>(ns * A1, owned);
-        auto* props = dalloc<int4>(ns * K.items, owned);
-        auto* confl = dalloc<std::int32_t>(ns * K.items, owned);
-        auto* pending = dalloc<std::int32_t>(ns * 64, owned);
-        auto* loff = dalloc<std::uint32_t>(ns * (K.lcap + 1), owned);
-        auto* lpoolp = dalloc<std::int32_t>(ns * K.lpool, owned);
-        auto* lhdr = dalloc<std::uint32_t>(ns * keys * 3, owned);
-        auto* larena = dalloc<std::int32_t>(ns * K.larena, owned);
-        auto* lunits = dalloc<std::int32_t>(ns * K.lcap, owned);
-        auto* ltot = dalloc<std::uint32_t>(ns * (2 * A1), owned);
-        auto* act = dalloc<double>(ns * A1, owned);
-        auto* dup = dalloc<unsigned long long>(ns * K.dupcap, owned);
-        auto* scratch = dalloc<std::int32_t>(ns * (A1 + 256), owned);
-        auto* mark = dalloc<std::uint32_t>(ns * A1, owned);
-        auto* merged = dalloc<unsigned long long>(ns * W, owned);
-        auto* mbuf = dalloc<std::uint32_t>(ns * static_cast<std::size_t>(mcap) * K.mwords, owned);
-        auto* mcube = dalloc<std::uint32_t>(ns * mcap, owned);
-        auto* tbuf = dalloc<uint4>(ns * tcap, owned);
         // expansion bitmap: bounded by the literal occurrences of the store
         // (static + learned) and by the initial-propagation item count.
         std::uint64_t tbits = std::max<std::uint64_t>(pool_size_ + K.lpool, S.n_units + S.n_uids + K.lcap) + 64;
         tbits = (tbits + 31) / 32 * 32;
         K.tbits = static_cast<std::uint32_t>(tbits);
-        auto* bitmap = dalloc<std::uint32_t>(ns * (tbits / 32), owned);
-        auto* litat = dalloc<std::int32_t>(ns * tbits, owned);
-
-        ck(cudaMemset(ctl, 0, ns * sizeof(dev::Ctl)), "memset");
-        ck(cudaMemset(cells, 0, ns * A1 * 4), "memset");
-        ck(cudaMemset(tpos, 0, ns * A1 * 4), "memset");
-        ck(cudaMemset(reason, 0xFF, ns * A1 * 4), "memset");
-        ck(cudaMemset(deps, 0, ns * W * A1 * 8), "memset");
-        ck(cudaMemset(dovf, 0, ns * A1), "memset");
-        ck(cudaMemset(claim, 0xFF, ns * K.items * 8), "memset");
-        ck(cudaMemset(win, 0xFF, ns * A1 * 8), "memset");
-        ck(cudaMemset(bitmap, 0, ns * (tbits / 32) * 4), "memset");
-        ck(cudaMemset(loff, 0, ns * (K.lcap + 1) * 4), "memset");
-        ck(cudaMemset(lhdr, 0, ns * keys * 3 * 4), "memset");
-        ck(cudaMemset(ltot, 0, ns * 2 * A1 * 4), "memset");
-        ck(cudaMemset(act, 0, ns * A1 * 8), "memset");
-        ck(cudaMemset(dup, 0, ns * static_cast<std::size_t>(K.dupcap) * 8), "memset");
-        ck(cudaMemset(mark, 0, ns * A1 * 4), "memset");
-
-        for (std::uint32_t s = 0; s < n_slots; ++s) {
-            dev::Slot& q = slots[s];
-            q.ctl = ctl + s;
-            q.cells = each(cells, A1, s);
-            q.tpos = each(tpos, A1, s);
-            q.reason = each(reason, A1, s);
-            q.deps = each(deps, W * A1, s);
-            q.dovf = each(dovf, A1, s);
-            q.trail = each(trail, A1, s);
-            q.ldec = each(ldec, A1 + 1, s);
-            q.fr[0] = each(fr0, A1, s);
-            q.fr[1] = each(fr1, A1, s);
-            q.froff = each(froff, A1 + 1, s);
-            q.claim = each(claim, K.items, s);
-            q.win = each(win, A1, s);
-            q.props = each(props, K.items, s);
-            q.confl = each(confl, K.items, s);
-            q.pending = each(pending, 64, s);
-            q.bitmap = each(bitmap, tbits / 32, s);
-            q.litat = each(litat, tbits, s);
-            q.loff = each(loff, K.lcap + 1, s);
-            q.lpool = each(lpoolp, K.lpool, s);
-            q.lhdr = each(lhdr, keys * 3, s);
-            q.larena = each(larena, K.larena, s);
-            q.lunits = each(lunits, K.lcap, s);
-            q.ltot = each(ltot, 2 * A1, s);
-            q.act = each(act, A1, s);
-            q.dup = each(dup, K.dupcap, s);
-            q.scratch = each(scratch, A1 + 256, s);
-            q.mark = each(mark, A1, s);
-            q.merged = each(merged, W, s);
-            q.mbuf = each(mbuf, static_cast<std::size_t>(mcap) * K.mwords, s);
-            q.mcube = each(mcube, mcap, s);
-            q.tbuf = each(tbuf, tcap, s);
-        }
-        d_slots = dupload(slots, owned);
+        // one contiguous chunk per slot
+        unsigned long long o = 0;
+        auto take = [&](std::size_t bytes) {
+            const unsigned long long at = o;
+            o += (bytes + 255) & ~static_cast<std::size_t>(255);
+            return at;
+        };
+        L.o_ctl = take(sizeof(dev::Ctl));
+        L.o_cells = take(4 * A1);
+        L.o_tpos = take(4 * A1);
+        L.o_reason = take(4 * A1);
+        L.o_deps = take(8 * W * A1);
+        L.o_dovf = take(A1);
+        L.o_trail = take(4 * A1);
+        L.o_ldec = take(4 * (A1 + 1));
+        L.o_fr0 = take(4 * A1);
+        L.o_fr1 = take(4 * A1);
+        L.o_froff = take(4 * (A1 + 1));
+        L.o_claim = take(8ull * K.items);
+        L.o_win = take(8 * A1);
+        L.o_props = take(16ull * K.items);
+        L.o_confl = take(4ull * K.items);
+        L.o_pending = take(4 * 64);
+        L.o_bitmap = take(tbits / 8);
+        L.o_litat = take(4 * tbits);
+        L.o_loff = take(4ull * (K.lcap + 1));
+        L.o_lpool = take(4ull * K.lpool);
+        L.o_lhdr = take(4 * keys * 3);
+        L.o_larena = take(4ull * K.larena);
+        L.o_lunits = take(4ull * K.lcap);
+        L.o_ltot = take(4 * 2 * A1);
+        L.o_act = take(8 * A1);
+        L.o_dup = take(8ull * K.dupcap);
+        L.o_scratch = take(4 * (A1 + 256));
+        L.o_mark = take(4 * A1);
+        L.o_merged = take(8 * W);
+        L.o_mbuf = take(4ull * mcap * K.mwords);
+        L.o_mcube = take(4ull * mcap);
+        L.o_tbuf = take(16ull * tcap);
+        L.bytes = o;
+        L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
+        ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
+        dev::init_slots<<<n_slots, 256>>>(L, static_cast<std::uint32_t>(A1), K.items);
+        ck(cudaGetLastError(), "init_slots");
+        slots.resize(n_slots);
+        for (std::uint32_t s = 0; s < n_slots; ++s) slots[s] = dev::Slot{L.base + static_cast<unsigned long long>(s) * o, &L};
         sh = dalloc<dev::Shared>(1, owned);
         ck(cudaMemset(sh, 0, sizeof(dev::Shared)), "memset");
         const std::uint32_t gb = grid_blocks ? grid_blocks : 1;
@@ -196,17 +153,13 @@ struct Arena {
 // Shared-memory working set of a single-CTA search: pass scratch for up to
 // tcap expansion entries plus the 2-bit assignment mirror, within `budget`.
 dev::SmemCfg plan_smem(std::uint32_t atoms, std::size_t budget) {
-    dev::SmemCfg c{};
     const std::uint32_t vw = (atoms + 1 + 31) / 32;
-    if (2ull * 4 * vw + 64 <= budget / 2) c.vwords = vw;
+    const std::uint32_t vwords = 2ull * 4 * vw + 64 <= budget / 2 ? vw : 0;
     for (std::uint32_t t = 16384; t >= 128; t /= 2) {
-        dev::SmemCfg x = c;
-        x.tcap = t;
-        x.hcap = 2 * t;
-        x.fcap = t + 1;
-        if (dev::smem_bytes(x) <= budget) return x;
+        const dev::SmemCfg x = dev::smem_layout(t, vwords);
+        if (x.bytes <= budget) return x;
     }
-    return c;
+    return dev::smem_layout(0, vwords);
 }
 
 std::uint32_t grid_blocks_for(int device) {
@@ -249,15 +202,19 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     std::vector<std::uint32_t> mb, mc;
     dev::SmemCfg smc{};
     std::size_t smem = 0;
+    std::uint32_t per_sm = 1;
     if (!opt.grid) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
-        const std::uint32_t per_sm = std::min<std::uint32_t>(4, (n_slots + sms - 1) / sms);
+        per_sm = std::min<std::uint32_t>(4, (n_slots + sms - 1) / sms);
         // keep most of the unified L1 for the (read-only) static store
         const std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
         smc = plan_smem(ar.A, budget);
-        smem = dev::smem_bytes(smc);
-        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        smem = smc.bytes;
+        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)),
+           "smem attribute");
+        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)),
            "smem attribute");
     }
@@ -265,12 +222,15 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     for (;;) {
         ck(cudaEventRecord(e0), "record");
         if (opt.grid) {
-            void* args[] = {&ar.S, &cfg, &ar.d_slots, &ar.K, &ar.sh, &ar.partial, &ar.pd, &ar.pi};
+            void* args[] = {&ar.S, &cfg, &ar.L, &ar.K, &ar.sh, &ar.partial, &ar.pd, &ar.pi, &smc};
             ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::grid_kernel<kGridBS>), dim3(gblocks),
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            dev::block_kernel<kBlockBS><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.d_slots, ar.K, ar.sh, smc);
+            if (per_sm > 1)
+                dev::block_kernel<kBlockBS, 4><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            else
+                dev::block_kernel<kBlockBS, 1><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             ck(cudaGetLastError(), "block launch");
         }
         ck(cudaEventRecord(e1), "record");
@@ -279,7 +239,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         cudaEventElapsedTime(&ms, e0, e1);
         res.device_ms += ms;
         ++res.launches;
-        ck(cudaMemcpy(ctl.data(), ar.slots[0].ctl, n_slots * sizeof(dev::Ctl), cudaMemcpyDeviceToHost), "ctl");
+        ck(cudaMemcpy(ctl.data(), ar.slots[0].ctl(), n_slots * sizeof(dev::Ctl), cudaMemcpyDeviceToHost), "ctl");
         bool more = false;
         std::uint32_t err = dev::kDone;
         for (std::uint32_t s = 0; s < n_slots; ++s) {
@@ -287,8 +247,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             if (c.n_mbuf) {
                 mb.resize(static_cast<std::size_t>(c.n_mbuf) * ar.K.mwords);
                 mc.resize(c.n_mbuf);
-                ck(cudaMemcpy(mb.data(), ar.slots[s].mbuf, mb.size() * 4, cudaMemcpyDeviceToHost), "models");
-                ck(cudaMemcpy(mc.data(), ar.slots[s].mcube, mc.size() * 4, cudaMemcpyDeviceToHost), "models");
+                ck(cudaMemcpy(mb.data(), ar.slots[s].mbuf(), mb.size() * 4, cudaMemcpyDeviceToHost), "models");
+                ck(cudaMemcpy(mc.data(), ar.slots[s].mcube(), mc.size() * 4, cudaMemcpyDeviceToHost), "models");
                 for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
                     EngineModel em;
                     em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(m) * ar.K.mwords,
@@ -300,7 +260,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             }
             if (c.n_trace) {
                 std::vector<uint4> tb(c.n_trace);
-                ck(cudaMemcpy(tb.data(), ar.slots[s].tbuf, tb.size() * sizeof(uint4), cudaMemcpyDeviceToHost), "trace");
+                ck(cudaMemcpy(tb.data(), ar.slots[s].tbuf(), tb.size() * sizeof(uint4), cudaMemcpyDeviceToHost), "trace");
                 if (cb.on_trace)
                     for (const uint4& t : tb) cb.on_trace(t.x, static_cast<std::int32_t>(t.y), t.z, t.w);
                 c.n_trace = 0;
@@ -313,7 +273,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             break;
         }
         if (!more || stop_early) break;
-        ck(cudaMemcpy(ar.slots[0].ctl, ctl.data(), n_slots * sizeof(dev::Ctl), cudaMemcpyHostToDevice), "ctl");
+        ck(cudaMemcpy(ar.slots[0].ctl(), ctl.data(), n_slots * sizeof(dev::Ctl), cudaMemcpyHostToDevice), "ctl");
         ck(cudaMemset(&ar.sh->stop, 0, sizeof(std::uint32_t)), "stop");
     }
     dev::Stats tot{};
@@ -366,7 +326,7 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     impl_->ar.alloc_slots(1, deps_words, lcap, lpool, 16, 128, 0, impl_->gblocks);
     if (!grid) {
         impl_->smc = plan_smem(impl_->ar.A, 96u * 1024u);
-        impl_->smem = dev::smem_bytes(impl_->smc);
+        impl_->smem = impl_->smc.bytes;
         ck(cudaFuncSetAttribute(dev::op_block_kernel<kBlockBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(impl_->smem)),
            "smem attribute");
@@ -394,12 +354,13 @@ void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
     cudaEventRecord(im.e0);
     if (im.grid) {
         dev::OpArgs o = op;
-        void* args[] = {&im.ar.S, &im.cfg, &im.ar.d_slots, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &o};
+        void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &o,
+                        &im.smc};
         ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::op_grid_kernel<kGridBS>), dim3(im.gblocks),
                                        dim3(kGridBS), args, 0, nullptr),
            "op grid launch");
     } else {
-        dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem>>>(im.ar.S, im.cfg, im.ar.d_slots, im.ar.K, im.ar.sh, op,
+        dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem>>>(im.ar.S, im.cfg, im.ar.L, im.ar.K, im.ar.sh, op,
                                                                 im.smc);
         ck(cudaGetLastError(), "op launch");
     }
@@ -488,7 +449,7 @@ std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
 
 dev::Ctl Session::ctl() const {
     dev::Ctl c{};
-    ck(cudaMemcpy(&c, impl_->ar.slots[0].ctl, sizeof(c), cudaMemcpyDeviceToHost), "ctl");
+    ck(cudaMemcpy(&c, impl_->ar.slots[0].ctl(), sizeof(c), cudaMemcpyDeviceToHost), "ctl");
     return c;
 }
 
@@ -501,17 +462,17 @@ std::vector<T> dl(const T* p, std::size_t n) {
 }
 }  // namespace
 
-std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells, impl_->ar.A + 1); }
-std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail, ctl().ts); }
-std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason, impl_->ar.A + 1); }
+std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1); }
+std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts); }
+std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1); }
 std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
-    return dl(impl_->ar.slots[0].deps + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1);
+    return dl(impl_->ar.slots[0].deps() + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1);
 }
-std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf, impl_->ar.A + 1); }
-std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl, ctl().n_confl); }
+std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1); }
+std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl); }
 std::vector<std::int32_t> Session::frontier() const {
     const dev::Ctl c = ctl();
-    return dl(impl_->ar.slots[0].fr[c.cur], c.F);
+    return dl(impl_->ar.slots[0].fr(c.cur), c.F);
 }
 
 }  // namespace yas

@@ -187,6 +187,11 @@ def main():
         flush.zero_()
         torch.cuda.synchronize()
         o = prop.propagate_and_check(2)
+    # exact literal count of the checked nogoods (roofline bytes), untimed
+    prop.count_literals(True)
+    prepare()
+    lits_per_step = prop.propagate_and_check(2).checked_lits
+    prop.count_literals(False)
     barrier(world)
     torch.cuda.synchronize()
     dev_ms, checks, lits, launches = [], 0, 0, 0
@@ -200,7 +205,7 @@ def main():
             launches += 1
             dev_ms.append(o.device_ms)
             checks += o.checks
-            lits += o.checked_lits
+            lits += lits_per_step
             assert not o.violated
     torch.cuda.synchronize()
     barrier(world)

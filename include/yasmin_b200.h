@@ -194,6 +194,9 @@ int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint
                           const uint64_t* deps, uint32_t n_deps, int overflow, int32_t antecedent);
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n); /* Frontier::seed / last.push_back */
 int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n); /* NogoodStore::add_learned */
+/* Exact literal counts of checked nogoods in yas_outcome.checked_lits (roofline
+ * accounting; costs an extra load per decided long nogood, off by default). */
+int yas_propagator_count_literals(yas_propagator* p, int on);
 /* Read back. cells: A+1 entries (cell[p] = +-level). reasons: >= 0 antecedent,
  * -1 none, -2 decision, -3 unit, -4 completion. deps: word w of every atom. */
 uint32_t yas_propagator_atoms(const yas_propagator* p);

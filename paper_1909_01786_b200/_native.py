@@ -27,7 +27,7 @@ EXPORTS = [
     "yas_free_ints",
     "yas_propagator_create", "yas_propagator_free", "yas_propagator_reset", "yas_propagator_initial",
     "yas_propagator_propagate", "yas_propagator_push_decision", "yas_propagator_assign", "yas_propagator_seed",
-    "yas_propagator_add_learned", "yas_propagator_atoms", "yas_propagator_cells", "yas_propagator_reasons",
+    "yas_propagator_add_learned", "yas_propagator_count_literals", "yas_propagator_atoms", "yas_propagator_cells", "yas_propagator_reasons",
     "yas_propagator_deps", "yas_propagator_trail", "yas_propagator_conflicts", "yas_propagator_frontier",
     "yas_propagator_level",
 ]
@@ -138,6 +138,7 @@ def lib() -> C.CDLL:
         "yas_propagator_assign": (C.c_int, [P, pI32, SZ, U32, pU64, U32, C.c_int, I32]),
         "yas_propagator_seed": (C.c_int, [P, pI32, SZ]),
         "yas_propagator_add_learned": (I32, [P, pI32, SZ]),
+        "yas_propagator_count_literals": (C.c_int, [P, C.c_int]),
         "yas_propagator_atoms": (U32, [P]),
         "yas_propagator_cells": (C.c_int, [P, pI32]),
         "yas_propagator_reasons": (C.c_int, [P, pI32]),

@@ -577,6 +577,10 @@ class Propagator:
     def add_learned(self, lits: Sequence[int]) -> int:
         return N.lib().yas_propagator_add_learned(self._h, _ints(lits), len(lits))
 
+    def count_literals(self, on: bool = True):
+        """Exact checked-literal accounting (roofline bytes); off by default."""
+        N.lib().yas_propagator_count_literals(self._h, 1 if on else 0)
+
     def level(self) -> int:
         return N.lib().yas_propagator_level(self._h)
 

@@ -698,6 +698,11 @@ int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_
     guarded(nullptr, 0, [&] { id = p->s->add_learned(std::vector<std::int32_t>(lits, lits + n)); return 0; });
     return id;
 }
+int yas_propagator_count_literals(yas_propagator* p, int on) {
+    if (!p) return YAS_ERR_ARG;
+    p->s->set_count_lits(on != 0);
+    return YAS_OK;
+}
 uint32_t yas_propagator_atoms(const yas_propagator* p) { return p ? p->atoms : 0; }
 uint32_t yas_propagator_level(const yas_propagator* p) { return p ? p->s->ctl().cdl : 0; }
 int yas_propagator_cells(const yas_propagator* p, int32_t* out) {

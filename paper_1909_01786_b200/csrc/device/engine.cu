@@ -424,15 +424,19 @@ struct Search {
     __device__ std::uint32_t occ_total(std::uint32_t li) const {
         return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot()[li];
     }
-    // j-th entry of the literal's occurrence list [static c0, learned c0, ..., static c3, learned c3]
-    // All segment bounds are loaded at once (one memory round trip), then one
-    // dependent load fetches the id.
-    __device__ std::int32_t occ_entry(std::uint32_t li, std::uint32_t j, bool learned) const {
+    // j-th entry of the literal's occurrence list [static c0, learned c0, ...,
+    // static c3, learned c3]: {id, guard, x, y} and its length class. All
+    // segment bounds are loaded at once (one memory round trip), then one
+    // dependent 16-byte load fetches the entry.
+    __device__ int4 occ_entry(std::uint32_t li, std::uint32_t j, bool learned, std::uint32_t& cls) const {
         const std::uint32_t* oo = S.occ_off + li * 4;
         std::uint32_t b[5];
 #pragma unroll
         for (int k = 0; k < 5; ++k) b[k] = __ldg(oo + k);
-        if (!learned) return __ldg(S.occ_ids + b[0] + j);  // classes are contiguous
+        if (!learned) {  // static classes are contiguous
+            cls = (j >= b[1] - b[0]) + (j >= b[2] - b[0]) + (j >= b[3] - b[0]);
+            return __ldg(S.occ + b[0] + j);
+        }
         const std::uint32_t* h = sl.lhdr() + 12 * li;
         std::uint32_t hp[4], hn[4];
 #pragma unroll
@@ -443,12 +447,13 @@ struct Search {
 #pragma unroll
         for (int cl = 0; cl < 4; ++cl) {
             const std::uint32_t ns = b[cl + 1] - b[cl];
-            if (j < ns) return __ldg(S.occ_ids + b[cl] + j);
+            cls = static_cast<std::uint32_t>(cl);
+            if (j < ns) return __ldg(S.occ + b[cl] + j);
             j -= ns;
             if (j < hn[cl]) return sl.larena()[hp[cl] + j];
             j -= hn[cl];
         }
-        return -1;
+        return make_int4(-1, 0, 0, 0);
     }
     __device__ std::uint32_t nwords(std::uint32_t level) const {
         const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
@@ -694,6 +699,55 @@ struct Search {
         }
     }
 
+    // Evaluate the nogood of occurrence entry `ent` (class `cls`) that was
+    // triggered by frontier literal `trig` (which holds). Binary and ternary
+    // nogoods are decided by the two literals carried in the entry; a long one
+    // only when one of them is dead or both are free, else by a full scan.
+    __device__ void evaluate_entry(const int4& ent, std::uint32_t cls, std::int32_t trig, bool& conflict, bool& prop,
+                                   std::int32_t& plit, std::uint32_t& len, unsigned long long* d0 = nullptr,
+                                   std::uint32_t* meta = nullptr) const {
+        if (cls == 0) {  // length-1 entry: its literal is the trigger, which holds
+            conflict = true;
+            len = 1;
+            return;
+        }
+        const int vx = val(atom_of(ent.z));
+        const int sx = vx == 0 ? 0 : ((vx > 0) == (ent.z > 0) ? 1 : -1);  // 1 holds, -1 dead, 0 free
+        int sy = 1;
+        if (cls >= 2) {
+            const int vy = val(atom_of(ent.w));
+            sy = vy == 0 ? 0 : ((vy > 0) == (ent.w > 0) ? 1 : -1);
+        }
+        if (cls == 3 && !(sx < 0 || sy < 0 || (sx == 0 && sy == 0))) {
+            evaluate(ent.x, conflict, prop, plit, len, d0, meta);
+            return;
+        }
+        len = cls + 1;
+        if (C.count_lits && cls == 3) len = length_of(static_cast<std::uint32_t>(ent.x));
+        if (sx < 0 || sy < 0 || (sx == 0 && sy == 0)) return;  // satisfied, or two free
+        if (sx > 0 && sy > 0) {
+            conflict = true;
+            return;
+        }
+        const std::int32_t u1 = sx == 0 ? ent.z : ent.w;
+        if (!may_assert(static_cast<std::uint32_t>(ent.y), -u1)) return;
+        prop = true;
+        plit = -u1;
+        if (d0) {  // Deps of the other (holding) literals: the trigger and, for ternaries, the other blocker
+            const std::uint32_t ta = atom_of(trig);
+            const std::uint32_t oa = cls == 2 ? atom_of(sx == 0 ? ent.w : ent.z) : ta;
+            const std::int32_t ct = sl.cells()[ta], co = sl.cells()[oa];
+            const unsigned long long dt = dep(0, ta), dq = dep(0, oa);
+            const std::uint8_t ot = sl.dovf()[ta], oo = sl.dovf()[oa];
+            unsigned long long acc = 0;
+            std::uint32_t ovf = 0;
+            if (lvl_of(ct) > 1) { acc |= dt; ovf |= ot; }
+            if (lvl_of(co) > 1) { acc |= dq; ovf |= oo; }
+            *d0 = acc;
+            *meta = occ_total(lidx(plit)) | (ovf << 31);
+        }
+    }
+
     // One pass with the working set in shared memory (T <= tcap).
     __device__ void pass_smem(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
         const bool learned = c->learned_n > 0;
@@ -707,13 +761,19 @@ struct Search {
             std::int32_t id = -1, plit = 0;
             std::uint32_t slot = 0, meta = 0, clen = 0;
             unsigned long long d0 = 0;
+            unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
             if (e < T) {
+                if (g.leader()) tq0 = clock64();
                 std::uint32_t lo = 0, hi = F;
                 while (hi - lo > 1) {
                     const std::uint32_t mid = (lo + hi) >> 1;
                     if (sm.froff()[mid] <= e) lo = mid; else hi = mid;
                 }
-                id = occ_entry(lidx(sm.fr()[lo]), e - sm.froff()[lo], learned);
+                const std::int32_t trig = sm.fr()[lo];
+                std::uint32_t cls;
+                const int4 ent = occ_entry(lidx(trig), e - sm.froff()[lo], learned, cls);
+                id = ent.x;
+                if (g.leader()) { asm volatile("" ::"r"(id)); tq1 = clock64(); }
                 const unsigned long long key = (static_cast<unsigned long long>(id + 1) << 32) | e;
                 for (std::uint32_t h = hslot(static_cast<std::uint32_t>(id), hm);; h = (h + 1) & hm) {
                     unsigned long long cur_k = sm.htab()[h];
@@ -726,7 +786,17 @@ struct Search {
                         break;
                     }
                 }
-                if (first) evaluate(id, conflict, prop, plit, clen, &d0, &meta);
+                if (g.leader()) tq2 = clock64();
+                if (first) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
+                if (g.leader()) {
+                    asm volatile("" ::"r"(plit), "r"(clen));
+                    const unsigned long long tq3 = clock64();
+                    c->prof[8] += tq1 - tq0;
+                    c->prof[9] += tq2 - tq1;
+                    c->prof[10] += tq3 - tq2;
+                    c->prof[12] += T;
+                    c->prof[13] += 1;
+                }
             }
             __syncwarp();
             warp_count(&c->st.checks, first);
@@ -788,10 +858,13 @@ struct Search {
                     const std::uint32_t mid = (lo + hi) >> 1;
                     if (sl.froff()[mid] <= e) lo = mid; else hi = mid;
                 }
-                id = occ_entry(lidx(fr[lo]), e - sl.froff()[lo], learned);
+                const std::int32_t trig = fr[lo];
+                std::uint32_t cls;
+                const int4 ent = occ_entry(lidx(trig), e - sl.froff()[lo], learned, cls);
+                id = ent.x;
                 const unsigned long long old = atomicMin(sl.claim() + id, ckey(gen, e));
                 first = static_cast<std::uint32_t>(old >> 32) != ~gen;
-                if (first) evaluate(id, conflict, prop, plit, clen);
+                if (first) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen);
             }
             __syncwarp();
             warp_count(&c->st.checks, first);
@@ -1003,12 +1076,16 @@ struct Search {
                     return -1;
                 }
                 const std::uint32_t np = c->locc_used;
-                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena()[np + q] = sl.larena()[h3[0] + q];
+                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena()[np + q] = sl.larena()[h3[0] + q];  // 16-byte entries
                 h3[0] = np;
                 h3[2] = ncap;
                 c->locc_used = np + ncap;
             }
-            sl.larena()[h3[0] + h3[1]] = static_cast<std::int32_t>(id);
+            std::int32_t other[2] = {0, 0};
+            for (std::uint32_t q = 0, n = 0; q < len && n < 2; ++q)
+                if (q != j) other[n++] = lits[q];
+            sl.larena()[h3[0] + h3[1]] = make_int4(static_cast<std::int32_t>(id), static_cast<std::int32_t>(kNone),
+                                                   other[0], other[1]);
             h3[1] += 1;
             sl.ltot()[li] += 1;
         }
@@ -1269,10 +1346,10 @@ struct Search {
             for (std::uint32_t cl = 0; cl < 4; ++cl) {
                 const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
                 for (std::uint32_t j = lo; j < hi; ++j)
-                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ_ids + j)))));
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ + j).x))));
                 const std::uint32_t* h = sl.lhdr() + 3 * (li * 4 + cl);
                 for (std::uint32_t j = 0; j < h[1]; ++j)
-                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena()[h[0] + j]))));
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena()[h[0] + j].x))));
             }
         return s;
     }

@@ -49,6 +49,7 @@ struct Config {
     std::uint32_t n_cubes;
     std::uint32_t cube_width;   // literals per cube
     std::uint64_t slice_ns;     // time slice per launch before yielding
+    std::uint32_t count_lits;   // accumulate literals of checked nogoods (roofline accounting)
 };
 
 // Read-only static store + program rules (host-built, uploaded once).
@@ -61,7 +62,7 @@ struct Static {
     const std::int32_t* pool;   // literal codes
     const std::uint32_t* guard; // N
     const std::uint32_t* occ_off;  // (2A+2)*4+1, key = lit_index*4 + class
-    const std::int32_t* occ_ids;
+    const int4* occ;               // {id, guard, x, y} per occurrence (see StaticStore::occ_fat)
     const std::int32_t* units;     // static unit literals (nogood literal sigma)
     const std::int32_t* uids;      // static length-1 CSR ids
     const uint4* rules;            // (head, b, t, n | vacuous<<31)
@@ -86,7 +87,7 @@ struct Ctl {
     double act_inc;
     std::uint32_t b[16];  // leader -> group broadcast scratch
     Stats st;
-    unsigned long long prof[10];  // clock64 cycles per phase (leader view, after barriers)
+    unsigned long long prof[16];  // clock64 cycles per phase (leader view, after barriers)
     unsigned long long prof_t;
 };
 
@@ -144,7 +145,7 @@ struct Slot {
     YAS_HD std::uint32_t* loff() const { return at<std::uint32_t>(L->o_loff); }
     YAS_HD std::int32_t* lpool() const { return at<std::int32_t>(L->o_lpool); }
     YAS_HD std::uint32_t* lhdr() const { return at<std::uint32_t>(L->o_lhdr); }  // (2A+2)*4 * {ptr,size,cap}
-    YAS_HD std::int32_t* larena() const { return at<std::int32_t>(L->o_larena); }
+    YAS_HD int4* larena() const { return at<int4>(L->o_larena); }  // learned occurrence entries
     YAS_HD std::int32_t* lunits() const { return at<std::int32_t>(L->o_lunits); }
     YAS_HD std::uint32_t* ltot() const { return at<std::uint32_t>(L->o_ltot); }
     YAS_HD double* act() const { return at<double>(L->o_act); }

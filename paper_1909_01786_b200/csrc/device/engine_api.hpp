@@ -75,6 +75,7 @@ public:
                 const std::vector<unsigned long long>& deps, bool ovf);
     void seed(const std::vector<std::int32_t>& lits);
     std::int32_t add_learned(const std::vector<std::int32_t>& lits);
+    void set_count_lits(bool on);
 
     // read back
     dev::Ctl ctl() const;

@@ -65,7 +65,12 @@ struct Arena {
         S.pool = dupload(st.pool, owned);
         S.guard = dupload(st.guard, owned);
         S.occ_off = dupload(st.occ_off, owned);
-        S.occ_ids = dupload(st.occ_ids, owned);
+        {
+            int4* occ = dalloc<int4>(st.occ_fat.size() / 4, owned);
+            if (!st.occ_fat.empty())
+                ck(cudaMemcpy(occ, st.occ_fat.data(), st.occ_fat.size() * 4, cudaMemcpyHostToDevice), "upload");
+            S.occ = occ;
+        }
         S.units = dupload(st.units, owned);
         S.uids = dupload(st.unit_ids, owned);
         std::vector<uint4> r(rules.size());
@@ -121,7 +126,7 @@ struct Arena {
         L.o_loff = take(4ull * (K.lcap + 1));
         L.o_lpool = take(4ull * K.lpool);
         L.o_lhdr = take(4 * keys * 3);
-        L.o_larena = take(4ull * K.larena);
+        L.o_larena = take(16ull * K.larena);
         L.o_lunits = take(4ull * K.lcap);
         L.o_ltot = take(4 * 2 * A1);
         L.o_act = take(8 * A1);
@@ -239,7 +244,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         cudaEventElapsedTime(&ms, e0, e1);
         res.device_ms += ms;
         ++res.launches;
-        ck(cudaMemcpy(ctl.data(), ar.slots[0].ctl(), n_slots * sizeof(dev::Ctl), cudaMemcpyDeviceToHost), "ctl");
+        ck(cudaMemcpy2D(ctl.data(), sizeof(dev::Ctl), ar.slots[0].ctl(), ar.L.bytes, sizeof(dev::Ctl), n_slots,
+                        cudaMemcpyDeviceToHost),
+           "ctl");
         bool more = false;
         std::uint32_t err = dev::kDone;
         for (std::uint32_t s = 0; s < n_slots; ++s) {
@@ -273,7 +280,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             break;
         }
         if (!more || stop_early) break;
-        ck(cudaMemcpy(ar.slots[0].ctl(), ctl.data(), n_slots * sizeof(dev::Ctl), cudaMemcpyHostToDevice), "ctl");
+        ck(cudaMemcpy2D(ar.slots[0].ctl(), ar.L.bytes, ctl.data(), sizeof(dev::Ctl), sizeof(dev::Ctl), n_slots,
+                        cudaMemcpyHostToDevice),
+           "ctl");
         ck(cudaMemset(&ar.sh->stop, 0, sizeof(std::uint32_t)), "stop");
     }
     dev::Stats tot{};
@@ -285,13 +294,13 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     for (const dev::Ctl& c : ctl) add(tot, c.st);
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
-        static const char* names[10] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
-                                        "conflict", "-", "-"};
-        unsigned long long p[10] = {0};
+        static const char* names[14] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
+                                        "conflict", "x.occ", "x.hash", "x.eval", "-", "sumT", "iters"};
+        unsigned long long p[16] = {0};
         for (const dev::Ctl& c : ctl)
-            for (int k = 0; k < 10; ++k) p[k] += c.prof[k];
+            for (int k = 0; k < 16; ++k) p[k] += c.prof[k];
         std::fprintf(stderr, "[yas profile] passes=%llu", static_cast<unsigned long long>(tot.passes));
-        for (int k = 0; k < 8; ++k) std::fprintf(stderr, " %s=%.1fMcyc", names[k], p[k] / 1e6);
+        for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %s=%.2fM", names[k], p[k] / 1e6);
         std::fprintf(stderr, "\n");
     }
     cudaEventDestroy(e0);
@@ -446,6 +455,8 @@ std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
     for (void* p : tmp) cudaFree(p);
     return static_cast<std::int32_t>(ctl().b[12]);
 }
+
+void Session::set_count_lits(bool on) { impl_->cfg.count_lits = on ? 1u : 0u; }
 
 dev::Ctl Session::ctl() const {
     dev::Ctl c{};

@@ -192,11 +192,21 @@ StaticStore build_store(const std::vector<Nogood>& nogoods, AtomId total_atoms) 
     for (std::size_t k = 0; k < keys; ++k) count[k + 1] += count[k];
     st.occ_off = count;
     st.occ_ids.resize(st.pool.size());
+    st.occ_fat.resize(4 * st.pool.size());
     std::vector<std::uint32_t> fill(count.begin(), count.end() - 1);
     for (std::uint32_t id = 0; id < st.size(); ++id) {
         const std::uint32_t cls = length_class(st.length(id));
-        for (std::uint32_t k = st.off[id]; k < st.off[id + 1]; ++k)
-            st.occ_ids[fill[lit_index(st.pool[k]) * 4 + cls]++] = static_cast<std::int32_t>(id);
+        for (std::uint32_t k = st.off[id]; k < st.off[id + 1]; ++k) {
+            const std::uint32_t at = fill[lit_index(st.pool[k]) * 4 + cls]++;
+            st.occ_ids[at] = static_cast<std::int32_t>(id);
+            std::int32_t other[2] = {0, 0};
+            for (std::uint32_t q = st.off[id], n = 0; q < st.off[id + 1] && n < 2; ++q)
+                if (q != k) other[n++] = st.pool[q];
+            st.occ_fat[4 * at + 0] = static_cast<std::int32_t>(id);
+            st.occ_fat[4 * at + 1] = static_cast<std::int32_t>(st.guard[id]);
+            st.occ_fat[4 * at + 2] = other[0];
+            st.occ_fat[4 * at + 3] = other[1];
+        }
     }
     auto first_of_len = [&](std::uint32_t len) {
         std::uint32_t i = 0;

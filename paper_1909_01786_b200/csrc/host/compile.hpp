@@ -77,6 +77,10 @@ struct StaticStore {
     std::vector<std::int32_t> unit_ids;  // CSR ids of length-1 entries
     std::vector<std::uint32_t> occ_off;  // (2A+2)*4 + 1
     std::vector<std::int32_t> occ_ids;
+    // Device copy of the occurrence lists: per (literal, nogood) one 16-byte
+    // entry {id, guard, x, y} with x, y two *other* literals of the nogood
+    // (0 when absent), so binary/ternary nogoods are decided from the entry.
+    std::vector<std::int32_t> occ_fat;  // 4 ints per occurrence, same order as occ_ids
     std::array<std::uint32_t, 4> bounds{0, 0, 0, 0};
 
     std::uint32_t size() const { return static_cast<std::uint32_t>(off.size() - 1); }

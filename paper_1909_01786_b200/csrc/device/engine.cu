@@ -92,8 +92,34 @@ __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long 
 // ---------------------------------------------------------------------------
 // Groups
 // ---------------------------------------------------------------------------
+// Warp 0 of a CTA on its own: small passes run warp-synchronously.
+struct WarpG {
+    static constexpr bool kBlock = false;
+    Ctl* c;
+    __device__ std::uint32_t tid() const { return lane_id(); }
+    __device__ std::uint32_t size() const { return 32; }
+    __device__ bool leader() const { return threadIdx.x == 0; }
+    __device__ void sync() { __syncwarp(); }
+    __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
+        const unsigned long long inc = warp_incl_scan(v);
+        total = __shfl_sync(0xffffffffu, inc, 31);
+        return inc - v;
+    }
+    __device__ void argmax(double& s, std::uint32_t& i) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            double os = __shfl_down_sync(0xffffffffu, s, d);
+            std::uint32_t oi = __shfl_down_sync(0xffffffffu, i, d);
+            if (better(os, oi, s, i)) { s = os; i = oi; }
+        }
+        s = __shfl_sync(0xffffffffu, s, 0);
+        i = __shfl_sync(0xffffffffu, i, 0);
+    }
+};
+
 template <int BS>
 struct BlockG {
+    static constexpr bool kBlock = true;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     unsigned long long* sbuf;  // kWarps+2 words of shared scratch
@@ -154,6 +180,7 @@ struct BlockG {
 
 template <int BS>
 struct GridG {
+    static constexpr bool kBlock = false;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     Shared* sh;
@@ -486,7 +513,20 @@ struct Search {
                                     std::uint32_t level) const {
         const std::uint32_t nw = nwords(level);
         std::uint8_t ovf = 0;
-        for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = deps_word(L, len, id, a, w, ovf);
+        for (std::uint32_t w0 = 0; w0 < nw; w0 += 4) {  // 4 words per sweep: independent loads
+            unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+            for (std::uint32_t k = 0; k < len; ++k) {
+                const std::uint32_t x = atom_of(lit_at(L, k, id));
+                if (x == a || lvl_of(sl.cells()[x]) <= 1) continue;
+#pragma unroll
+                for (std::uint32_t q = 0; q < 4; ++q)
+                    if (w0 + q < nw) acc[q] |= dep(w0 + q, x);
+                if (w0 == 0) ovf |= sl.dovf()[x];
+            }
+#pragma unroll
+            for (std::uint32_t q = 0; q < 4; ++q)
+                if (w0 + q < nw) dep(w0 + q, a) = acc[q];
+        }
         sl.dovf()[a] = ovf;
     }
     __device__ unsigned long long deps_word(const std::int32_t* L, std::uint32_t len, std::uint32_t id,
@@ -891,6 +931,8 @@ struct Search {
 
     // One propagation call to fixpoint or violation (propagate.cpp:170-205).
     // Returns true when conflicts were found (they are in confl[0..n_confl)).
+    static constexpr std::uint32_t kWarpPassT = 96;  // passes this small run in warp 0 alone
+
     __device__ bool propagate(std::uint32_t level) {
         mark(0);
         frontier_offsets();
@@ -898,8 +940,30 @@ struct Search {
             const std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, viol = c->b[11];
             if (viol) return true;
             if (F == 0) return false;
+            if constexpr (G::kBlock) {
+                if (T <= kWarpPassT && sm.tcap() && F + 1 <= sm.fcap()) {
+                    if (threadIdx.x < 32) {
+                        WarpG wg{c};
+                        Search<WarpG> ws(wg, S, C, sl, K, sh, t0, sm);
+                        ws.small_passes(level);
+                    }
+                    g.sync();
+                    continue;
+                }
+            }
             if (sm.tcap() && T <= sm.tcap() && F + 1 <= sm.fcap()) pass_smem(F, T, cur, level);
             else pass_global(F, T, gen, cur, level);
+        }
+    }
+
+    // Warp-synchronous passes while they stay small (called by warp 0 only).
+    __device__ void small_passes(std::uint32_t level) {
+        for (;;) {
+            __syncwarp();
+            const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
+            __syncwarp();
+            if (viol || F == 0 || T > kWarpPassT || F + 1 > sm.fcap()) return;
+            pass_smem(F, T, cur, level);
         }
     }
 

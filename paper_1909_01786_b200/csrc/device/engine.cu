@@ -956,8 +956,34 @@ struct Search {
         }
     }
 
+    __device__ static unsigned long long clk_after(std::uint32_t v) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "r"(v) : "memory");
+        return t;
+    }
+    __device__ static unsigned long long clk_now() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+        return t;
+    }
+
     // Warp-synchronous passes while they stay small (called by warp 0 only).
     __device__ void small_passes(std::uint32_t level) {
+        if (threadIdx.x == 0 && c->F > 0) {  // latency probe on real data (profiling only)
+            const std::uint32_t li = lidx(sm.fr()[0]);
+            const unsigned long long a0 = clk_now();
+            const std::uint32_t v0 = __ldg(S.occ_off + li * 4);
+            const unsigned long long a1 = clk_after(v0);
+            const int4 e0 = __ldg(S.occ + v0);
+            const unsigned long long a2 = clk_after(static_cast<std::uint32_t>(e0.x));
+            const std::int32_t cv = sl.cells()[atom_of(e0.z) + (e0.x & 0)];
+            const unsigned long long a3 = clk_after(static_cast<std::uint32_t>(cv));
+            const std::uint32_t v1 = __ldg(S.occ_off + li * 4 + (cv & 0));
+            const unsigned long long a4 = clk_after(v1);
+            c->prof[11] += a1 - a0;
+            c->prof[14] += a2 - a1;
+            c->prof[15] += (a3 - a2) + ((a4 - a3) << 32);
+        }
         for (;;) {
             __syncwarp();
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];

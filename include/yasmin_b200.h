@@ -207,6 +207,11 @@ size_t yas_propagator_trail(const yas_propagator* p, int32_t* out, size_t cap);
 size_t yas_propagator_conflicts(const yas_propagator* p, int32_t* out, size_t cap);
 size_t yas_propagator_frontier(const yas_propagator* p, int32_t* out, size_t cap);
 uint32_t yas_propagator_level(const yas_propagator* p);
+/* Diagnostics (no reference counterpart): SM clock cycles spent per phase of the
+ * propagation loop since the propagator was created, measured by the leader
+ * thread between barriers: [1] frontier offsets, [2] expand+evaluate,
+ * [3] resolve, [4] apply, [5] compact. */
+int yas_propagator_profile(const yas_propagator* p, uint64_t out[16]);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,8 @@ import enum
 from dataclasses import dataclass, field
 from typing import Callable, Iterable, List, Optional, Sequence
 
+import numpy as np
+
 from . import _native as N
 
 kAnyTruth = 0xFFFFFFFF
@@ -430,6 +432,10 @@ def emit_stats(stats: SolveStats, ctx: StatsContext, csv: bool) -> str:
 # low level: store + propagator
 # ---------------------------------------------------------------------------
 def _ints(xs: Sequence[int]):
+    """int32 buffer for the C-ABI: numpy int32 arrays are passed without a copy."""
+    if isinstance(xs, np.ndarray):
+        a = np.ascontiguousarray(xs, dtype=np.int32)
+        return a.ctypes.data_as(C.POINTER(C.c_int32)) if a.size else (C.c_int32 * 1)()
     return (C.c_int32 * max(1, len(xs)))(*xs)
 
 
@@ -546,7 +552,8 @@ class Propagator:
             self._h = C.c_void_p(0)
 
     def _outcome(self, o: N.yas_outcome) -> PropagationOutcome:
-        return PropagationOutcome(bool(o.violated), self.conflicts(), o.propagations, o.passes, o.checks, o.device_ms,
+        confl = self.conflicts() if o.n_conflicts else []
+        return PropagationOutcome(bool(o.violated), confl, o.propagations, o.passes, o.checks, o.device_ms,
                                   o.checked_lits)
 
     def reset(self):
@@ -584,6 +591,12 @@ class Propagator:
     def level(self) -> int:
         return N.lib().yas_propagator_level(self._h)
 
+    def profile(self) -> List[int]:
+        """Diagnostics: SM cycles per propagation phase (see yas_propagator_profile)."""
+        out = (C.c_uint64 * 16)()
+        N.lib().yas_propagator_profile(self._h, out)
+        return list(out)
+
     def cells(self) -> List[int]:
         out = (C.c_int32 * (self.atoms + 1))()
         N.lib().yas_propagator_cells(self._h, out)
@@ -600,14 +613,23 @@ class Propagator:
         N.lib().yas_propagator_deps(self._h, word, out, ovf)
         return list(out), list(ovf)
 
+    def _array(self, fn) -> np.ndarray:
+        out = np.empty(self.atoms + 1, dtype=np.int32)  # trail, frontier, conflicts: one pass, <= A entries
+        n = fn(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), out.size)
+        if n > out.size:  # (cannot happen for trail/frontier; conflicts may exceed A)
+            out = np.empty(n, dtype=np.int32)
+            n = fn(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), out.size)
+        return out[:n]
+
     def _list(self, fn) -> List[int]:
-        n = fn(self._h, None, 0)
-        out = (C.c_int32 * max(1, n))()
-        fn(self._h, out, n)
-        return list(out[:n])
+        return self._array(fn).tolist()
 
     def trail(self) -> List[int]:
         return self._list(N.lib().yas_propagator_trail)
+
+    def trail_array(self) -> np.ndarray:
+        """The trail as an int32 numpy array (one D2H copy, no Python list)."""
+        return self._array(N.lib().yas_propagator_trail)
 
     def conflicts(self) -> List[int]:
         return self._list(N.lib().yas_propagator_conflicts)

@@ -550,7 +550,7 @@ int yas_store_build(const int32_t* lits, const uint32_t* offsets, size_t n, cons
             std::vector<std::int32_t> l(lits + offsets[k], lits + offsets[k + 1]);
             for (std::int32_t x : l)
                 if (x == 0 || lit_atom(x) > total_atoms) throw std::invalid_argument("literal out of range");
-            auto ng = Nogood::make(std::move(l), origins ? origins[k] : kConstraint, guards ? guards[k] : kAnyTruth);
+            auto ng = Nogood::make(std::move(l), origins ? origins[k] : static_cast<std::uint8_t>(kConstraint), guards ? guards[k] : kAnyTruth);
             if (!ng || ng->lits.empty()) throw std::invalid_argument("vacuous or empty nogood " + std::to_string(k));
             ngs.push_back(std::move(*ng));
         }
@@ -650,7 +650,7 @@ void yas_propagator_free(yas_propagator* p) { delete p; }
 
 static void outcome_from(yas_propagator* p, bool violated, const dev::Ctl& before, yas_outcome* o) {
     if (!o) return;
-    const dev::Ctl c = p->s->ctl();
+    const dev::Ctl& c = p->s->ctl();
     o->violated = violated ? 1 : 0;
     o->propagations = c.st.propagations - before.st.propagations;
     o->passes = c.st.passes - before.st.passes;
@@ -685,13 +685,13 @@ int yas_propagator_push_decision(yas_propagator* p, int32_t lit) {
 int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level, const uint64_t* deps,
                           uint32_t n_deps, int overflow, int32_t antecedent) {
     return guarded(nullptr, 0, [&] {
-        std::vector<unsigned long long> d(deps, deps + n_deps);
-        p->s->assign(std::vector<std::int32_t>(lits, lits + n), level, antecedent, d, overflow != 0);
+        p->s->assign(lits, n, level, antecedent, reinterpret_cast<const unsigned long long*>(deps), deps ? n_deps : 0,
+                     overflow != 0);
         return static_cast<int>(YAS_OK);
     });
 }
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n) {
-    return guarded(nullptr, 0, [&] { p->s->seed(std::vector<std::int32_t>(lits, lits + n)); return static_cast<int>(YAS_OK); });
+    return guarded(nullptr, 0, [&] { p->s->seed(lits, n); return static_cast<int>(YAS_OK); });
 }
 int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n) {
     int32_t id = -1;
@@ -704,6 +704,14 @@ int yas_propagator_count_literals(yas_propagator* p, int on) {
     return YAS_OK;
 }
 uint32_t yas_propagator_atoms(const yas_propagator* p) { return p ? p->atoms : 0; }
+int yas_propagator_profile(const yas_propagator* p, uint64_t out[16]) {
+    if (!p || !out) return YAS_ERR_ARG;
+    return guarded(nullptr, 0, [&] {
+        const dev::Ctl& c = p->s->ctl();
+        for (int k = 0; k < 16; ++k) out[k] = c.prof[k];
+        return static_cast<int>(YAS_OK);
+    });
+}
 uint32_t yas_propagator_level(const yas_propagator* p) { return p ? p->s->ctl().cdl : 0; }
 int yas_propagator_cells(const yas_propagator* p, int32_t* out) {
     const auto v = p->s->cells();
@@ -726,9 +734,7 @@ int yas_propagator_deps(const yas_propagator* p, uint32_t word, uint64_t* out, u
     return YAS_OK;
 }
 size_t yas_propagator_trail(const yas_propagator* p, int32_t* out, size_t cap) {
-    const auto v = p->s->trail();
-    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-    return v.size();
+    return p->s->trail_into(out, cap);
 }
 size_t yas_propagator_conflicts(const yas_propagator* p, int32_t* out, size_t cap) {
     const auto v = p->s->conflicts();

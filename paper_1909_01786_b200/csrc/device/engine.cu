@@ -95,6 +95,7 @@ __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long 
 // Warp 0 of a CTA on its own: small passes run warp-synchronously.
 struct WarpG {
     static constexpr bool kBlock = false;
+    static constexpr bool kGrid = false;
     Ctl* c;
     __device__ std::uint32_t tid() const { return lane_id(); }
     __device__ std::uint32_t size() const { return 32; }
@@ -120,6 +121,7 @@ struct WarpG {
 template <int BS>
 struct BlockG {
     static constexpr bool kBlock = true;
+    static constexpr bool kGrid = false;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     unsigned long long* sbuf;  // kWarps+2 words of shared scratch
@@ -181,38 +183,73 @@ struct BlockG {
 template <int BS>
 struct GridG {
     static constexpr bool kBlock = false;
+    static constexpr bool kGrid = true;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     Shared* sh;
-    unsigned long long* partial;  // 2 * gridDim.x
+    unsigned long long* partial;  // 2 parities x {block totals, block extras} x gridDim.x
     double* pd;                   // gridDim.x
     std::uint32_t* pi;            // gridDim.x
     unsigned long long* sbuf;
     double* sd;
     std::uint32_t* si;
     std::uint32_t parity;
+    unsigned long long* bc;  // shared: per-block pass counters {checks, conflicts, literals}
+    std::uint32_t epoch;     // barriers passed (same in every block)
+    std::uint32_t* wsm;      // shared: 64 words per warp (compaction)
 
     __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
     __device__ std::uint32_t size() const { return gridDim.x * BS; }
     __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
+    // Block-interleaved numbering: consecutive ids land on different SMs, so
+    // a small amount of work is spread over the whole GPU.
+    __device__ std::uint32_t itid() const { return threadIdx.x * gridDim.x + blockIdx.x; }
+    __device__ std::uint32_t iwarp() const { return (threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
 
+    // Exclusive scan of one value per thread over this block only.
+    __device__ unsigned long long block_scan(unsigned long long v, unsigned long long& total) {
+        const std::uint32_t w = threadIdx.x >> 5;
+        unsigned long long inc = warp_incl_scan(v);
+        if (lane_id() == 31) sbuf[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long x = lane_id() < kWarps ? sbuf[lane_id()] : 0ull;
+            unsigned long long xi = warp_incl_scan(x);
+            if (lane_id() < kWarps) sbuf[lane_id()] = xi - x;
+            if (lane_id() == 31) sbuf[kWarps] = xi;
+        }
+        __syncthreads();
+        const unsigned long long r = sbuf[w] + inc - v;
+        total = sbuf[kWarps];
+        __syncthreads();
+        return r;
+    }
+
+    // Grid barrier: one release-add on a monotone arrival counter per block,
+    // then a relaxed spin until the counter reaches epoch * gridDim (wrap-safe
+    // difference) and an acquire fence. The counter is never reset; every block
+    // passes the same barriers, so each keeps its epoch in sh->arrive[block]
+    // across launches (see persist()). 1.2 us per barrier on B200 with 148
+    // CTAs (scripts/barrier_probe.cu), against 2.1 us for a counter+generation
+    // barrier with two fences and 5.5 us for flag all-gathers.
     __device__ void sync() {
         __syncthreads();
+        ++epoch;
         if (threadIdx.x == 0) {
-            volatile std::uint32_t* vgen = &sh->bar_gen;
-            const std::uint32_t g0 = *vgen;
-            __threadfence();
-            const std::uint32_t arrived = atomicAdd(&sh->bar_count, 1u);
-            if (arrived == gridDim.x - 1) {
-                sh->bar_count = 0;
-                __threadfence();
-                atomicAdd(&sh->bar_gen, 1u);
-            } else {
-                while (*vgen == g0) { }
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&sh->bar_count), "r"(1u) : "memory");
+            const std::uint32_t target = epoch * gridDim.x;
+            for (;;) {
+                std::uint32_t v;
+                asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&sh->bar_count) : "memory");
+                if (static_cast<int>(v - target) >= 0) break;
             }
             __threadfence();
         }
         __syncthreads();
+    }
+    // Store this block's epoch for the next launch on the same arena.
+    __device__ void persist() const {
+        if (threadIdx.x == 0) sh->arrive[blockIdx.x] = epoch;
     }
 
     __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
@@ -227,7 +264,7 @@ struct GridG {
             if (lane_id() == 31) sbuf[kWarps] = xi;
         }
         __syncthreads();
-        unsigned long long* part = partial + parity * gridDim.x;
+        unsigned long long* part = partial + parity * 2 * gridDim.x;
         parity ^= 1u;
         if (threadIdx.x == 0) part[blockIdx.x] = sbuf[kWarps];
         sync();
@@ -248,6 +285,52 @@ struct GridG {
         __syncthreads();
         const unsigned long long r = sbuf[kWarps + 1] + sbuf[w] + inc - v;
         total = sbuf[kWarps + 2];
+        __syncthreads();
+        return r;
+    }
+
+    // scan() that also sums one block-level value (*ex, in shared memory,
+    // final when the call is made) over the grid: *ex_total on return.
+    __device__ unsigned long long scan_ex(unsigned long long v, unsigned long long& total, const unsigned long long* ex,
+                                          unsigned long long& ex_total) {
+        const std::uint32_t w = threadIdx.x >> 5;
+        unsigned long long inc = warp_incl_scan(v);
+        if (lane_id() == 31) sbuf[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            unsigned long long x = lane_id() < kWarps ? sbuf[lane_id()] : 0ull;
+            unsigned long long xi = warp_incl_scan(x);
+            if (lane_id() < kWarps) sbuf[lane_id()] = xi - x;
+            if (lane_id() == 31) sbuf[kWarps] = xi;
+        }
+        __syncthreads();
+        unsigned long long* part = partial + parity * 2 * gridDim.x;
+        parity ^= 1u;
+        if (threadIdx.x == 0) {
+            part[blockIdx.x] = sbuf[kWarps];
+            part[gridDim.x + blockIdx.x] = *ex;
+        }
+        sync();
+        if (w == 0) {
+            unsigned long long before = 0, all = 0, xall = 0;
+            for (std::uint32_t b = lane_id(); b < gridDim.x; b += 32) {
+                const unsigned long long x = part[b];
+                all += x;
+                xall += part[gridDim.x + b];
+                if (b < blockIdx.x) before += x;
+            }
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                before += __shfl_down_sync(0xffffffffu, before, d);
+                all += __shfl_down_sync(0xffffffffu, all, d);
+                xall += __shfl_down_sync(0xffffffffu, xall, d);
+            }
+            if (lane_id() == 0) { sbuf[kWarps + 1] = before; sbuf[kWarps + 2] = all; sbuf[kWarps + 3] = xall; }
+        }
+        __syncthreads();
+        const unsigned long long r = sbuf[kWarps + 1] + sbuf[w] + inc - v;
+        total = sbuf[kWarps + 2];
+        ex_total = sbuf[kWarps + 3];
         __syncthreads();
         return r;
     }
@@ -915,6 +998,7 @@ struct Search {
             if (prop) sl.props()[ps] = make_int4(id, plit, 0, 0);
         }
         g.sync();
+        mark(2);
         // resolve: final min-e of every proposing nogood, atomicMin per atom
         const std::uint32_t np = c->n_props;
         for (std::uint32_t i = g.tid(); i < np; i += g.size()) {
@@ -925,8 +1009,343 @@ struct Search {
             atomicMin(sl.win() + atom_of(p.y), wkey(gen, e, p.y < 0));
         }
         g.sync();
+        mark(3);
         apply<false>(level, false);
+        mark(4);
         compact<false>(T, cur ^ 1u, true, 0);
+        mark(5);
+    }
+
+    // ---- whole-grid passes (GridG) ---------------------------------------------
+    // A pass costs four grid barriers: expand+evaluate | resolve | select the
+    // winners + scan | place them. Every block keeps the loop state (F, T, gen,
+    // frontier buffer, trail size) in registers; the pass's conflict count is
+    // exchanged with the scan, so no block reads a counter another block may
+    // already be bumping for the next pass.
+
+    // Expansion entries e in [0, T) are split into one contiguous range per
+    // warp. A warp locates the frontier literal of its first entry with a
+    // 32-ary search, then walks: per batch of 32*U entries it loads the next 32
+    // frontier offsets once and every lane finds its trigger with five register
+    // shuffles. U independent entries per lane keep U gathers, U claim atomics
+    // and their cell lookups in flight at once.
+    template <int U>
+    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned) {
+        const std::int32_t* fr = sl.fr(cur);
+        const std::uint32_t* froff = sl.froff();
+        const std::uint32_t lane = lane_id();
+        const std::uint32_t nwarps = g.size() >> 5, wid = g.iwarp();
+        const std::uint32_t per = (((T + nwarps - 1) / nwarps) + 31u) & ~31u;
+        const unsigned long long start64 = static_cast<unsigned long long>(wid) * per;
+        std::uint32_t checks = 0, nconf = 0, lits = 0;
+        if (start64 < T) {
+            const std::uint32_t start = static_cast<std::uint32_t>(start64);
+            const std::uint32_t end = T - start < per ? T : start + per;
+            std::uint32_t lo = 0, hi = F;  // froff[lo] <= start < froff[hi] = T
+            while (hi - lo > 1) {
+                const std::uint32_t step = (hi - lo + 31u) >> 5;
+                const std::uint32_t idx = lo + lane * step;
+                const bool ok = idx < hi && froff[idx] <= start;
+                const unsigned b = __ballot_sync(0xffffffffu, ok);
+                lo += static_cast<std::uint32_t>(31 - __clz(b)) * step;
+                hi = min(hi, lo + step);
+            }
+            std::uint32_t p0 = lo, f0 = froff[lo];
+            for (std::uint32_t base = start; base < end; base += 32u * U) {
+                const std::uint32_t q = p0 + 1 + lane;
+                const std::uint32_t v = q <= F ? froff[q] : 0xffffffffu;
+                const bool narrow = __shfl_sync(0xffffffffu, v, 31) <= base + 32u * U - 1;
+                std::uint32_t pe[U], se[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t e = base + 32u * u + lane;
+                    if (!narrow) {
+                        std::uint32_t cnt = 0;
+#pragma unroll
+                        for (int st = 16; st >= 1; st >>= 1)
+                            if (__shfl_sync(0xffffffffu, v, cnt + st - 1) <= e) cnt += st;
+                        const std::uint32_t sv = __shfl_sync(0xffffffffu, v, cnt == 0 ? 0 : cnt - 1);
+                        pe[u] = p0 + cnt;
+                        se[u] = cnt == 0 ? f0 : sv;
+                    } else {  // many empty occurrence lists inside the batch: per-lane search
+                        std::uint32_t l2 = p0, h2 = F;
+                        if (e < T)
+                            while (h2 - l2 > 1) {
+                                const std::uint32_t m = (l2 + h2) >> 1;
+                                if (froff[m] <= e) l2 = m; else h2 = m;
+                            }
+                        pe[u] = l2;
+                        se[u] = froff[l2];
+                    }
+                }
+                std::int32_t trig[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) trig[u] = base + 32u * u + lane < end ? fr[pe[u]] : 0;
+                int4 ent[U];
+                std::uint32_t cls[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t e = base + 32u * u + lane;
+                    cls[u] = 0;
+                    ent[u] = e < end ? occ_entry(lidx(trig[u]), e - se[u], learned, cls[u]) : make_int4(-1, 0, 0, 0);
+                }
+                unsigned long long old[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t e = base + 32u * u + lane;
+                    old[u] = e < end ? atomicMin(sl.claim() + ent[u].x, ckey(gen, e)) : ckey(gen, 0);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const bool first = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                    bool conflict = false, prop = false;
+                    std::int32_t plit = 0;
+                    std::uint32_t clen = 0;
+                    if (first) evaluate_entry(ent[u], cls[u], trig[u], conflict, prop, plit, clen);
+                    checks += first ? 1u : 0u;
+                    lits += clen;
+                    nconf += conflict ? 1u : 0u;
+                    const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+                    if (conflict) sl.confl()[cs] = ent[u].x;
+                    const std::uint32_t ps = warp_append(&c->n_props, prop);
+                    if (prop) sl.props()[ps] = make_int4(ent[u].x, plit, 0, 0);
+                }
+                p0 = __shfl_sync(0xffffffffu, pe[U - 1], 31);
+                f0 = __shfl_sync(0xffffffffu, se[U - 1], 31);
+            }
+        }
+        checks = __reduce_add_sync(0xffffffffu, checks);
+        nconf = __reduce_add_sync(0xffffffffu, nconf);
+        lits = __reduce_add_sync(0xffffffffu, lits);
+        if (lane == 0) {
+            if (checks) atomicAdd(g.bc + 0, static_cast<unsigned long long>(checks));
+            if (nconf) atomicAdd(g.bc + 1, static_cast<unsigned long long>(nconf));
+            if (lits) atomicAdd(g.bc + 2, static_cast<unsigned long long>(lits));
+        }
+    }
+
+    // Final min-e of every proposing nogood; per atom the smallest (e, sign)
+    // key wins. The e goes back into the proposal for the selection.
+    __device__ void grid_resolve(std::uint32_t gen) {
+        const std::uint32_t np = *reinterpret_cast<volatile std::uint32_t*>(&c->n_props);
+        int4* props = sl.props();
+        for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
+            const int4 p = props[i];
+            const std::uint32_t e = static_cast<std::uint32_t>(sl.claim()[p.x]);
+            atomicMin(sl.win() + atom_of(p.y), wkey(gen, e, p.y < 0));
+            props[i].z = static_cast<std::int32_t>(e);
+        }
+    }
+
+    // Per proposal: the winner of its atom assigns it (cell, reason, Deps),
+    // records literal and occurrence count at its e and marks e in the
+    // expansion bitmap; an opposite-sign loser turns its nogood into a
+    // conflict (assignment.cpp:116-124).
+    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev) {
+        const std::uint32_t np = *reinterpret_cast<volatile std::uint32_t*>(&c->n_props);
+        const int4* props = sl.props();
+        for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
+            const int4 p = props[i];
+            const std::uint32_t e = static_cast<std::uint32_t>(p.z);
+            const std::uint32_t a = atom_of(p.y);
+            const unsigned long long w = sl.win()[a];
+            if ((static_cast<std::uint32_t>(w) >> 1) == e) {
+                set_cell(a, p.y > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
+                sl.reason()[a] = p.x;
+                std::uint32_t len;
+                const std::int32_t* L = lits_of(static_cast<std::uint32_t>(p.x), len);
+                write_deps_from(L, len, static_cast<std::uint32_t>(p.x), a, dlev);
+                sl.occat()[e] = occ_total(lidx(p.y));
+                sl.litat()[e] = p.y;
+                atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
+            } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull)) {
+                sl.confl()[atomicAdd(&c->n_confl, 1u)] = p.x;
+            }
+        }
+    }
+
+    // Largest lane w with key[w] <= x, key non-decreasing over the lanes and
+    // key[0] <= x (five register shuffles).
+    __device__ static std::uint32_t lane_search(std::uint32_t key, std::uint32_t x) {
+        std::uint32_t w = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+            if (__shfl_sync(0xffffffffu, key, w + st) <= x) w += st;
+        return w;
+    }
+
+    // Winner count and occurrence sum of bitmap word wi (the 32 occurrence
+    // counts of a word are one aligned 128-byte line: eight vector loads).
+    __device__ unsigned long long word_value(std::uint32_t wi, std::uint32_t bits) const {
+        if (!bits) return 0ull;
+        const uint4* line = reinterpret_cast<const uint4*>(sl.occat() + static_cast<std::size_t>(wi) * 32);
+        uint4 q[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) q[k] = line[k];
+        std::uint32_t occ = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            occ += (bits >> (4 * k) & 1u) ? q[k].x : 0u;
+            occ += (bits >> (4 * k + 1) & 1u) ? q[k].y : 0u;
+            occ += (bits >> (4 * k + 2) & 1u) ? q[k].z : 0u;
+            occ += (bits >> (4 * k + 3) & 1u) ? q[k].w : 0u;
+        }
+        return (static_cast<unsigned long long>(__popc(bits)) << 32) | occ;
+    }
+
+    // Place the winners of this warp's 32 words (lane = word, `bits`), given
+    // each word's exclusive (count, occurrence) prefix `pre`: the set bits are
+    // dealt to the lanes 32 at a time in e order; a segmented lane scan gives
+    // each winner its occurrence offset inside its word.
+    __device__ void place_words(std::uint32_t wi, std::uint32_t bits, unsigned long long pre, std::int32_t* out,
+                                std::uint32_t ts0) {
+        const std::uint32_t lane = lane_id();
+        const std::uint32_t w0 = wi - lane;
+        std::uint32_t inc = __popc(bits);
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const std::uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= static_cast<std::uint32_t>(d)) inc += o;
+        }
+        const std::uint32_t exb = inc - __popc(bits);
+        const std::uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+        const std::uint32_t r0 = static_cast<std::uint32_t>(pre >> 32), o0 = static_cast<std::uint32_t>(pre);
+        std::uint32_t carry_w = 0xffffffffu, carry_s = 0;
+        for (std::uint32_t ch = 0; ch < total; ch += 32) {
+            const std::uint32_t idx = ch + lane;
+            const std::uint32_t w = lane_search(exb, idx);
+            const std::uint32_t bw = __shfl_sync(0xffffffffu, bits, w);
+            const std::uint32_t ew = __shfl_sync(0xffffffffu, exb, w);
+            const std::uint32_t rw = __shfl_sync(0xffffffffu, r0, w);
+            const std::uint32_t ow = __shfl_sync(0xffffffffu, o0, w);
+            const bool valid = idx < total;
+            const std::uint32_t k = idx - ew;
+            const std::uint32_t e = (w0 + w) * 32 + (valid ? __fns(bw, 0, static_cast<int>(k + 1)) : 0u);
+            const std::int32_t lit = valid ? sl.litat()[e] : 0;
+            const std::uint32_t occv = valid ? sl.occat()[e] : 0u;
+            std::uint32_t x = occv;  // segmented inclusive scan by word
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const std::uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+                const std::uint32_t wd = __shfl_up_sync(0xffffffffu, w, d);
+                if (lane >= static_cast<std::uint32_t>(d) && wd == w) x += y;
+            }
+            if (w == carry_w) x += carry_s;
+            if (valid) {
+                const std::uint32_t r = rw + k;
+                out[r] = lit;
+                sl.froff()[r] = ow + x - occv;
+                sl.trail()[ts0 + r] = lit;
+                sl.tpos()[atom_of(lit)] = ts0 + r;
+            }
+            carry_w = __shfl_sync(0xffffffffu, w, 31);
+            carry_s = __shfl_sync(0xffffffffu, x, 31);
+        }
+    }
+
+    // Winners, in e order, become the next frontier. Small passes are placed
+    // by block 0 alone with block scans (no grid barrier); large ones by the
+    // whole grid, one grid scan per round of words.
+    static constexpr std::uint32_t kBlockPlaceWords = 2048;
+
+    __device__ void grid_place(std::uint32_t T, std::uint32_t dst, std::uint32_t ts0, std::uint32_t& F_next,
+                               std::uint32_t& T_next) {
+        const std::uint32_t nw = (T + 31) / 32;
+        std::int32_t* out = sl.fr(dst);
+        std::uint32_t* bmp = sl.bitmap();
+        unsigned long long carry = 0;
+        if (nw <= kBlockPlaceWords) {
+            if (blockIdx.x == 0) {
+                for (std::uint32_t base = 0; base < nw; base += blockDim.x) {
+                    const std::uint32_t wi = base + threadIdx.x;
+                    const std::uint32_t bits = wi < nw ? bmp[wi] : 0u;
+                    if (bits) bmp[wi] = 0u;
+                    unsigned long long tot;
+                    const unsigned long long pre = g.block_scan(word_value(wi, bits), tot) + carry;
+                    place_words(wi, bits, pre, out, ts0);
+                    carry += tot;
+                }
+                F_next = static_cast<std::uint32_t>(carry >> 32);
+                T_next = static_cast<std::uint32_t>(carry);
+                if (threadIdx.x == 0) {
+                    sl.froff()[F_next] = T_next;
+                    c->F = F_next;
+                    c->T = T_next;
+                }
+            }
+            return;  // other blocks read F, T after the pass barrier
+        }
+        for (std::uint32_t base = 0; base < nw; base += g.size()) {
+            const std::uint32_t wi = base + g.tid();
+            const std::uint32_t bits = wi < nw ? bmp[wi] : 0u;
+            if (bits) bmp[wi] = 0u;
+            unsigned long long tot;
+            const unsigned long long pre = g.scan(word_value(wi, bits), tot) + carry;
+            place_words(wi, bits, pre, out, ts0);
+            carry += tot;
+        }
+        F_next = static_cast<std::uint32_t>(carry >> 32);
+        T_next = static_cast<std::uint32_t>(carry);
+        if (g.leader()) sl.froff()[F_next] = T_next;
+    }
+
+    __device__ bool propagate_grid(std::uint32_t level) {
+        mark(0);
+        frontier_offsets();
+        std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
+        const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
+        const bool learned = c->learned_n > 0;
+        if (threadIdx.x < 4) g.bc[threadIdx.x] = 0;
+        __syncthreads();
+        bool violated = false;
+        while (F != 0) {
+            grid_expand<4>(F, T, cur, gen, learned);
+            g.sync();
+            mark(2);
+            grid_resolve(gen);
+            g.sync();
+            mark(3);
+            grid_select(level, dlev);
+            g.sync();
+            mark(4);
+            // final for this pass: no block bumps it before the pass barrier
+            const std::uint32_t nconf = *reinterpret_cast<volatile std::uint32_t*>(&c->n_confl);
+            std::uint32_t Fn = 0, Tn = 0;
+            const bool small = (T + 31) / 32 <= kBlockPlaceWords;
+            grid_place(T, cur ^ 1u, ts, Fn, Tn);
+            if (g.leader()) {
+                c->n_props = 0;  // every block read it before the select barrier
+                c->st.passes += 1;
+            }
+            g.sync();
+            mark(5);
+            if (small) {
+                Fn = *reinterpret_cast<volatile std::uint32_t*>(&c->F);
+                Tn = *reinterpret_cast<volatile std::uint32_t*>(&c->T);
+            }
+            if (g.leader()) c->st.propagations += Fn;
+            ts += Fn;
+            F = Fn;
+            T = Tn;
+            cur ^= 1u;
+            gen += 1;
+            if (nconf) { violated = true; break; }
+        }
+        if (threadIdx.x == 0) {
+            atomicAdd(&c->st.checks, g.bc[0]);
+            if (g.bc[2]) atomicAdd(&c->st.checked_lits, g.bc[2]);
+        }
+        g.sync();
+        if (g.leader()) {
+            c->F = F;
+            c->T = T;
+            c->cur = cur;
+            c->gen = gen;
+            c->ts = ts;
+            c->b[11] = violated ? 1u : 0u;
+        }
+        g.sync();
+        return violated;
     }
 
     // One propagation call to fixpoint or violation (propagate.cpp:170-205).
@@ -934,6 +1353,7 @@ struct Search {
     static constexpr std::uint32_t kWarpPassT = 96;  // passes this small run in warp 0 alone
 
     __device__ bool propagate(std::uint32_t level) {
+        if constexpr (G::kGrid) return propagate_grid(level);
         mark(0);
         frontier_offsets();
         for (;;) {
@@ -1807,10 +2227,14 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
     const Slot sl{L.base, &L};
-    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u};
+    __shared__ unsigned long long gcnt[4];
+    __shared__ std::uint32_t gwsm[BS / 32 * 64];
+    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gwsm};
     if (g.leader() && sl.ctl()->status == kYield) sl.ctl()->status = kRunning;
     g.sync();
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
+    g.persist();
 }
 
 // Low-level operations on one slot (Propagator-style API for tests and the
@@ -1954,8 +2378,12 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ double sd[BS / 32];
     __shared__ std::uint32_t si[BS / 32];
     const Slot sl{L.base, &L};
-    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u};
+    __shared__ unsigned long long gcnt[4];
+    __shared__ std::uint32_t gwsm[BS / 32 * 64];
+    GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gwsm};
     do_op(g, S, C, sl, K, sh, op, Sm{&smc});
+    g.persist();
 }
 
 // Per-slot initial values that are not zero.

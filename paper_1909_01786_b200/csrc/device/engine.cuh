@@ -111,7 +111,7 @@ struct SlotLayout {
     unsigned long long bytes;
     unsigned long long o_ctl, o_cells, o_tpos, o_reason, o_deps, o_dovf, o_trail, o_ldec, o_fr0, o_fr1, o_froff,
         o_claim, o_win, o_props, o_confl, o_pending, o_bitmap, o_litat, o_loff, o_lpool, o_lhdr, o_larena,
-        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf;
+        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf, o_occat;
 };
 
 #if defined(__CUDACC__)
@@ -142,6 +142,7 @@ struct Slot {
     YAS_HD std::int32_t* pending() const { return at<std::int32_t>(L->o_pending); }
     YAS_HD std::uint32_t* bitmap() const { return at<std::uint32_t>(L->o_bitmap); }
     YAS_HD std::int32_t* litat() const { return at<std::int32_t>(L->o_litat); }
+    YAS_HD std::uint32_t* occat() const { return at<std::uint32_t>(L->o_occat); }  // grid slots only
     YAS_HD std::uint32_t* loff() const { return at<std::uint32_t>(L->o_loff); }
     YAS_HD std::int32_t* lpool() const { return at<std::int32_t>(L->o_lpool); }
     YAS_HD std::uint32_t* lhdr() const { return at<std::uint32_t>(L->o_lhdr); }  // (2A+2)*4 * {ptr,size,cap}
@@ -164,6 +165,8 @@ struct Shared {  // global (all-slot) coordination
     std::uint32_t bar_count, bar_gen;
     unsigned long long t_start;
     std::uint32_t partial_pad[27];
+    // grid barrier: block b publishes the epoch of the barrier it reached
+    std::uint32_t arrive[1024];
 };
 
 }  // namespace yas::dev

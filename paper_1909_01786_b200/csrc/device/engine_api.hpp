@@ -71,16 +71,17 @@ public:
     bool initial_propagation();
     bool propagate(std::uint32_t level);
     void push_decision(std::int32_t lit);
-    void assign(const std::vector<std::int32_t>& lits, std::uint32_t level, std::int32_t antecedent,
-                const std::vector<unsigned long long>& deps, bool ovf);
-    void seed(const std::vector<std::int32_t>& lits);
+    void assign(const std::int32_t* lits, std::size_t n, std::uint32_t level, std::int32_t antecedent,
+                const unsigned long long* deps, std::size_t n_deps, bool ovf);
+    void seed(const std::int32_t* lits, std::size_t n);
     std::int32_t add_learned(const std::vector<std::int32_t>& lits);
     void set_count_lits(bool on);
 
     // read back
-    dev::Ctl ctl() const;
+    const dev::Ctl& ctl() const;  // synchronises with the session's stream
     std::vector<std::int32_t> cells() const;
     std::vector<std::int32_t> trail() const;
+    std::size_t trail_into(std::int32_t* out, std::size_t cap) const;  // returns the trail size
     std::vector<std::int32_t> reasons() const;
     std::vector<unsigned long long> deps_word(std::uint32_t w) const;
     std::vector<std::uint8_t> deps_overflow() const;

@@ -137,6 +137,7 @@ struct Arena {
         L.o_mbuf = take(4ull * mcap * K.mwords);
         L.o_mcube = take(4ull * mcap);
         L.o_tbuf = take(16ull * tcap);
+        L.o_occat = take(grid_blocks ? 4 * tbits : 0);  // whole-grid passes only
         L.bytes = o;
         L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
         ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
@@ -147,7 +148,7 @@ struct Arena {
         sh = dalloc<dev::Shared>(1, owned);
         ck(cudaMemset(sh, 0, sizeof(dev::Shared)), "memset");
         const std::uint32_t gb = grid_blocks ? grid_blocks : 1;
-        partial = dalloc<unsigned long long>(2 * gb, owned);
+        partial = dalloc<unsigned long long>(4 * gb, owned);
         pd = dalloc<double>(gb, owned);
         pi = dalloc<std::uint32_t>(gb, owned);
     }
@@ -324,7 +325,29 @@ struct Session::Impl {
     bool grid = false;
     std::uint32_t gblocks = 0;
     int device = 0;
+    cudaStream_t stream{};
     cudaEvent_t e0{}, e1{};
+    // Every op is stream ordered: inputs go through one persistent device
+    // staging buffer (an H2D copy is ordered after the previous kernel), and
+    // the control block is copied into pinned host memory after each kernel,
+    // so only calls that return device state synchronise.
+    std::int32_t* d_lits = nullptr;
+    std::size_t d_lits_cap = 0;
+    unsigned long long* d_deps = nullptr;
+    dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
+    bool ctl_pending = false;
+    std::vector<std::uint32_t> seen;  // assign(): first occurrence per atom
+    std::uint32_t seen_epoch = 0;
+
+    std::int32_t* stage(const std::int32_t* src, std::size_t n) {
+        if (n > d_lits_cap) {
+            if (d_lits) cudaFree(d_lits);
+            d_lits_cap = std::max<std::size_t>(n, 2 * d_lits_cap);
+            ck(cudaMalloc(&d_lits, d_lits_cap * sizeof(std::int32_t)), "cudaMalloc staging");
+        }
+        if (n) ck(cudaMemcpyAsync(d_lits, src, n * sizeof(std::int32_t), cudaMemcpyHostToDevice, stream), "stage");
+        return d_lits;
+    }
 };
 
 Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, int device, std::uint32_t lcap,
@@ -352,34 +375,50 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     c.fanout = 1;
     c.learned_capacity = ~0ull;
     c.n_cubes = 1;
+    ck(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&impl_->e0), "event");
     ck(cudaEventCreate(&impl_->e1), "event");
+    ck(cudaMalloc(&impl_->d_deps, 1024 * sizeof(unsigned long long)), "cudaMalloc deps");
+    ck(cudaMallocHost(&impl_->h_ctl, sizeof(dev::Ctl)), "cudaMallocHost");
+    std::memset(impl_->h_ctl, 0, sizeof(dev::Ctl));
+    impl_->seen.assign(impl_->ar.A + 1, 0);
     reset();
 }
 
 Session::~Session() {
+    cudaStreamSynchronize(impl_->stream);
+    if (impl_->d_lits) cudaFree(impl_->d_lits);
+    cudaFree(impl_->d_deps);
+    cudaFreeHost(impl_->h_ctl);
     cudaEventDestroy(impl_->e0);
     cudaEventDestroy(impl_->e1);
+    cudaStreamDestroy(impl_->stream);
 }
 
 namespace {
+// Enqueue one op kernel and the control-block copy behind it. `ms` (when
+// given) waits for the kernel and returns its CUDA-event time.
 void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
-    cudaEventRecord(im.e0);
+    ck(cudaEventRecord(im.e0, im.stream), "record");
     if (im.grid) {
         dev::OpArgs o = op;
         void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &o,
                         &im.smc};
         ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::op_grid_kernel<kGridBS>), dim3(im.gblocks),
-                                       dim3(kGridBS), args, 0, nullptr),
+                                       dim3(kGridBS), args, 0, im.stream),
            "op grid launch");
     } else {
-        dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem>>>(im.ar.S, im.cfg, im.ar.L, im.ar.K, im.ar.sh, op,
-                                                                im.smc);
+        dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem, im.stream>>>(im.ar.S, im.cfg, im.ar.L, im.ar.K, im.ar.sh,
+                                                                          op, im.smc);
         ck(cudaGetLastError(), "op launch");
     }
-    cudaEventRecord(im.e1);
-    ck(cudaEventSynchronize(im.e1), "op kernel");
-    if (ms) cudaEventElapsedTime(ms, im.e0, im.e1);
+    ck(cudaEventRecord(im.e1, im.stream), "record");
+    ck(cudaMemcpyAsync(im.h_ctl, im.ar.slots[0].ctl(), sizeof(dev::Ctl), cudaMemcpyDeviceToHost, im.stream), "ctl");
+    im.ctl_pending = true;
+    if (ms) {
+        ck(cudaEventSynchronize(im.e1), "op kernel");
+        cudaEventElapsedTime(ms, im.e0, im.e1);
+    }
 }
 }  // namespace
 
@@ -411,83 +450,100 @@ void Session::push_decision(std::int32_t lit) {
     run_op(*impl_, op, nullptr);
 }
 
-void Session::assign(const std::vector<std::int32_t>& lits_in, std::uint32_t level, std::int32_t antecedent,
-                     const std::vector<unsigned long long>& deps, bool ovf) {
+void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_t level, std::int32_t antecedent,
+                     const unsigned long long* deps, std::size_t n_deps, bool ovf) {
     // the device op takes distinct atoms (a repeated atom would be agreed or a
     // conflict in try_set, i.e. no change): keep the first occurrence only
+    Impl& im = *impl_;
+    if (++im.seen_epoch == 0) {
+        std::fill(im.seen.begin(), im.seen.end(), 0u);
+        im.seen_epoch = 1;
+    }
     std::vector<std::int32_t> lits;
-    lits.reserve(lits_in.size());
-    std::vector<char> seen(impl_->ar.A + 1, 0);
-    for (std::int32_t l : lits_in) {
+    lits.reserve(n_in);
+    for (std::size_t i = 0; i < n_in; ++i) {
+        const std::int32_t l = lits_in[i];
         const std::uint32_t a = static_cast<std::uint32_t>(l < 0 ? -l : l);
-        if (a > impl_->ar.A || seen[a]) continue;
-        seen[a] = 1;
+        if (a == 0 || a > im.ar.A || im.seen[a] == im.seen_epoch) continue;
+        im.seen[a] = im.seen_epoch;
         lits.push_back(l);
     }
-    std::vector<void*> tmp;
+    unsigned long long d[1024] = {0};
+    for (std::size_t i = 0; i < n_deps && i < W_; ++i) d[i] = deps[i];
+    ck(cudaMemcpyAsync(im.d_deps, d, W_ * sizeof(unsigned long long), cudaMemcpyHostToDevice, im.stream), "deps");
     dev::OpArgs op{};
     op.op = dev::kOpAssign;
     op.level = level;
     op.antecedent = antecedent;
-    op.lits = dupload(lits, tmp);
+    op.lits = im.stage(lits.data(), lits.size());
     op.n = static_cast<std::uint32_t>(lits.size());
-    std::vector<unsigned long long> d(W_, 0ull);
-    for (std::size_t i = 0; i < deps.size() && i < W_; ++i) d[i] = deps[i];
-    op.deps = dupload(d, tmp);
+    op.deps = im.d_deps;
     op.ovf = ovf ? 1u : 0u;
-    run_op(*impl_, op, nullptr);
-    for (void* p : tmp) cudaFree(p);
+    run_op(im, op, nullptr);
 }
 
-void Session::seed(const std::vector<std::int32_t>& lits) {
-    std::vector<void*> tmp;
+void Session::seed(const std::int32_t* lits, std::size_t n) {
     dev::OpArgs op{};
     op.op = dev::kOpSeed;
-    op.lits = dupload(lits, tmp);
-    op.n = static_cast<std::uint32_t>(lits.size());
+    op.lits = impl_->stage(lits, n);
+    op.n = static_cast<std::uint32_t>(n);
     run_op(*impl_, op, nullptr);
-    for (void* p : tmp) cudaFree(p);
 }
 
 std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
-    std::vector<void*> tmp;
     dev::OpArgs op{};
     op.op = dev::kOpLearn;
-    op.lits = dupload(lits, tmp);
+    op.lits = impl_->stage(lits.data(), lits.size());
     op.n = static_cast<std::uint32_t>(lits.size());
     run_op(*impl_, op, nullptr);
-    for (void* p : tmp) cudaFree(p);
     return static_cast<std::int32_t>(ctl().b[12]);
 }
 
 void Session::set_count_lits(bool on) { impl_->cfg.count_lits = on ? 1u : 0u; }
 
-dev::Ctl Session::ctl() const {
-    dev::Ctl c{};
-    ck(cudaMemcpy(&c, impl_->ar.slots[0].ctl(), sizeof(c), cudaMemcpyDeviceToHost), "ctl");
-    return c;
+const dev::Ctl& Session::ctl() const {
+    if (impl_->ctl_pending) {
+        ck(cudaStreamSynchronize(impl_->stream), "stream");
+        impl_->ctl_pending = false;
+    }
+    return *impl_->h_ctl;
 }
 
 namespace {
 template <class T>
-std::vector<T> dl(const T* p, std::size_t n) {
+std::size_t dl_into(const T* p, std::size_t n, T* out, cudaStream_t s) {
+    if (n) {
+        ck(cudaMemcpyAsync(out, p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "download");
+        ck(cudaStreamSynchronize(s), "download");
+    }
+    return n;
+}
+template <class T>
+std::vector<T> dl(const T* p, std::size_t n, cudaStream_t s) {
     std::vector<T> v(n);
-    if (n) ck(cudaMemcpy(v.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost), "download");
+    dl_into(p, n, v.data(), s);
     return v;
 }
 }  // namespace
 
-std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1); }
-std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts); }
-std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1); }
-std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
-    return dl(impl_->ar.slots[0].deps() + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1);
+std::size_t Session::trail_into(std::int32_t* out, std::size_t cap) const {
+    const std::size_t n = ctl().ts;
+    if (out && cap >= n) dl_into(impl_->ar.slots[0].trail(), n, out, impl_->stream);
+    else if (out && cap) dl_into(impl_->ar.slots[0].trail(), cap, out, impl_->stream);
+    return n;
 }
-std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1); }
-std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl); }
+
+std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1, impl_->stream); }
+std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts, impl_->stream); }
+std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream); }
+std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
+    return dl(impl_->ar.slots[0].deps() + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1, impl_->stream);
+}
+std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream); }
+std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl, impl_->stream); }
 std::vector<std::int32_t> Session::frontier() const {
-    const dev::Ctl c = ctl();
-    return dl(impl_->ar.slots[0].fr(c.cur), c.F);
+    const dev::Ctl& c = ctl();
+    return dl(impl_->ar.slots[0].fr(c.cur), c.F, impl_->stream);
 }
 
 }  // namespace yas

@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_propagate.py -x -q > gpurun_out/pt2.log 2>&1; echo "rc=$?" >> gpurun_out/pt2.log
+timeout 300 python scripts/planted_profile.py > gpurun_out/prof1m.log 2>&1
+timeout 300 python scripts/planted_profile.py 800000 8000000 50 3 > gpurun_out/prof8m.log 2>&1
+timeout 300 python scripts/planted_profile.py 100000 1000000 1 3 > gpurun_out/prof1m_1pct.log 2>&1
+timeout 300 python bench.py --no-extras > gpurun_out/bench2.json 2>gpurun_out/bench2.err

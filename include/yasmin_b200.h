@@ -212,6 +212,13 @@ uint32_t yas_propagator_level(const yas_propagator* p);
  * thread between barriers: [1] frontier offsets, [2] expand+evaluate,
  * [3] resolve, [4] apply, [5] compact. */
 int yas_propagator_profile(const yas_propagator* p, uint64_t out[16]);
+/* Diagnostics: on = 1/0 enables/disables per-pass, per-block phase timestamps
+ * (global timer, ns) for whole-grid propagations, -1 leaves it; out (when
+ * given) receives 64 passes x blocks x 10 stamps: [0] pass start, [1] expand
+ * done, [2] after barrier, [3] resolve done, [4] after barrier, [5] select
+ * done, [6] after barrier, [7] place done, [8] after barrier; stamp [9] of
+ * block 0 = T << 32 | F of the pass. */
+int yas_propagator_pass_trace(yas_propagator* p, int on, uint64_t* out, size_t cap, uint32_t* blocks);
 
 #ifdef __cplusplus
 }

@@ -591,6 +591,17 @@ class Propagator:
     def level(self) -> int:
         return N.lib().yas_propagator_level(self._h)
 
+    def pass_trace(self, on: Optional[bool] = None):
+        """Diagnostics: enable/disable (on) and read the per-pass, per-block
+        phase timestamps of whole-grid propagations: array [64, blocks, 10]."""
+        N.lib().yas_propagator_pass_trace(self._h, -1 if on is None else int(bool(on)), None, 0, None)
+        blocks = C.c_uint32(0)
+        out = np.zeros(64 * 148 * 10 * 4, dtype=np.uint64)
+        N.lib().yas_propagator_pass_trace(self._h, -1, out.ctypes.data_as(C.POINTER(C.c_uint64)), out.size,
+                                          C.byref(blocks))
+        b = max(1, blocks.value)
+        return out[: 64 * b * 10].reshape(64, b, 10)
+
     def profile(self) -> List[int]:
         """Diagnostics: SM cycles per propagation phase (see yas_propagator_profile)."""
         out = (C.c_uint64 * 16)()

@@ -704,6 +704,19 @@ int yas_propagator_count_literals(yas_propagator* p, int on) {
     return YAS_OK;
 }
 uint32_t yas_propagator_atoms(const yas_propagator* p) { return p ? p->atoms : 0; }
+int yas_propagator_pass_trace(yas_propagator* p, int on, uint64_t* out, size_t cap, uint32_t* blocks) {
+    if (!p) return YAS_ERR_ARG;
+    return guarded(nullptr, 0, [&] {
+        if (on >= 0) p->s->set_pass_trace(on != 0);
+        if (out) {
+            std::uint32_t b = 0;
+            const auto v = p->s->pass_trace(b);
+            for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
+            if (blocks) *blocks = b;
+        }
+        return static_cast<int>(YAS_OK);
+    });
+}
 int yas_propagator_profile(const yas_propagator* p, uint64_t out[16]) {
     if (!p || !out) return YAS_ERR_ARG;
     return guarded(nullptr, 0, [&] {

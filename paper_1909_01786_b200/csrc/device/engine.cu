@@ -196,7 +196,8 @@ struct GridG {
     std::uint32_t parity;
     unsigned long long* bc;  // shared: per-block pass counters {checks, conflicts, literals}
     std::uint32_t epoch;     // barriers passed (same in every block)
-    std::uint32_t* wsm;      // shared: 64 words per warp (compaction)
+    std::uint32_t* snap;     // shared: control words snapshotted at a barrier
+    std::int32_t* scanq;     // shared: per-warp queue of nogoods needing a full scan
 
     __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
     __device__ std::uint32_t size() const { return gridDim.x * BS; }
@@ -232,7 +233,12 @@ struct GridG {
     // across launches (see persist()). 1.2 us per barrier on B200 with 148
     // CTAs (scripts/barrier_probe.cu), against 2.1 us for a counter+generation
     // barrier with two fences and 5.5 us for flag all-gathers.
-    __device__ void sync() {
+    __device__ void sync() { sync_snap(nullptr, nullptr); }
+    // Barrier that also snapshots up to two control words, read once per
+    // block by thread 0 after the barrier, into shared memory (snap[0..1]):
+    // all threads reading one global word would queue thousands of requests
+    // on one L2 slice.
+    __device__ void sync_snap(const std::uint32_t* a, const std::uint32_t* b) {
         __syncthreads();
         ++epoch;
         if (threadIdx.x == 0) {
@@ -244,6 +250,8 @@ struct GridG {
                 if (static_cast<int>(v - target) >= 0) break;
             }
             __threadfence();
+            if (a) snap[0] = *reinterpret_cast<const volatile std::uint32_t*>(a);
+            if (b) snap[1] = *reinterpret_cast<const volatile std::uint32_t*>(b);
         }
         __syncthreads();
     }
@@ -472,7 +480,18 @@ struct Search {
 
     // ---- assignment access: 2-bit shared mirror when present --------------
     // sign of the atom's value: 0 unassigned, 1 true, -1 false
+    // Whole-grid slots keep a 2-bit mirror of the assignment in global memory
+    // (16 atoms per word; 25 KB for 100k atoms) next to the cells.
+    __device__ static int mirror_val(std::uint32_t word, std::uint32_t a) {
+        const std::uint32_t v = (word >> (2 * (a & 15))) & 3u;
+        return v == 0 ? 0 : (v == 3 ? 1 : -1);
+    }
+    // Pass-snapshot read (L1-cached): only for values that cannot change
+    // during the current phase.
+    __device__ std::uint32_t mirror_word_snap(std::uint32_t a) const { return __ldca(sl.gmirror() + (a >> 4)); }
+
     __device__ int val(std::uint32_t a) const {
+        if constexpr (G::kGrid) return mirror_val(__ldcg(sl.gmirror() + (a >> 4)), a);
         if (sm.vwords()) {
             const std::uint32_t b = 1u << (a & 31);
             if (!(sm.vasg()[a >> 5] & b)) return 0;
@@ -483,6 +502,13 @@ struct Search {
     }
     __device__ void set_cell(std::uint32_t a, std::int32_t cv) const {
         sl.cells()[a] = cv;
+        if constexpr (G::kGrid) {
+            std::uint32_t* w = sl.gmirror() + (a >> 4);
+            const std::uint32_t sh2 = 2 * (a & 15);
+            if (cv == 0) atomicAnd(w, ~(3u << sh2));
+            else atomicOr(w, (cv > 0 ? 3u : 1u) << sh2);  // bits are clear while unassigned
+            return;
+        }
         if (sm.vwords()) {
             const std::uint32_t b = 1u << (a & 31);
             if (cv == 0) {
@@ -535,18 +561,20 @@ struct Search {
         return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot()[li];
     }
     // j-th entry of the literal's occurrence list [static c0, learned c0, ...,
-    // static c3, learned c3]: {id, guard, x, y} and its length class. All
-    // segment bounds are loaded at once (one memory round trip), then one
-    // dependent 16-byte load fetches the entry.
+    // static c3, learned c3]: {id, guard, x, y} and its length class. Entries
+    // carry their class in the top two bits of the id, so with no learned
+    // nogoods one offset load and one dependent 16-byte load suffice.
+    __device__ static int4 decode(int4 ent, std::uint32_t& cls) {
+        cls = static_cast<std::uint32_t>(ent.x) >> 30;
+        ent.x &= 0x3fffffff;
+        return ent;
+    }
     __device__ int4 occ_entry(std::uint32_t li, std::uint32_t j, bool learned, std::uint32_t& cls) const {
         const std::uint32_t* oo = S.occ_off + li * 4;
+        if (!learned) return decode(__ldg(S.occ + __ldg(oo) + j), cls);
         std::uint32_t b[5];
 #pragma unroll
         for (int k = 0; k < 5; ++k) b[k] = __ldg(oo + k);
-        if (!learned) {  // static classes are contiguous
-            cls = (j >= b[1] - b[0]) + (j >= b[2] - b[0]) + (j >= b[3] - b[0]);
-            return __ldg(S.occ + b[0] + j);
-        }
         const std::uint32_t* h = sl.lhdr() + 12 * li;
         std::uint32_t hp[4], hn[4];
 #pragma unroll
@@ -557,12 +585,12 @@ struct Search {
 #pragma unroll
         for (int cl = 0; cl < 4; ++cl) {
             const std::uint32_t ns = b[cl + 1] - b[cl];
-            cls = static_cast<std::uint32_t>(cl);
-            if (j < ns) return __ldg(S.occ + b[cl] + j);
+            if (j < ns) return decode(__ldg(S.occ + b[cl] + j), cls);
             j -= ns;
-            if (j < hn[cl]) return sl.larena()[hp[cl] + j];
+            if (j < hn[cl]) return decode(sl.larena()[hp[cl] + j], cls);
             j -= hn[cl];
         }
+        cls = 0;
         return make_int4(-1, 0, 0, 0);
     }
     __device__ std::uint32_t nwords(std::uint32_t level) const {
@@ -579,11 +607,20 @@ struct Search {
 
     // phase accounting: cycles since the previous mark go to bucket k
     __device__ void mark(int k) const {
+        if constexpr (G::kGrid) return;  // grid passes: see stamp()
         if (g.leader()) {
             const unsigned long long t = clock64();
             c->prof[k] += t - c->prof_t;
             c->prof_t = t;
         }
+    }
+
+    // Diagnostics: thread 0 of every block stamps the global timer at phase
+    // boundaries of the first kPtracePasses passes of a grid propagation.
+    static constexpr std::uint32_t kPtracePasses = 64, kPtraceStamps = 10;
+    __device__ void stamp(std::uint32_t pass, std::uint32_t k) const {
+        if (C.ptrace && threadIdx.x == 0 && pass < kPtracePasses)
+            C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x + blockIdx.x) * kPtraceStamps + k] = gtimer();
     }
 
     __device__ void fail(std::uint32_t status) {
@@ -800,14 +837,30 @@ struct Search {
         }
         std::uint32_t nfree = 0;
         std::int32_t u1 = 0;
-        for (std::uint32_t k = 0; k < len; ++k) {
-            const std::int32_t l = lit_at(L, k, static_cast<std::uint32_t>(id));
-            const int v = val(atom_of(l));
-            if (v == 0) {
-                if (nfree == 0) u1 = l;
-                if (++nfree == 2) return;
-            } else if ((v > 0) != (l > 0)) {
-                return;  // a dead literal: satisfied
+        bool dead = false;
+        if (len <= 8) {  // all literal loads, then all value loads: two round trips
+            std::int32_t l[8];
+            int v[8];
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) l[k] = k < len ? lit_at(L, k, static_cast<std::uint32_t>(id)) : 0;
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) v[k] = k < len ? val(atom_of(l[k])) : 2;
+#pragma unroll
+            for (int k = 7; k >= 0; --k) {  // u1 = first free literal in nogood order
+                if (v[k] == 0) { ++nfree; u1 = l[k]; }
+                else if (v[k] != 2 && (v[k] > 0) != (l[k] > 0)) dead = true;
+            }
+            if (dead || nfree >= 2) return;
+        } else {
+            for (std::uint32_t k = 0; k < len; ++k) {
+                const std::int32_t l = lit_at(L, k, static_cast<std::uint32_t>(id));
+                const int v = val(atom_of(l));
+                if (v == 0) {
+                    if (nfree == 0) u1 = l;
+                    if (++nfree == 2) return;
+                } else if ((v > 0) != (l > 0)) {
+                    return;  // a dead literal: satisfied
+                }
             }
         }
         if (nfree == 0) conflict = true;
@@ -884,9 +937,7 @@ struct Search {
             std::int32_t id = -1, plit = 0;
             std::uint32_t slot = 0, meta = 0, clen = 0;
             unsigned long long d0 = 0;
-            unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
             if (e < T) {
-                if (g.leader()) tq0 = clock64();
                 std::uint32_t lo = 0, hi = F;
                 while (hi - lo > 1) {
                     const std::uint32_t mid = (lo + hi) >> 1;
@@ -896,7 +947,6 @@ struct Search {
                 std::uint32_t cls;
                 const int4 ent = occ_entry(lidx(trig), e - sm.froff()[lo], learned, cls);
                 id = ent.x;
-                if (g.leader()) { asm volatile("" ::"r"(id)); tq1 = clock64(); }
                 const unsigned long long key = (static_cast<unsigned long long>(id + 1) << 32) | e;
                 for (std::uint32_t h = hslot(static_cast<std::uint32_t>(id), hm);; h = (h + 1) & hm) {
                     unsigned long long cur_k = sm.htab()[h];
@@ -909,17 +959,7 @@ struct Search {
                         break;
                     }
                 }
-                if (g.leader()) tq2 = clock64();
                 if (first) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
-                if (g.leader()) {
-                    asm volatile("" ::"r"(plit), "r"(clen));
-                    const unsigned long long tq3 = clock64();
-                    c->prof[8] += tq1 - tq0;
-                    c->prof[9] += tq2 - tq1;
-                    c->prof[10] += tq3 - tq2;
-                    c->prof[12] += T;
-                    c->prof[13] += 1;
-                }
             }
             __syncwarp();
             warp_count(&c->st.checks, first);
@@ -1029,15 +1069,63 @@ struct Search {
     // frontier offsets once and every lane finds its trigger with five register
     // shuffles. U independent entries per lane keep U gathers, U claim atomics
     // and their cell lookups in flight at once.
+    // Full scan of nogood `id` against the pass snapshot (propagate.cpp:86-168
+    // without watches): literals, then their values, each as one batch of
+    // independent loads.
+    __device__ void scan_snap(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len) const {
+        const std::uint32_t guard = guard_of(static_cast<std::uint32_t>(id));
+        const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+        std::uint32_t nfree = 0;
+        std::int32_t u1 = 0;
+        for (std::uint32_t k0 = 0; k0 < len; k0 += 8) {
+            std::int32_t l[8];
+            std::uint32_t w[8];
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) l[k] = k0 + k < len ? lit_at(L, k0 + k, static_cast<std::uint32_t>(id)) : 0;
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) w[k] = mirror_word_snap(atom_of(l[k]));
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) {
+                if (k0 + k >= len) break;
+                const int v = mirror_val(w[k], atom_of(l[k]));
+                if (v == 0) {
+                    if (nfree == 0) u1 = l[k];
+                    ++nfree;
+                } else if ((v > 0) != (l[k] > 0)) {
+                    return;  // a dead literal: satisfied
+                }
+            }
+            if (nfree >= 2) return;
+        }
+        if (nfree == 0) conflict = true;
+        else if (may_assert(guard, -u1)) {
+            prop = true;
+            plit = -u1;
+        }
+    }
+
+    // Expansion entries e in [0, T) are split into one contiguous range per
+    // warp (warps numbered block-interleaved). A warp locates the frontier
+    // literal of its first entry with a 32-ary search, then walks: per batch
+    // of 32*U entries it loads the next 32 frontier offsets once and every
+    // lane finds its trigger with five register shuffles. The U entries of a
+    // lane are processed in lock step — gathers, claim atomics and the value
+    // loads of the two literals carried in the entry are all issued before
+    // any of them is used — and the few long nogoods the entry cannot decide
+    // are compacted over the warp's lanes for one batched full scan.
+    static constexpr int kExpandU = 8;
+
     template <int U>
     __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned) {
         const std::int32_t* fr = sl.fr(cur);
         const std::uint32_t* froff = sl.froff();
         const std::uint32_t lane = lane_id();
+        const unsigned below = (1u << lane) - 1u;
+        std::int32_t* scanq = g.scanq + (threadIdx.x >> 5) * (32 * U);
         const std::uint32_t nwarps = g.size() >> 5, wid = g.iwarp();
         const std::uint32_t per = (((T + nwarps - 1) / nwarps) + 31u) & ~31u;
         const unsigned long long start64 = static_cast<unsigned long long>(wid) * per;
-        std::uint32_t checks = 0, nconf = 0, lits = 0;
+        std::uint32_t checks = 0, lits = 0;
         if (start64 < T) {
             const std::uint32_t start = static_cast<std::uint32_t>(start64);
             const std::uint32_t end = T - start < per ? T : start + per;
@@ -1095,39 +1183,105 @@ struct Search {
                     const std::uint32_t e = base + 32u * u + lane;
                     old[u] = e < end ? atomicMin(sl.claim() + ent[u].x, ckey(gen, e)) : ckey(gen, 0);
                 }
+                std::uint32_t wx[U], wy[U];  // issued while the claims are in flight
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const bool first = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
-                    bool conflict = false, prop = false;
-                    std::int32_t plit = 0;
-                    std::uint32_t clen = 0;
-                    if (first) evaluate_entry(ent[u], cls[u], trig[u], conflict, prop, plit, clen);
-                    checks += first ? 1u : 0u;
-                    lits += clen;
-                    nconf += conflict ? 1u : 0u;
-                    const std::uint32_t cs = warp_append(&c->n_confl, conflict);
-                    if (conflict) sl.confl()[cs] = ent[u].x;
-                    const std::uint32_t ps = warp_append(&c->n_props, prop);
-                    if (prop) sl.props()[ps] = make_int4(ent[u].x, plit, 0, 0);
+                    wx[u] = mirror_word_snap(cls[u] >= 1 ? atom_of(ent[u].z) : 0u);
+                    wy[u] = mirror_word_snap(cls[u] >= 2 ? atom_of(ent[u].w) : 0u);
+                }
+                bool first[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) first[u] = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                // decide from the entry: 0 nothing, 1 conflict, 2 proposal, 3 full scan
+                std::uint32_t stt[U];
+                std::int32_t plit[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    plit[u] = 0;
+                    stt[u] = 0;
+                    if (!first[u]) continue;
+                    ++checks;
+                    if (cls[u] == 0) { stt[u] = 1; lits += 1; continue; }
+                    const int vx = mirror_val(wx[u], atom_of(ent[u].z));
+                    const int sx = vx == 0 ? 0 : ((vx > 0) == (ent[u].z > 0) ? 1 : -1);  // 1 holds, -1 dead, 0 free
+                    int sy = 1;
+                    if (cls[u] >= 2) {
+                        const int vy = mirror_val(wy[u], atom_of(ent[u].w));
+                        sy = vy == 0 ? 0 : ((vy > 0) == (ent[u].w > 0) ? 1 : -1);
+                    }
+                    const bool decided = sx < 0 || sy < 0 || (sx == 0 && sy == 0);
+                    if (cls[u] == 3 && !decided) { stt[u] = 3; continue; }
+                    lits += (cls[u] == 3 && C.count_lits) ? length_of(static_cast<std::uint32_t>(ent[u].x)) : cls[u] + 1;
+                    if (decided) continue;
+                    if (sx > 0 && sy > 0) { stt[u] = 1; continue; }
+                    const std::int32_t u1 = sx == 0 ? ent[u].z : ent[u].w;
+                    if (may_assert(static_cast<std::uint32_t>(ent[u].y), -u1)) { stt[u] = 2; plit[u] = -u1; }
+                }
+                unsigned cm[U], pm[U], qm[U];
+                std::uint32_t nprop = 0, nscan = 0;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    cm[u] = __ballot_sync(0xffffffffu, stt[u] == 1);
+                    pm[u] = __ballot_sync(0xffffffffu, stt[u] == 2);
+                    qm[u] = __ballot_sync(0xffffffffu, stt[u] == 3);
+                    nprop += __popc(pm[u]);
+                    nscan += __popc(qm[u]);
+                    if (cm[u]) {  // rare
+                        std::uint32_t at = 0;
+                        if (lane == 0) at = atomicAdd(&c->n_confl, static_cast<std::uint32_t>(__popc(cm[u])));
+                        at = __shfl_sync(0xffffffffu, at, 0);
+                        if (cm[u] >> lane & 1u) sl.confl()[at + __popc(cm[u] & below)] = ent[u].x;
+                    }
+                }
+                if (nprop) {  // one reservation per batch for all its proposals
+                    std::uint32_t at = 0;
+                    if (lane == 0) at = atomicAdd(&c->n_props, nprop);
+                    at = __shfl_sync(0xffffffffu, at, 0);
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (pm[u] >> lane & 1u) sl.props()[at + __popc(pm[u] & below)] = make_int4(ent[u].x, plit[u], 0, 0);
+                        at += __popc(pm[u]);
+                    }
+                }
+                if (nscan) {  // long nogoods the entry could not decide: one lane each
+                    std::uint32_t at = 0;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (qm[u] >> lane & 1u) scanq[at + __popc(qm[u] & below)] = ent[u].x;
+                        at += __popc(qm[u]);
+                    }
+                    __syncwarp();
+                    for (std::uint32_t r = 0; r < nscan; r += 32) {
+                        bool conflict = false, prop = false;
+                        std::int32_t pl = 0, id = 0;
+                        if (r + lane < nscan) {
+                            id = scanq[r + lane];
+                            std::uint32_t len = 0;
+                            scan_snap(id, conflict, prop, pl, len);
+                            lits += len;
+                        }
+                        const std::uint32_t cs = warp_append(&c->n_confl, conflict);
+                        if (conflict) sl.confl()[cs] = id;
+                        const std::uint32_t ps = warp_append(&c->n_props, prop);
+                        if (prop) sl.props()[ps] = make_int4(id, pl, 0, 0);
+                    }
+                    __syncwarp();
                 }
                 p0 = __shfl_sync(0xffffffffu, pe[U - 1], 31);
                 f0 = __shfl_sync(0xffffffffu, se[U - 1], 31);
             }
         }
         checks = __reduce_add_sync(0xffffffffu, checks);
-        nconf = __reduce_add_sync(0xffffffffu, nconf);
         lits = __reduce_add_sync(0xffffffffu, lits);
         if (lane == 0) {
             if (checks) atomicAdd(g.bc + 0, static_cast<unsigned long long>(checks));
-            if (nconf) atomicAdd(g.bc + 1, static_cast<unsigned long long>(nconf));
             if (lits) atomicAdd(g.bc + 2, static_cast<unsigned long long>(lits));
         }
     }
 
     // Final min-e of every proposing nogood; per atom the smallest (e, sign)
     // key wins. The e goes back into the proposal for the selection.
-    __device__ void grid_resolve(std::uint32_t gen) {
-        const std::uint32_t np = *reinterpret_cast<volatile std::uint32_t*>(&c->n_props);
+    __device__ void grid_resolve(std::uint32_t gen, std::uint32_t np) {
         int4* props = sl.props();
         for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
             const int4 p = props[i];
@@ -1141,8 +1295,7 @@ struct Search {
     // records literal and occurrence count at its e and marks e in the
     // expansion bitmap; an opposite-sign loser turns its nogood into a
     // conflict (assignment.cpp:116-124).
-    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev) {
-        const std::uint32_t np = *reinterpret_cast<volatile std::uint32_t*>(&c->n_props);
+    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np) {
         const int4* props = sl.props();
         for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
             const int4 p = props[i];
@@ -1290,7 +1443,6 @@ struct Search {
     }
 
     __device__ bool propagate_grid(std::uint32_t level) {
-        mark(0);
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
@@ -1298,18 +1450,26 @@ struct Search {
         if (threadIdx.x < 4) g.bc[threadIdx.x] = 0;
         __syncthreads();
         bool violated = false;
+        std::uint32_t pass = 0;
         while (F != 0) {
-            grid_expand<4>(F, T, cur, gen, learned);
+            stamp(pass, 0);
+            // few entries per warp: short batches; many: eight per lane in flight
+            if (T <= 64u * (g.size() >> 5)) grid_expand<2>(F, T, cur, gen, learned);
+            else grid_expand<kExpandU>(F, T, cur, gen, learned);
+            stamp(pass, 1);
+            g.sync_snap(&c->n_props, nullptr);
+            const std::uint32_t np = g.snap[0];
+            stamp(pass, 2);
+            grid_resolve(gen, np);
+            stamp(pass, 3);
             g.sync();
-            mark(2);
-            grid_resolve(gen);
-            g.sync();
-            mark(3);
-            grid_select(level, dlev);
-            g.sync();
-            mark(4);
+            stamp(pass, 4);
+            grid_select(level, dlev, np);
+            stamp(pass, 5);
+            g.sync_snap(&c->n_confl, nullptr);
+            stamp(pass, 6);
             // final for this pass: no block bumps it before the pass barrier
-            const std::uint32_t nconf = *reinterpret_cast<volatile std::uint32_t*>(&c->n_confl);
+            const std::uint32_t nconf = g.snap[0];
             std::uint32_t Fn = 0, Tn = 0;
             const bool small = (T + 31) / 32 <= kBlockPlaceWords;
             grid_place(T, cur ^ 1u, ts, Fn, Tn);
@@ -1317,12 +1477,19 @@ struct Search {
                 c->n_props = 0;  // every block read it before the select barrier
                 c->st.passes += 1;
             }
-            g.sync();
-            mark(5);
+            stamp(pass, 7);
             if (small) {
-                Fn = *reinterpret_cast<volatile std::uint32_t*>(&c->F);
-                Tn = *reinterpret_cast<volatile std::uint32_t*>(&c->T);
+                g.sync_snap(&c->F, &c->T);
+                Fn = g.snap[0];
+                Tn = g.snap[1];
+            } else {
+                g.sync();
             }
+            stamp(pass, 8);
+            if (C.ptrace && g.leader() && pass < kPtracePasses)
+                C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x) * kPtraceStamps + 9] =
+                    (static_cast<unsigned long long>(T) << 32) | F;
+            ++pass;
             if (g.leader()) c->st.propagations += Fn;
             ts += Fn;
             F = Fn;
@@ -1376,34 +1543,8 @@ struct Search {
         }
     }
 
-    __device__ static unsigned long long clk_after(std::uint32_t v) {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t) : "r"(v) : "memory");
-        return t;
-    }
-    __device__ static unsigned long long clk_now() {
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
-        return t;
-    }
-
     // Warp-synchronous passes while they stay small (called by warp 0 only).
     __device__ void small_passes(std::uint32_t level) {
-        if (threadIdx.x == 0 && c->F > 0) {  // latency probe on real data (profiling only)
-            const std::uint32_t li = lidx(sm.fr()[0]);
-            const unsigned long long a0 = clk_now();
-            const std::uint32_t v0 = __ldg(S.occ_off + li * 4);
-            const unsigned long long a1 = clk_after(v0);
-            const int4 e0 = __ldg(S.occ + v0);
-            const unsigned long long a2 = clk_after(static_cast<std::uint32_t>(e0.x));
-            const std::int32_t cv = sl.cells()[atom_of(e0.z) + (e0.x & 0)];
-            const unsigned long long a3 = clk_after(static_cast<std::uint32_t>(cv));
-            const std::uint32_t v1 = __ldg(S.occ_off + li * 4 + (cv & 0));
-            const unsigned long long a4 = clk_after(v1);
-            c->prof[11] += a1 - a0;
-            c->prof[14] += a2 - a1;
-            c->prof[15] += (a3 - a2) + ((a4 - a3) << 32);
-        }
         for (;;) {
             __syncwarp();
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
@@ -1594,7 +1735,7 @@ struct Search {
             std::int32_t other[2] = {0, 0};
             for (std::uint32_t q = 0, n = 0; q < len && n < 2; ++q)
                 if (q != j) other[n++] = lits[q];
-            sl.larena()[h3[0] + h3[1]] = make_int4(static_cast<std::int32_t>(id), static_cast<std::int32_t>(kNone),
+            sl.larena()[h3[0] + h3[1]] = make_int4(static_cast<std::int32_t>(id | cls << 30), static_cast<std::int32_t>(kNone),
                                                    other[0], other[1]);
             h3[1] += 1;
             sl.ltot()[li] += 1;
@@ -1856,10 +1997,10 @@ struct Search {
             for (std::uint32_t cl = 0; cl < 4; ++cl) {
                 const std::uint32_t lo = __ldg(S.occ_off + li * 4 + cl), hi = __ldg(S.occ_off + li * 4 + cl + 1);
                 for (std::uint32_t j = lo; j < hi; ++j)
-                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ + j).x))));
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(__ldg(S.occ + j).x) & 0x3fffffffu)));
                 const std::uint32_t* h = sl.lhdr() + 3 * (li * 4 + cl);
                 for (std::uint32_t j = 0; j < h[1]; ++j)
-                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena()[h[0] + j].x))));
+                    s += ldexp(1.0, -static_cast<int>(length_of(static_cast<std::uint32_t>(sl.larena()[h[0] + j].x) & 0x3fffffffu)));
             }
         return s;
     }
@@ -2228,9 +2369,10 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ std::uint32_t si[BS / 32];
     const Slot sl{L.base, &L};
     __shared__ unsigned long long gcnt[4];
-    __shared__ std::uint32_t gwsm[BS / 32 * 64];
+    __shared__ std::uint32_t gsnap[4];
+    __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gwsm};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq};
     if (g.leader() && sl.ctl()->status == kYield) sl.ctl()->status = kRunning;
     g.sync();
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
@@ -2379,9 +2521,10 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ std::uint32_t si[BS / 32];
     const Slot sl{L.base, &L};
     __shared__ unsigned long long gcnt[4];
-    __shared__ std::uint32_t gwsm[BS / 32 * 64];
+    __shared__ std::uint32_t gsnap[4];
+    __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gwsm};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq};
     do_op(g, S, C, sl, K, sh, op, Sm{&smc});
     g.persist();
 }

@@ -76,6 +76,9 @@ public:
     void seed(const std::int32_t* lits, std::size_t n);
     std::int32_t add_learned(const std::vector<std::int32_t>& lits);
     void set_count_lits(bool on);
+    // diagnostics: per-pass x per-block phase timestamps of grid propagations
+    void set_pass_trace(bool on);
+    std::vector<unsigned long long> pass_trace(std::uint32_t& blocks) const;
 
     // read back
     const dev::Ctl& ctl() const;  // synchronises with the session's stream

@@ -138,6 +138,7 @@ struct Arena {
         L.o_mcube = take(4ull * mcap);
         L.o_tbuf = take(16ull * tcap);
         L.o_occat = take(grid_blocks ? 4 * tbits : 0);  // whole-grid passes only
+        L.o_gmirror = take(grid_blocks ? 4 * ((A1 + 15) / 16 + 1) : 0);
         L.bytes = o;
         L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
         ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
@@ -501,6 +502,19 @@ std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
 
 void Session::set_count_lits(bool on) { impl_->cfg.count_lits = on ? 1u : 0u; }
 
+void Session::set_pass_trace(bool on) {
+    Impl& im = *impl_;
+    const std::size_t n = 64ull * std::max<std::uint32_t>(1, im.gblocks) * 10;
+    if (on && !im.cfg.ptrace) {
+        ck(cudaMalloc(&im.cfg.ptrace, n * sizeof(unsigned long long)), "cudaMalloc trace");
+        ck(cudaMemset(im.cfg.ptrace, 0, n * sizeof(unsigned long long)), "memset trace");
+        im.ar.owned.push_back(im.cfg.ptrace);
+    } else if (!on) {
+        im.cfg.ptrace = nullptr;  // freed with the arena
+    }
+}
+
+
 const dev::Ctl& Session::ctl() const {
     if (impl_->ctl_pending) {
         ck(cudaStreamSynchronize(impl_->stream), "stream");
@@ -544,6 +558,13 @@ std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots
 std::vector<std::int32_t> Session::frontier() const {
     const dev::Ctl& c = ctl();
     return dl(impl_->ar.slots[0].fr(c.cur), c.F, impl_->stream);
+}
+
+std::vector<unsigned long long> Session::pass_trace(std::uint32_t& blocks) const {
+    blocks = std::max<std::uint32_t>(1, impl_->gblocks);
+    if (!impl_->cfg.ptrace) return {};
+    ctl();
+    return dl(impl_->cfg.ptrace, 64ull * blocks * 10, impl_->stream);
 }
 
 }  // namespace yas

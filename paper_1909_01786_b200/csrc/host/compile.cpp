@@ -202,7 +202,7 @@ StaticStore build_store(const std::vector<Nogood>& nogoods, AtomId total_atoms) 
             std::int32_t other[2] = {0, 0};
             for (std::uint32_t q = st.off[id], n = 0; q < st.off[id + 1] && n < 2; ++q)
                 if (q != k) other[n++] = st.pool[q];
-            st.occ_fat[4 * at + 0] = static_cast<std::int32_t>(id);
+            st.occ_fat[4 * at + 0] = static_cast<std::int32_t>(id | cls << 30);  // class in the top bits
             st.occ_fat[4 * at + 1] = static_cast<std::int32_t>(st.guard[id]);
             st.occ_fat[4 * at + 2] = other[0];
             st.occ_fat[4 * at + 3] = other[1];

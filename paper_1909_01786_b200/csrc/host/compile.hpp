@@ -78,8 +78,9 @@ struct StaticStore {
     std::vector<std::uint32_t> occ_off;  // (2A+2)*4 + 1
     std::vector<std::int32_t> occ_ids;
     // Device copy of the occurrence lists: per (literal, nogood) one 16-byte
-    // entry {id, guard, x, y} with x, y two *other* literals of the nogood
-    // (0 when absent), so binary/ternary nogoods are decided from the entry.
+    // entry {id | length_class << 30, guard, x, y} with x, y two *other*
+    // literals of the nogood (0 when absent), so binary/ternary nogoods are
+    // decided from the entry. Nogood ids therefore stay below 2^30.
     std::vector<std::int32_t> occ_fat;  // 4 ints per occurrence, same order as occ_ids
     std::array<std::uint32_t, 4> bounds{0, 0, 0, 0};
 

@@ -20,20 +20,15 @@ print(f"store built in {time.perf_counter() - t:.2f}s, seeded {len(seeded)}")
 prop = Y.Propagator(store, 16, engine="grid")
 sd = np.asarray(seeded, dtype=np.int32)
 fr = np.asarray([dec] + seeded, dtype=np.int32)
-names = ["-", "offsets", "expand+eval", "resolve", "select", "place"]
 for r in range(reps):
     t0 = time.perf_counter()
     prop.reset(); prop.push_decision(dec); prop.assign_propagated(sd, 2); prop.seed(fr)
     t1 = time.perf_counter()
-    p0 = prop.profile()
     o = prop.propagate_and_check(2)
     t2 = time.perf_counter()
     tr = prop.trail_array()
     t3 = time.perf_counter()
-    p1 = prop.profile()
-    d = [b - a for a, b in zip(p0, p1)]
-    tot = sum(d[1:6]) or 1
-    split = " ".join(f"{names[k]}={d[k] / 1.965e3:.1f}us" for k in range(1, 6))
+    split = ""
     print(f"rep {r}: kernel {o.device_ms * 1e3:.1f}us passes={o.passes} checks={o.checks} viol={o.violated} "
           f"trail={len(tr)} | {split} | host: prepare {1e3 * (t1 - t0):.2f}ms propagate {1e3 * (t2 - t1):.2f}ms "
           f"trail {1e3 * (t3 - t2):.2f}ms")

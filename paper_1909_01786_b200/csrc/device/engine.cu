@@ -632,6 +632,48 @@ struct Search {
     __device__ void write_deps_from(const std::int32_t* L, std::uint32_t len, std::uint32_t id, std::uint32_t a,
                                     std::uint32_t level) const {
         const std::uint32_t nw = nwords(level);
+        if (len <= 8) {
+            // literals, then cells + overflow bytes, then 4 Deps words of every
+            // contributing literal per sweep: 2 + ceil(nw/4) round trips
+            std::int32_t l[8];
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) l[k] = k < len ? lit_at(L, k, id) : 0;
+            std::uint32_t x[8];
+            bool on[8];
+            std::uint8_t ov[8];
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) {
+                x[k] = atom_of(l[k]);
+                const std::int32_t cv = sl.cells()[x[k]];
+                ov[k] = sl.dovf()[x[k]];
+                on[k] = k < len && x[k] != a && lvl_of(cv) > 1;
+            }
+            std::uint8_t ovf = 0;
+#pragma unroll
+            for (std::uint32_t k = 0; k < 8; ++k) {
+                ovf |= on[k] ? ov[k] : 0;
+                x[k] = on[k] ? x[k] : 0u;  // atom 0: a valid, never-set row
+            }
+            for (std::uint32_t w0 = 0; w0 < nw; w0 += 2) {
+                const std::uint32_t w1 = w0 + 1 < nw ? w0 + 1 : w0;
+                unsigned long long d0[8], d1[8];  // unconditional loads, all in flight together
+#pragma unroll
+                for (std::uint32_t k = 0; k < 8; ++k) {
+                    d0[k] = dep(w0, x[k]);
+                    d1[k] = dep(w1, x[k]);
+                }
+                unsigned long long a0 = 0, a1 = 0;
+#pragma unroll
+                for (std::uint32_t k = 0; k < 8; ++k) {
+                    a0 |= d0[k];
+                    a1 |= d1[k];
+                }
+                dep(w0, a) = a0;
+                if (w0 + 1 < nw) dep(w0 + 1, a) = a1;
+            }
+            sl.dovf()[a] = ovf;
+            return;
+        }
         std::uint8_t ovf = 0;
         for (std::uint32_t w0 = 0; w0 < nw; w0 += 4) {  // 4 words per sweep: independent loads
             unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
@@ -1297,18 +1339,49 @@ struct Search {
     // conflict (assignment.cpp:116-124).
     __device__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np) {
         const int4* props = sl.props();
+        const bool one_word = nwords(dlev) == 1;
         for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
             const int4 p = props[i];
             const std::uint32_t e = static_cast<std::uint32_t>(p.z);
             const std::uint32_t a = atom_of(p.y);
+            const std::uint32_t id = static_cast<std::uint32_t>(p.x);
+            // everything that depends only on the proposal, in one round trip
             const unsigned long long w = sl.win()[a];
+            const std::uint32_t li = lidx(p.y);
+            const std::uint32_t ob = __ldg(S.occ_off + li * 4), oe = __ldg(S.occ_off + li * 4 + 4), lt = sl.ltot()[li];
+            std::uint32_t len;
+            const std::int32_t* L = lits_of(id, len);
             if ((static_cast<std::uint32_t>(w) >> 1) == e) {
                 set_cell(a, p.y > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
                 sl.reason()[a] = p.x;
-                std::uint32_t len;
-                const std::int32_t* L = lits_of(static_cast<std::uint32_t>(p.x), len);
-                write_deps_from(L, len, static_cast<std::uint32_t>(p.x), a, dlev);
-                sl.occat()[e] = occ_total(lidx(p.y));
+                if (one_word && len <= 8) {  // literals, then their cells / Deps / overflow: two round trips
+                    std::int32_t l[8];
+#pragma unroll
+                    for (std::uint32_t k = 0; k < 8; ++k) l[k] = k < len ? lit_at(L, k, id) : 0;
+                    std::int32_t cv[8];
+                    unsigned long long dv[8];
+                    std::uint8_t ov[8];
+#pragma unroll
+                    for (std::uint32_t k = 0; k < 8; ++k) {
+                        const std::uint32_t x = atom_of(l[k]);
+                        cv[k] = sl.cells()[x];
+                        dv[k] = dep(0, x);
+                        ov[k] = sl.dovf()[x];
+                    }
+                    unsigned long long acc = 0;
+                    std::uint8_t ovf = 0;
+#pragma unroll
+                    for (std::uint32_t k = 0; k < 8; ++k)
+                        if (k < len && atom_of(l[k]) != a && lvl_of(cv[k]) > 1) {
+                            acc |= dv[k];
+                            ovf |= ov[k];
+                        }
+                    dep(0, a) = acc;
+                    sl.dovf()[a] = ovf;
+                } else {
+                    write_deps_from(L, len, id, a, dlev);
+                }
+                sl.occat()[e] = oe - ob + lt;
                 sl.litat()[e] = p.y;
                 atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
             } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull)) {
@@ -1550,8 +1623,98 @@ struct Search {
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
             __syncwarp();
             if (viol || F == 0 || T > kWarpPassT || F + 1 > sm.fcap()) return;
-            pass_smem(F, T, cur, level);
+            if (T <= 32) tiny_pass(F, T, cur, level);
+            else pass_smem(F, T, cur, level);
         }
+    }
+
+    // A whole pass with one expansion entry per lane (T <= 32; warp 0 of a
+    // single-CTA search). Register-level replacements for the shared-memory
+    // machinery of pass_smem: duplicate nogoods by __match_any_sync on the id
+    // (the lowest lane has the smallest e, i.e. comes first in item order),
+    // per-atom winners by __match_any_sync on the proposed atom (lowest lane =
+    // smallest key), positions by ballot prefix counts and one warp scan.
+    __device__ void tiny_pass(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
+        const std::uint32_t lane = lane_id();
+        const unsigned below = (1u << lane) - 1u;
+        const bool act = lane < T;
+        const bool learned = c->learned_n > 0;
+        const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
+        std::uint32_t lo = 0, hi = F;  // frontier literal of entry e = lane
+        while (hi - lo > 1) {
+            const std::uint32_t mid = (lo + hi) >> 1;
+            if (sm.froff()[mid] <= lane) lo = mid; else hi = mid;
+        }
+        const std::int32_t trig = sm.fr()[lo];
+        std::uint32_t cls = 0;
+        const int4 ent = act ? occ_entry(lidx(trig), lane - sm.froff()[lo], learned, cls) : make_int4(-1, 0, 0, 0);
+        const std::int32_t id = ent.x;
+        const unsigned same = __match_any_sync(0xffffffffu, act ? id : -2 - static_cast<std::int32_t>(lane));
+        const bool first = act && static_cast<std::uint32_t>(__ffs(same) - 1) == lane;
+        bool conflict = false, prop = false;
+        std::int32_t plit = 0;
+        std::uint32_t clen = 0, meta = 0;
+        unsigned long long d0 = 0;
+        if (first) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
+        // winner per proposed atom: the lowest proposing lane
+        const std::uint32_t pa = atom_of(plit);
+        const unsigned grp = __match_any_sync(0xffffffffu, prop ? static_cast<std::int32_t>(pa) : -2 - static_cast<std::int32_t>(lane));
+        const std::uint32_t wl = static_cast<std::uint32_t>(__ffs(grp) - 1);
+        const std::int32_t wlit = __shfl_sync(0xffffffffu, plit, wl);
+        const bool winner = prop && wl == lane;
+        const bool lose = prop && !winner && ((wlit < 0) != (plit < 0));
+        const unsigned cm = __ballot_sync(0xffffffffu, conflict || lose);
+        const unsigned wm = __ballot_sync(0xffffffffu, winner);
+        const std::uint32_t nchk = __popc(__ballot_sync(0xffffffffu, first));
+        const std::uint32_t nlit = __reduce_add_sync(0xffffffffu, clen);
+        const std::uint32_t nc0 = c->n_confl, ts0 = c->ts;
+        if (cm >> lane & 1u) sl.confl()[nc0 + __popc(cm & below)] = id;
+        const std::uint32_t occ = winner ? (meta & 0x7fffffffu) : 0u;
+        std::uint32_t oinc = occ;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const std::uint32_t o = __shfl_up_sync(0xffffffffu, oinc, d);
+            if (lane >= static_cast<std::uint32_t>(d)) oinc += o;
+        }
+        const std::uint32_t cnt = __popc(wm), tnext = __shfl_sync(0xffffffffu, oinc, 31);
+        const std::uint32_t dst = cur ^ 1u;
+        if (winner) {
+            set_cell(pa, plit > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
+            sl.reason()[pa] = id;
+            if (nwords(dlev) == 1) {
+                dep(0, pa) = d0;
+                sl.dovf()[pa] = static_cast<std::uint8_t>(meta >> 31);
+            } else {
+                std::uint32_t len;
+                const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
+                write_deps_from(L, len, static_cast<std::uint32_t>(id), pa, dlev);
+            }
+            const std::uint32_t r = __popc(wm & below);
+            sl.fr(dst)[r] = plit;
+            sl.froff()[r] = oinc - occ;
+            sm.fr()[r] = plit;
+            sm.froff()[r] = oinc - occ;
+            sl.trail()[ts0 + r] = plit;
+            sl.tpos()[pa] = ts0 + r;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            sl.froff()[cnt] = tnext;
+            sm.froff()[cnt] = tnext;
+            c->st.checks += nchk;
+            c->st.checked_lits += nlit;
+            c->n_confl = nc0 + __popc(cm);
+            c->ts = ts0 + cnt;
+            c->F = cnt;
+            c->T = tnext;
+            c->st.propagations += cnt;
+            c->n_props = 0;
+            c->st.passes += 1;
+            c->cur = dst;
+            c->b[11] = c->n_confl > 0 ? 1u : 0u;
+            c->gen += 1;
+        }
+        __syncwarp();
     }
 
     // Initial propagation (propagate.cpp:23-47): static units in compile order
@@ -2009,15 +2172,49 @@ struct Search {
     __device__ void decide_or_complete() {
         double best = -1.0;
         std::uint32_t bi = 0xffffffffu;
-        for (std::uint32_t r = g.tid(); r < S.R; r += g.size()) {
-            const uint4 ru = __ldg(S.rules + r);
-            if (ru.w >> 31) continue;
-            const std::uint32_t n = ru.w & 0x7fffffffu;
-            if (val(ru.x) != 0) continue;
-            if (ru.z != 0 && val(ru.z) <= 0) continue;
-            if (n != 0 && val(n) < 0) continue;
-            const double s = score(ru.x);
-            if (better(s, r, best, bi)) { best = s; bi = r; }
+        // find_applicable + score (decide.cpp:43-79): DU rules per thread per
+        // step, every load of a step issued before any is used
+        constexpr int DU = 8;
+        const std::uint32_t gs = g.size();
+        for (std::uint32_t r0 = g.tid(); r0 < S.R; r0 += DU * gs) {
+            uint4 ru[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                const std::uint32_t r = r0 + k * gs;
+                ru[k] = r < S.R ? __ldg(S.rules + r) : make_uint4(0u, 0u, 0u, 0x80000000u);
+            }
+            bool app[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                const std::uint32_t n = ru[k].w & 0x7fffffffu;
+                app[k] = !(ru[k].w >> 31) && val(ru[k].x) == 0 && (ru[k].z == 0 || val(ru[k].z) > 0) &&
+                         (n == 0 || val(n) >= 0);
+            }
+            if (C.heur == 0) {  // occurrence count: 2 x (two offsets + learned count) per head
+                std::uint32_t o[DU][6];
+#pragma unroll
+                for (int k = 0; k < DU; ++k) {
+                    const std::uint32_t h = app[k] ? ru[k].x : 0u;
+                    o[k][0] = __ldg(S.occ_off + 8 * h);
+                    o[k][1] = __ldg(S.occ_off + 8 * h + 4);
+                    o[k][2] = sl.ltot()[2 * h];
+                    o[k][3] = __ldg(S.occ_off + 8 * h + 4);
+                    o[k][4] = __ldg(S.occ_off + 8 * h + 8);
+                    o[k][5] = sl.ltot()[2 * h + 1];
+                }
+#pragma unroll
+                for (int k = 0; k < DU; ++k) {
+                    const double sc = static_cast<double>(o[k][1] - o[k][0] + o[k][2] + o[k][4] - o[k][3] + o[k][5]);
+                    if (app[k] && better(sc, r0 + k * gs, best, bi)) { best = sc; bi = r0 + k * gs; }
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < DU; ++k) {
+                    if (!app[k]) continue;
+                    const double sc = score(ru[k].x);
+                    if (better(sc, r0 + k * gs, best, bi)) { best = sc; bi = r0 + k * gs; }
+                }
+            }
         }
         g.argmax(best, bi);
         if (bi != 0xffffffffu) {

@@ -100,6 +100,7 @@ struct WarpG {
     __device__ std::uint32_t tid() const { return lane_id(); }
     __device__ std::uint32_t size() const { return 32; }
     __device__ bool leader() const { return threadIdx.x == 0; }
+    __device__ bool leader_warp() const { return true; }
     __device__ void sync() { __syncwarp(); }
     __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
         const unsigned long long inc = warp_incl_scan(v);
@@ -131,6 +132,7 @@ struct BlockG {
     __device__ std::uint32_t tid() const { return threadIdx.x; }
     __device__ std::uint32_t size() const { return BS; }
     __device__ bool leader() const { return threadIdx.x == 0; }
+    __device__ bool leader_warp() const { return threadIdx.x < 32; }
     __device__ void sync() { __syncthreads(); }
 
     // Exclusive scan of one value per thread over the whole group.
@@ -202,6 +204,7 @@ struct GridG {
     __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
     __device__ std::uint32_t size() const { return gridDim.x * BS; }
     __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
+    __device__ bool leader_warp() const { return blockIdx.x == 0 && threadIdx.x < 32; }
     // Block-interleaved numbering: consecutive ids land on different SMs, so
     // a small amount of work is spread over the whole GPU.
     __device__ std::uint32_t itid() const { return threadIdx.x * gridDim.x + blockIdx.x; }
@@ -597,8 +600,53 @@ struct Search {
         const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
         return nw < C.W ? nw : C.W;
     }
+    // Deps rows are atom-major: the words of one atom are contiguous (row
+    // stride rounded up to an even word count for 16-byte vector access).
+    __device__ std::uint32_t dstride() const { return (C.W + 1u) & ~1u; }
     __device__ unsigned long long& dep(std::uint32_t w, std::uint32_t a) const {
-        return sl.deps()[static_cast<std::size_t>(w) * (S.A + 1) + a];
+        return sl.deps()[static_cast<std::size_t>(a) * dstride() + w];
+    }
+    // OR words [w0, w0 + 2*NQ) of the Deps rows of atoms x[k] (on[k]) into
+    // acc, as 16-byte loads all issued before any is used.
+    template <int NK, int NQ>
+    __device__ void or_rows(const std::uint32_t* x, const bool* on, std::uint32_t w0, std::uint32_t nw,
+                            unsigned long long* acc) const {
+        ulonglong2 v[NK][NQ];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
+            const ulonglong2* row = reinterpret_cast<const ulonglong2*>(sl.deps() + static_cast<std::size_t>(on[k] ? x[k] : 0u) * dstride() + w0);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) v[k][q] = (on[k] && w0 + 2 * q < nw) ? row[q] : make_ulonglong2(0ull, 0ull);
+        }
+#pragma unroll
+        for (int k = 0; k < NK; ++k)
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                acc[2 * q] |= v[k][q].x;
+                acc[2 * q + 1] |= v[k][q].y;
+            }
+    }
+    template <int NQ>
+    __device__ void store_row(std::uint32_t a, std::uint32_t w0, std::uint32_t nw, const unsigned long long* acc) const {
+        ulonglong2* row = reinterpret_cast<ulonglong2*>(sl.deps() + static_cast<std::size_t>(a) * dstride() + w0);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (w0 + 2 * q < nw) {
+                if (w0 + 2 * q + 1 < nw) row[q] = make_ulonglong2(acc[2 * q], acc[2 * q + 1]);
+                else reinterpret_cast<unsigned long long*>(row)[2 * q] = acc[2 * q];
+            }
+    }
+    // Deps of atom a from the rows of up to two contributing atoms.
+    __device__ void deps_from_pair(std::uint32_t a, std::uint32_t x0, bool on0, std::uint32_t x1, bool on1,
+                                   std::uint32_t nw) const {
+        const std::uint32_t xs[2] = {x0, x1};
+        const bool ons[2] = {on0, on1};
+        for (std::uint32_t w0 = 0; w0 < nw; w0 += 8) {
+            unsigned long long acc[8] = {0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
+            or_rows<2, 4>(xs, ons, w0, nw, acc);
+            store_row<4>(a, w0, nw, acc);
+        }
+        sl.dovf()[a] = static_cast<std::uint8_t>((on0 ? sl.dovf()[x0] : 0) | (on1 ? sl.dovf()[x1] : 0));
     }
     __device__ bool holds(std::int32_t l) const {
         const int v = val(atom_of(l));
@@ -650,26 +698,12 @@ struct Search {
             }
             std::uint8_t ovf = 0;
 #pragma unroll
-            for (std::uint32_t k = 0; k < 8; ++k) {
-                ovf |= on[k] ? ov[k] : 0;
-                x[k] = on[k] ? x[k] : 0u;  // atom 0: a valid, never-set row
-            }
-            for (std::uint32_t w0 = 0; w0 < nw; w0 += 2) {
-                const std::uint32_t w1 = w0 + 1 < nw ? w0 + 1 : w0;
-                unsigned long long d0[8], d1[8];  // unconditional loads, all in flight together
-#pragma unroll
-                for (std::uint32_t k = 0; k < 8; ++k) {
-                    d0[k] = dep(w0, x[k]);
-                    d1[k] = dep(w1, x[k]);
-                }
-                unsigned long long a0 = 0, a1 = 0;
-#pragma unroll
-                for (std::uint32_t k = 0; k < 8; ++k) {
-                    a0 |= d0[k];
-                    a1 |= d1[k];
-                }
-                dep(w0, a) = a0;
-                if (w0 + 1 < nw) dep(w0 + 1, a) = a1;
+            for (std::uint32_t k = 0; k < 8; ++k) ovf |= on[k] ? ov[k] : 0;
+            for (std::uint32_t w0 = 0; w0 < nw; w0 += 4) {
+                unsigned long long acc[4] = {0ull, 0ull, 0ull, 0ull};
+                or_rows<4, 2>(x, on, w0, nw, acc);
+                or_rows<4, 2>(x + 4, on + 4, w0, nw, acc);
+                store_row<2>(a, w0, nw, acc);
             }
             sl.dovf()[a] = ovf;
             return;
@@ -1623,9 +1657,59 @@ struct Search {
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
             __syncwarp();
             if (viol || F == 0 || T > kWarpPassT || F + 1 > sm.fcap()) return;
-            if (T <= 32) tiny_pass(F, T, cur, level);
-            else pass_smem(F, T, cur, level);
+            if (T <= 32) {
+                tiny_pass(F, T, cur, level);
+                mark(8);
+            } else {
+                pass_smem(F, T, cur, level);
+                mark(9);
+            }
         }
+    }
+
+    // evaluate() of one nogood by the whole warp (results uniform): 32
+    // literals per step, free/dead detection by ballot, Deps word 0 of the
+    // proposal by OR-reduction (propagate.cpp:86-168, :49-62).
+    __device__ void w_evaluate(std::uint32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
+                               unsigned long long& d0, std::uint32_t& meta) const {
+        const std::uint32_t lane = lane_id();
+        const std::uint32_t guard = guard_of(id);
+        const std::int32_t* L = lits_of(id, len);
+        conflict = prop = false;
+        plit = 0;
+        d0 = 0;
+        meta = 0;
+        std::uint32_t nfree = 0;
+        std::int32_t u1 = 0;
+        for (std::uint32_t k0 = 0; k0 < len; k0 += 32) {
+            const std::uint32_t k = k0 + lane;
+            const std::int32_t l = k < len ? lit_at(L, k, id) : 0;
+            const int v = k < len ? val(atom_of(l)) : 1;
+            if (__any_sync(0xffffffffu, k < len && v != 0 && (v > 0) != (l > 0))) return;  // satisfied
+            const unsigned fm = __ballot_sync(0xffffffffu, k < len && v == 0);
+            if (fm && nfree == 0) u1 = __shfl_sync(0xffffffffu, l, __ffs(fm) - 1);
+            nfree += __popc(fm);
+            if (nfree >= 2) return;
+        }
+        if (nfree == 0) {
+            conflict = true;
+            return;
+        }
+        if (!may_assert(guard, -u1)) return;
+        prop = true;
+        plit = -u1;
+        const std::uint32_t ua = atom_of(u1);
+        unsigned long long acc = 0;
+        std::uint32_t ov = 0;
+        for (std::uint32_t k = lane; k < len; k += 32) {
+            const std::uint32_t x = atom_of(lit_at(L, k, id));
+            if (x == ua || lvl_of(sl.cells()[x]) <= 1) continue;
+            acc |= dep(0, x);
+            ov |= sl.dovf()[x];
+        }
+        d0 = w_or64(acc);
+        ov = __reduce_or_sync(0xffffffffu, ov);
+        meta = occ_total(lidx(plit)) | (ov ? 0x80000000u : 0u);
     }
 
     // A whole pass with one expansion entry per lane (T <= 32; warp 0 of a
@@ -1655,7 +1739,32 @@ struct Search {
         std::int32_t plit = 0;
         std::uint32_t clen = 0, meta = 0;
         unsigned long long d0 = 0;
-        if (first) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
+        // long nogoods the two literals in the entry cannot decide are scanned
+        // by the whole warp, one at a time
+        bool full = false;
+        if (first && cls == 3) {
+            const int vx = val(atom_of(ent.z)), vy = val(atom_of(ent.w));
+            const int sx = vx == 0 ? 0 : ((vx > 0) == (ent.z > 0) ? 1 : -1);
+            const int sy = vy == 0 ? 0 : ((vy > 0) == (ent.w > 0) ? 1 : -1);
+            full = !(sx < 0 || sy < 0 || (sx == 0 && sy == 0));
+        }
+        if (first && !full) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
+        for (unsigned need = __ballot_sync(0xffffffffu, full); need; need &= need - 1) {
+            const std::uint32_t src = static_cast<std::uint32_t>(__ffs(need) - 1);
+            bool cf, pr;
+            std::int32_t pl;
+            std::uint32_t ln, mt;
+            unsigned long long dd;
+            w_evaluate(static_cast<std::uint32_t>(__shfl_sync(0xffffffffu, id, src)), cf, pr, pl, ln, dd, mt);
+            if (lane == src) {
+                conflict = cf;
+                prop = pr;
+                plit = pl;
+                clen = ln;
+                d0 = dd;
+                meta = mt;
+            }
+        }
         // winner per proposed atom: the lowest proposing lane
         const std::uint32_t pa = atom_of(plit);
         const unsigned grp = __match_any_sync(0xffffffffu, prop ? static_cast<std::int32_t>(pa) : -2 - static_cast<std::int32_t>(lane));
@@ -1684,6 +1793,10 @@ struct Search {
             if (nwords(dlev) == 1) {
                 dep(0, pa) = d0;
                 sl.dovf()[pa] = static_cast<std::uint8_t>(meta >> 31);
+            } else if (cls == 1 || cls == 2) {  // the other literals are the trigger and the entry's blocker
+                const std::uint32_t x0 = atom_of(trig);
+                const std::uint32_t x1 = cls == 2 ? atom_of(pa == atom_of(ent.z) ? ent.w : ent.z) : 0u;
+                deps_from_pair(pa, x0, lvl_of(sl.cells()[x0]) > 1, x1, x1 != 0 && lvl_of(sl.cells()[x1]) > 1, nwords(dlev));
             } else {
                 std::uint32_t len;
                 const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
@@ -1822,233 +1935,345 @@ struct Search {
         g.sync();
     }
 
-    // ---- leader-only sequential pieces ---------------------------------------
-    __device__ void sort_by_atom(std::int32_t* v, std::uint32_t n) const {
-        // heapsort keyed by atom id (Nogood::make order; one sign per atom here)
-        auto key = [](std::int32_t x) { return atom_of(x); };
-        auto sift = [&](std::uint32_t root, std::uint32_t end) {
-            for (;;) {
-                std::uint32_t ch = 2 * root + 1;
-                if (ch >= end) return;
-                if (ch + 1 < end && key(v[ch + 1]) > key(v[ch])) ++ch;
-                if (key(v[root]) >= key(v[ch])) return;
-                const std::int32_t t = v[root]; v[root] = v[ch]; v[ch] = t;
-                root = ch;
-            }
-        };
-        for (std::uint32_t i = n / 2; i-- > 0;) sift(i, n);
-        for (std::uint32_t end = n; end > 1; --end) {
-            const std::int32_t t = v[0]; v[0] = v[end - 1]; v[end - 1] = t;
-            sift(0, end - 1);
+    // ---- conflict analysis and learning: one warp (the leader's) --------------
+    // The paper's Learning / fwd-learning kernels as warp code:
+    // literal sets are spread over the lanes, maxima / OR-reductions /
+    // compactions are warp collectives, so a step costs one memory round trip
+    // instead of one per literal. All functions are called by all 32 lanes.
+    __device__ static unsigned long long w_or64(unsigned long long v) {
+        const std::uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<std::uint32_t>(v));
+        const std::uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<std::uint32_t>(v >> 32));
+        return (static_cast<unsigned long long>(hi) << 32) | lo;
+    }
+    __device__ static unsigned long long w_min64(unsigned long long v) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+            v = o < v ? o : v;
         }
+        return v;
+    }
+    __device__ static unsigned long long w_max64(unsigned long long v) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+            v = o > v ? o : v;
+        }
+        return v;
+    }
+    __device__ static unsigned long long w_add64(unsigned long long v) {
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+        return v;
+    }
+    __device__ std::int32_t* sortbuf() const { return sl.scratch() + S.A + 256; }
+
+    // Sort v[0..n) by atom (Nogood::make order; atoms are distinct) by rank.
+    __device__ void w_sort(std::int32_t* v, std::uint32_t n) const {
+        const std::uint32_t lane = lane_id();
+        if (n <= 32) {
+            const std::int32_t x = lane < n ? v[lane] : 0;
+            const std::uint32_t ka = lane < n ? atom_of(x) : 0xffffffffu;
+            std::uint32_t r = 0;
+            for (std::uint32_t s2 = 0; s2 < n; ++s2) r += __shfl_sync(0xffffffffu, ka, s2) < ka;
+            __syncwarp();
+            if (lane < n) v[r] = x;
+            __syncwarp();
+            return;
+        }
+        std::int32_t* tmp = sortbuf();
+        for (std::uint32_t i = lane; i < n; i += 32) {
+            const std::int32_t x = v[i];
+            const std::uint32_t ka = atom_of(x);
+            std::uint32_t r = 0;
+#pragma unroll 8
+            for (std::uint32_t j = 0; j < n; ++j) r += atom_of(v[j]) < ka;
+            tmp[r] = x;
+        }
+        __syncwarp();
+        for (std::uint32_t i = lane; i < n; i += 32) v[i] = tmp[i];
+        __syncwarp();
     }
 
     // NogoodStore::add_learned (nogood_store.cpp:81-107). Returns id or -1.
-    __device__ std::int32_t add_learned(const std::int32_t* lits, std::uint32_t len, bool count_capacity = true) {
-        if (count_capacity && c->learned_n >= C.learned_capacity) {
-            c->status = kErrCapacity;
-            return -1;
-        }
-        if (c->learned_n >= K.lcap || c->lpool_used + len > K.lpool) {
-            c->status = kErrArena;
+    __device__ std::int32_t w_add_learned(const std::int32_t* lits, std::uint32_t len, bool count_capacity = true) {
+        const std::uint32_t lane = lane_id();
+        if ((count_capacity && c->learned_n >= C.learned_capacity) || c->learned_n >= K.lcap ||
+            c->lpool_used + len > K.lpool) {
+            __syncwarp();
+            if (lane == 0) c->status = (count_capacity && c->learned_n >= C.learned_capacity) ? kErrCapacity : kErrArena;
+            __syncwarp();
             return -1;
         }
         // duplicate census (learned_seen_, nogood_store.cpp:87-89)
-        unsigned long long h = 0xcbf29ce484222325ull;
-        for (std::uint32_t k = 0; k < len; ++k) h = (h ^ static_cast<std::uint32_t>(lits[k])) * 0x100000001b3ull;
+        unsigned long long h = 0;
+        for (std::uint32_t k = lane; k < len; k += 32) {
+            unsigned long long x = (static_cast<unsigned long long>(static_cast<std::uint32_t>(lits[k])) << 20) ^ k;
+            x *= 0x9E3779B97F4A7C15ull;
+            h += x ^ (x >> 29);
+        }
+        h = w_add64(h) + len;
         const std::uint32_t mask = K.dupcap - 1;
         const unsigned long long tag = static_cast<unsigned long long>(c->epoch) << 32;
         for (std::uint32_t at = static_cast<std::uint32_t>(h ^ (h >> 32)) & mask;; at = (at + 1) & mask) {
             const unsigned long long ent = sl.dup()[at];
             if ((ent >> 32) != c->epoch || ent == 0) {
-                sl.dup()[at] = tag | (c->learned_n + 1);
+                __syncwarp();
+                if (lane == 0) sl.dup()[at] = tag | (c->learned_n + 1);
                 break;
             }
             const std::uint32_t other = static_cast<std::uint32_t>(ent) - 1;
             const std::uint32_t olo = sl.loff()[other], olen = sl.loff()[other + 1] - olo;
             bool same = olen == len;
-            for (std::uint32_t k = 0; same && k < len; ++k) same = sl.lpool()[olo + k] == lits[k];
-            if (same) {
-                c->st.duplicate_learned += 1;
+            for (std::uint32_t k = lane; same && k < len; k += 32) same = sl.lpool()[olo + k] == lits[k];
+            if (__all_sync(0xffffffffu, same)) {
+                if (lane == 0) c->st.duplicate_learned += 1;
                 break;
             }
         }
         const std::uint32_t k = c->learned_n;
         const std::uint32_t id = S.N + k;
         const std::uint32_t lo = c->lpool_used;
-        for (std::uint32_t j = 0; j < len; ++j) sl.lpool()[lo + j] = lits[j];
-        sl.loff()[k + 1] = lo + len;
-        c->lpool_used = lo + len;
+        for (std::uint32_t j = lane; j < len; j += 32) sl.lpool()[lo + j] = lits[j];
         const std::uint32_t cls = len >= 4 ? 3u : len - 1u;
-        for (std::uint32_t j = 0; j < len; ++j) {
+        bool fail = false;
+        for (std::uint32_t j = lane; j < len; j += 32) {  // distinct literals: distinct lists
             const std::uint32_t li = lidx(lits[j]);
             std::uint32_t* h3 = sl.lhdr() + 3 * (li * 4 + cls);
-            if (h3[1] == h3[2]) {
-                const std::uint32_t ncap = h3[2] ? 2 * h3[2] : 4u;
-                if (c->locc_used + ncap > K.larena) {
-                    c->status = kErrArena;
-                    return -1;
-                }
-                const std::uint32_t np = c->locc_used;
-                for (std::uint32_t q = 0; q < h3[1]; ++q) sl.larena()[np + q] = sl.larena()[h3[0] + q];  // 16-byte entries
+            std::uint32_t base = h3[0], size = h3[1], cap = h3[2];
+            if (size == cap) {
+                const std::uint32_t ncap = cap ? 2 * cap : 4u;
+                const std::uint32_t np = atomicAdd(&c->locc_used, ncap);
+                if (np + ncap > K.larena) { fail = true; continue; }
+                for (std::uint32_t q = 0; q < size; ++q) sl.larena()[np + q] = sl.larena()[base + q];  // 16-byte entries
+                base = np;
                 h3[0] = np;
                 h3[2] = ncap;
-                c->locc_used = np + ncap;
             }
-            std::int32_t other[2] = {0, 0};
-            for (std::uint32_t q = 0, n = 0; q < len && n < 2; ++q)
-                if (q != j) other[n++] = lits[q];
-            sl.larena()[h3[0] + h3[1]] = make_int4(static_cast<std::int32_t>(id | cls << 30), static_cast<std::int32_t>(kNone),
-                                                   other[0], other[1]);
-            h3[1] += 1;
+            const std::int32_t o0 = j == 0 ? (len > 1 ? lits[1] : 0) : lits[0];
+            const std::int32_t o1 = j <= 1 ? (len > 2 ? lits[2] : 0) : lits[1];
+            sl.larena()[base + size] = make_int4(static_cast<std::int32_t>(id | cls << 30), static_cast<std::int32_t>(kNone), o0, o1);
+            h3[1] = size + 1;
             sl.ltot()[li] += 1;
         }
-        if (len == 1) sl.lunits()[c->lunits_n++] = static_cast<std::int32_t>(id);
-        c->learned_n = k + 1;
+        __syncwarp();
+        if (__any_sync(0xffffffffu, fail)) {
+            if (lane == 0) c->status = kErrArena;
+            __syncwarp();
+            return -1;
+        }
+        if (lane == 0) {
+            sl.loff()[k + 1] = lo + len;
+            c->lpool_used = lo + len;
+            if (len == 1) sl.lunits()[c->lunits_n++] = static_cast<std::int32_t>(id);
+            c->learned_n = k + 1;
+        }
+        __syncwarp();
         return static_cast<std::int32_t>(id);
     }
 
-    // Driver::try_assert (solver.cpp:117-146) on the current frontier.
-    __device__ void try_assert(std::uint32_t id) {
+    // State of nogood `id` under the current assignment: any dead literal
+    // (satisfied), number of free literals and the free one when unique.
+    __device__ void w_status(std::uint32_t id, bool& dead, std::uint32_t& nfree, std::int32_t& rem) const {
         std::uint32_t len;
         const std::int32_t* L = lits_of(id, len);
-        std::int32_t rem = 0;
-        for (std::uint32_t k = 0; k < len; ++k) {
+        std::uint32_t nf = 0;
+        std::int32_t fl = 0;
+        bool dd = false;
+        for (std::uint32_t k = lane_id(); k < len; k += 32) {
             const std::int32_t l = lit_at(L, k, id);
-            const int cv = val(atom_of(l));
-            if (cv == 0) {
-                if (rem != 0) return;
-                rem = l;
-            } else if ((cv > 0) != (l > 0)) {
-                return;
-            }
+            const int v = val(atom_of(l));
+            if (v == 0) { ++nf; fl = l; }
+            else if ((v > 0) != (l > 0)) dd = true;
         }
-        if (rem == 0) {
-            sl.pending()[c->n_pending++] = static_cast<std::int32_t>(id);
+        dead = __any_sync(0xffffffffu, dd);
+        nfree = __reduce_add_sync(0xffffffffu, nf);
+        const unsigned holder = __ballot_sync(0xffffffffu, nf != 0);
+        rem = holder ? __shfl_sync(0xffffffffu, fl, __ffs(holder) - 1) : 0;
+    }
+
+    // Driver::try_assert (solver.cpp:117-146) on the current frontier.
+    __device__ void w_try_assert(std::uint32_t id) {
+        const std::uint32_t lane = lane_id();
+        bool dead;
+        std::uint32_t nfree;
+        std::int32_t rem;
+        w_status(id, dead, nfree, rem);
+        if (dead || nfree >= 2) return;
+        if (nfree == 0) {
+            if (lane == 0) sl.pending()[c->n_pending++] = static_cast<std::int32_t>(id);
+            __syncwarp();
             return;
         }
         if (!may_assert(guard_of(id), -rem)) return;
         const std::int32_t lit = -rem;
         const std::uint32_t a = atom_of(lit), cdl = c->cdl;
-        write_deps_from(L, len, id, a, cdl);
-        set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
-        sl.reason()[a] = static_cast<std::int32_t>(id);
-        sl.tpos()[a] = c->ts;
-        sl.trail()[c->ts++] = lit;
-        sl.fr(c->cur)[c->F++] = lit;
-        c->st.propagations += 1;
-    }
-
-    __device__ bool is_unit_now(std::uint32_t id) const {
-        std::uint32_t len, nfree = 0;
+        std::uint32_t len;
         const std::int32_t* L = lits_of(id, len);
-        for (std::uint32_t k = 0; k < len; ++k) {
-            const std::int32_t l = lit_at(L, k, id);
-            const int cv = val(atom_of(l));
-            if (cv == 0) ++nfree;
-            else if ((cv > 0) != (l > 0)) return false;
+        const std::uint32_t nw = nwords(cdl);
+        std::uint32_t ov = 0;
+        for (std::uint32_t w = 0; w < nw; ++w) {  // Deps: OR over the other literals (propagate.cpp:49-62)
+            unsigned long long acc = 0;
+            for (std::uint32_t k = lane; k < len; k += 32) {
+                const std::uint32_t x = atom_of(lit_at(L, k, id));
+                if (x == a || lvl_of(sl.cells()[x]) <= 1) continue;
+                acc |= dep(w, x);
+                if (w == 0) ov |= sl.dovf()[x];
+            }
+            acc = w_or64(acc);
+            if (lane == 0) dep(w, a) = acc;
         }
-        return nfree == 1;
+        ov = __reduce_or_sync(0xffffffffu, ov);
+        if (lane == 0) {
+            sl.dovf()[a] = static_cast<std::uint8_t>(ov);
+            set_cell(a, lit > 0 ? static_cast<std::int32_t>(cdl) : -static_cast<std::int32_t>(cdl));
+            sl.reason()[a] = static_cast<std::int32_t>(id);
+            sl.tpos()[a] = c->ts;
+            sl.trail()[c->ts++] = lit;
+            sl.fr(c->cur)[c->F++] = lit;
+            c->st.propagations += 1;
+        }
+        __syncwarp();
     }
 
     // fwd_learning (learn.cpp:106-142). Writes the learned literals to out and
     // returns their count, or 0xffffffff on a Deps overflow (-> res fallback).
-    __device__ std::uint32_t fwd(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+    __device__ std::uint32_t w_fwd(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+        const std::uint32_t lane = lane_id();
+        const unsigned below = (1u << lane) - 1u;
         std::uint32_t len;
         const std::int32_t* L = lits_of(delta, len);
         std::uint32_t cl = 0;
-        for (std::uint32_t k = 0; k < len; ++k) {
+        bool ov = false;
+        for (std::uint32_t k = lane; k < len; k += 32) {
             const std::uint32_t a = atom_of(lit_at(L, k, delta));
-            const std::uint32_t lv = lvl_of(sl.cells()[a]);
-            cl = lv > cl ? lv : cl;
-            if (sl.dovf()[a]) return 0xffffffffu;
+            cl = max(cl, lvl_of(sl.cells()[a]));
+            ov |= sl.dovf()[a] != 0;
         }
+        cl = __reduce_max_sync(0xffffffffu, cl);
+        if (__any_sync(0xffffffffu, ov)) return 0xffffffffu;
         const std::uint32_t nw = nwords(c->cdl);
-        std::uint32_t n = 0;
-        target = 0;
+        std::uint32_t n = 0, tg = 0;
         for (std::uint32_t w = 0; w < nw; ++w) {
             unsigned long long m = 0;
-            for (std::uint32_t k = 0; k < len; ++k) {
+            for (std::uint32_t k = lane; k < len; k += 32) {
                 const std::uint32_t a = atom_of(lit_at(L, k, delta));
                 if (lvl_of(sl.cells()[a]) > 1) m |= dep(w, a);
             }
-            for (unsigned long long b = m; b; b &= b - 1) {
-                const std::uint32_t level = 64 * w + static_cast<std::uint32_t>(__ffsll(static_cast<long long>(b))) ;
-                out[n++] = sl.ldec()[level];
-                if (level < cl && level > target) target = level;
+            m = w_or64(m);
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const std::uint32_t b32 = static_cast<std::uint32_t>(m >> (32 * half));
+                if (b32 >> lane & 1u) {
+                    const std::uint32_t level = 64 * w + 32 * half + lane + 1;
+                    out[n + __popc(b32 & below)] = sl.ldec()[level];
+                    if (level < cl) tg = max(tg, level);
+                }
+                n += __popc(b32);
             }
         }
+        target = __reduce_max_sync(0xffffffffu, tg);
         if (target == 0) target = 1;
-        sort_by_atom(out, n);
+        __syncwarp();
+        w_sort(out, n);
         return n;
     }
 
-    // res_learning (learn.cpp:53-104): resolve until a positive UIP.
-    __device__ std::uint32_t res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+    // res_learning (learn.cpp:53-104): resolve until a positive UIP. The set is
+    // kept as atoms in out[0..n) (unordered) with membership stamps in mark[].
+    __device__ std::uint32_t w_res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+        const std::uint32_t lane = lane_id();
+        const unsigned below = (1u << lane) - 1u;
         std::uint32_t* mark = sl.mark();
-        const std::uint32_t stamp = ++c->stamp;
+        const std::uint32_t stamp = c->stamp + 1;
+        __syncwarp();
+        if (lane == 0) c->stamp = stamp;
         std::uint32_t len;
         const std::int32_t* L = lits_of(delta, len);
-        std::uint32_t n = 0;
-        for (std::uint32_t k = 0; k < len; ++k) {
+        std::uint32_t n = len;
+        for (std::uint32_t k = lane; k < len; k += 32) {
             const std::uint32_t a = atom_of(lit_at(L, k, delta));
             mark[a] = stamp;
-            out[n++] = static_cast<std::int32_t>(a);
+            out[k] = static_cast<std::int32_t>(a);
         }
+        __syncwarp();
         for (;;) {
-            std::uint32_t si = 0;
-            for (std::uint32_t k = 1; k < n; ++k)
-                if (sl.tpos()[out[k]] > sl.tpos()[out[si]]) si = k;
+            // sigma = greatest trail position; kappa = greatest level of the others
+            unsigned long long best = 0;  // (tpos + 1) << 32 | k
+            std::uint32_t m1 = 0, c1 = 0;
+            for (std::uint32_t k = lane; k < n; k += 32) {
+                const std::uint32_t a = static_cast<std::uint32_t>(out[k]);
+                const unsigned long long key = (static_cast<unsigned long long>(sl.tpos()[a] + 1) << 32) | k;
+                best = key > best ? key : best;
+                const std::uint32_t lv = lvl_of(sl.cells()[a]);
+                if (lv > m1) { m1 = lv; c1 = 1; } else if (lv == m1) ++c1;
+            }
+            best = w_max64(best);
+            const std::uint32_t gm1 = __reduce_max_sync(0xffffffffu, m1);
+            const std::uint32_t gc1 = __reduce_add_sync(0xffffffffu, m1 == gm1 ? c1 : 0u);
+            std::uint32_t m2 = 0;
+            for (std::uint32_t k = lane; k < n; k += 32) {
+                const std::uint32_t lv = lvl_of(sl.cells()[out[k]]);
+                if (lv < gm1) m2 = max(m2, lv);
+            }
+            m2 = __reduce_max_sync(0xffffffffu, m2);
+            const std::uint32_t si = static_cast<std::uint32_t>(best);
             const std::uint32_t sa = static_cast<std::uint32_t>(out[si]);
-            const std::uint32_t slev = lvl_of(sl.cells()[sa]);
-            std::uint32_t kappa = 0;
-            for (std::uint32_t k = 0; k < n; ++k)
-                if (k != si) { const std::uint32_t lv = lvl_of(sl.cells()[out[k]]); kappa = lv > kappa ? lv : kappa; }
-            if (kappa != slev && sl.cells()[sa] > 0) {
+            const std::int32_t scell = sl.cells()[sa];
+            const std::uint32_t slev = lvl_of(scell);
+            const std::uint32_t kappa = slev == gm1 ? (gc1 > 1 ? gm1 : m2) : gm1;
+            if (kappa != slev && scell > 0) {
                 target = kappa > 1 ? kappa : 1;
-                for (std::uint32_t k = 0; k < n; ++k) {
+                for (std::uint32_t k = lane; k < n; k += 32) {
                     const std::int32_t a = out[k];
                     out[k] = sl.cells()[a] > 0 ? a : -a;
                 }
-                sort_by_atom(out, n);
+                __syncwarp();
+                w_sort(out, n);
                 return n;
             }
             const std::int32_t r = sl.reason()[sa];
-            out[si] = out[--n];
-            mark[sa] = 0;
-            if (r >= 0) {
-                std::uint32_t elen;
-                const std::int32_t* E = lits_of(static_cast<std::uint32_t>(r), elen);
-                for (std::uint32_t k = 0; k < elen; ++k) {
-                    const std::uint32_t a = atom_of(lit_at(E, k, static_cast<std::uint32_t>(r)));
-                    if (a == sa || mark[a] == stamp) continue;
-                    mark[a] = stamp;
-                    out[n++] = static_cast<std::int32_t>(a);
-                }
-            } else if (r == kReasonCompletion) {
-                for (std::uint32_t lv = 2; lv <= c->cdl; ++lv) {
-                    const std::uint32_t a = atom_of(sl.ldec()[lv]);
-                    if (a == sa || mark[a] == stamp) continue;
-                    mark[a] = stamp;
-                    out[n++] = static_cast<std::int32_t>(a);
-                }
-            } else {
-                c->status = kErrLogic;
+            __syncwarp();
+            if (lane == 0) {
+                out[si] = out[n - 1];
+                mark[sa] = 0;
+            }
+            --n;
+            __syncwarp();
+            const std::int32_t* E = nullptr;
+            std::uint32_t elen = 0;
+            if (r >= 0) E = lits_of(static_cast<std::uint32_t>(r), elen);
+            else if (r == kReasonCompletion) elen = c->cdl >= 2 ? c->cdl - 1 : 0;
+            else {
+                if (lane == 0) c->status = kErrLogic;
+                __syncwarp();
                 return 0;
             }
+            for (std::uint32_t k0 = 0; k0 < elen; k0 += 32) {
+                const std::uint32_t k = k0 + lane;
+                std::uint32_t a = 0;
+                if (k < elen) a = r >= 0 ? atom_of(lit_at(E, k, static_cast<std::uint32_t>(r))) : atom_of(sl.ldec()[k + 2]);
+                const bool keep = k < elen && a != sa && mark[a] != stamp;
+                const unsigned km = __ballot_sync(0xffffffffu, keep);
+                if (keep) {
+                    mark[a] = stamp;
+                    out[n + __popc(km & below)] = static_cast<std::int32_t>(a);
+                }
+                n += __popc(km);
+            }
+            __syncwarp();
         }
     }
 
-    __device__ void bump_activity(const std::int32_t* lits, std::uint32_t n) {
-        if (C.heur != 2) return;
-        for (std::uint32_t k = 0; k < n; ++k) sl.act()[atom_of(lits[k])] += c->act_inc;
-    }
-
-    // Driver::handle_conflicts (solver.cpp:161-214), leader part. Returns
-    // 0 = exhausted, 1 = continue; writes the backjump plan to c->b.
+    // Driver::handle_conflicts (solver.cpp:161-214), leader-warp part: writes
+    // the backjump plan to c->b.
     __device__ void analyze_and_learn() {
-        c->st.conflicts += 1;
-        c->b[0] = 0;
+        const std::uint32_t lane = lane_id();
+        if (lane == 0) {
+            c->st.conflicts += 1;
+            c->b[0] = 0;
+        }
+        __syncwarp();
         if (c->cdl == 1) return;  // nothing to revise
         const std::uint32_t nc = c->n_confl;
         // select conflicts: min (length, id); fanout K in fwd mode (learn.cpp:148-157)
@@ -2062,11 +2287,12 @@ struct Search {
         std::uint32_t bj = 0xffffffffu;
         while (n_sel < K2) {
             unsigned long long best = ~0ull;
-            for (std::uint32_t i = 0; i < nc; ++i) {
+            for (std::uint32_t i = lane; i < nc; i += 32) {
                 const std::uint32_t id = static_cast<std::uint32_t>(sl.confl()[i]);
                 const unsigned long long key = (static_cast<unsigned long long>(length_of(id)) << 32) | id;
                 if ((!have_prev || key > prev) && key < best) best = key;
             }
+            best = w_min64(best);
             if (best == ~0ull) break;
             prev = best;
             have_prev = true;
@@ -2074,63 +2300,80 @@ struct Search {
             std::uint32_t target = 1, n = 0xffffffffu;
             std::uint32_t used = 1;  // 0 fwd, 1 res
             if (C.mode == 0) {
-                n = fwd(delta, buf, target);
+                n = w_fwd(delta, buf, target);
                 if (n != 0xffffffffu) used = 0;
             }
             if (n == 0xffffffffu) {
-                n = res(delta, buf, target);
+                n = w_res(delta, buf, target);
                 if (c->status != kRunning) return;
             }
             // structural self-checks (solver.cpp:171-186)
             if (used == 1) {
-                std::uint32_t cl = 0, at = 0;
-                for (std::uint32_t k = 0; k < n; ++k) { const std::uint32_t lv = lvl_of(sl.cells()[atom_of(buf[k])]); cl = lv > cl ? lv : cl; }
-                for (std::uint32_t k = 0; k < n; ++k) at += lvl_of(sl.cells()[atom_of(buf[k])]) == cl;
-                if (at != 1) c->st.uip_check_failures += 1;
-                c->st.res_learned += 1;
-                if (C.mode == 0) c->st.fwd_fallbacks += 1;
+                std::uint32_t cl = 0;
+                for (std::uint32_t k = lane; k < n; k += 32) cl = max(cl, lvl_of(sl.cells()[atom_of(buf[k])]));
+                cl = __reduce_max_sync(0xffffffffu, cl);
+                std::uint32_t at = 0;
+                for (std::uint32_t k = lane; k < n; k += 32) at += lvl_of(sl.cells()[atom_of(buf[k])]) == cl;
+                at = __reduce_add_sync(0xffffffffu, at);
+                if (lane == 0) {
+                    if (at != 1) c->st.uip_check_failures += 1;
+                    c->st.res_learned += 1;
+                    if (C.mode == 0) c->st.fwd_fallbacks += 1;
+                }
             } else {
-                for (std::uint32_t k = 0; k < n; ++k)
-                    if (sl.reason()[atom_of(buf[k])] != kReasonDecision) c->st.fwd_decision_only_failures += 1;
-                c->st.fwd_learned += 1;
+                std::uint32_t bad = 0;
+                for (std::uint32_t k = lane; k < n; k += 32) bad += sl.reason()[atom_of(buf[k])] != kReasonDecision;
+                bad = __reduce_add_sync(0xffffffffu, bad);
+                if (lane == 0) {
+                    c->st.fwd_decision_only_failures += bad;
+                    c->st.fwd_learned += 1;
+                }
             }
-            const std::int32_t id = add_learned(buf, n);
+            __syncwarp();
+            const std::int32_t id = w_add_learned(buf, n);
             if (id < 0) return;
-            added[n_sel] = id;
-            levels[n_sel] = static_cast<std::int32_t>(target);
+            if (C.heur == 2)
+                for (std::uint32_t k = lane; k < n; k += 32) sl.act()[atom_of(buf[k])] += c->act_inc;
+            if (lane == 0) {
+                added[n_sel] = id;
+                levels[n_sel] = static_cast<std::int32_t>(target);
+                c->st.learned_count += 1;
+                c->st.learned_length_sum += n;
+                if (C.trace && c->n_trace < K.tcap)
+                    sl.tbuf()[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
+            }
             ++n_sel;
             bj = target < bj ? target : bj;
-            c->st.learned_count += 1;
-            c->st.learned_length_sum += n;
-            bump_activity(buf, n);
-            if (C.trace && c->n_trace < K.tcap)
-                sl.tbuf()[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
+            __syncwarp();
         }
         // Heuristic::on_conflict (decide.cpp:34-41)
         if (C.heur == 2) {
-            c->act_inc /= C.decay;
-            if (c->act_inc > 1e100) {
-                for (std::uint32_t a = 0; a <= S.A; ++a) sl.act()[a] *= 1e-100;
-                c->act_inc *= 1e-100;
+            const double inc = c->act_inc / C.decay;
+            if (inc > 1e100)
+                for (std::uint32_t a = lane; a <= S.A; a += 32) sl.act()[a] *= 1e-100;
+            __syncwarp();
+            if (lane == 0) c->act_inc = inc > 1e100 ? inc * 1e-100 : inc;
+        }
+        if (lane == 0) {
+            const bool restart = C.restarts && c->st.conflicts - c->conflicts_at_restart >= c->restart_threshold;
+            if (restart) {
+                c->st.restarts += 1;
+                c->conflicts_at_restart = c->st.conflicts;
+                c->restart_threshold = static_cast<unsigned long long>(
+                    ceil(static_cast<double>(c->restart_threshold) * C.restart_factor));
             }
+            c->b[0] = 1;
+            c->b[1] = restart ? 1u : 0u;
+            c->b[2] = restart ? 1u : bj;
+            c->b[3] = n_sel;
+            c->F = 0;
+            c->n_confl = 0;
         }
-        const bool restart = C.restarts && c->st.conflicts - c->conflicts_at_restart >= c->restart_threshold;
-        if (restart) {
-            c->st.restarts += 1;
-            c->conflicts_at_restart = c->st.conflicts;
-            c->restart_threshold = static_cast<unsigned long long>(
-                ceil(static_cast<double>(c->restart_threshold) * C.restart_factor));
-        }
-        c->b[0] = 1;
-        c->b[1] = restart ? 1u : 0u;
-        c->b[2] = restart ? 1u : bj;
-        c->b[3] = n_sel;
-        c->F = 0;
-        c->n_confl = 0;
+        __syncwarp();
     }
 
     __device__ bool handle_conflicts() {
-        if (g.leader()) analyze_and_learn();
+        if (g.leader_warp()) analyze_and_learn();
         g.sync();
         if (c->status != kRunning) return false;
         if (c->b[0] == 0) return false;
@@ -2138,15 +2381,21 @@ struct Search {
         const std::uint32_t target = c->b[2];
         backjump(target);
         if (restart) initial_propagation(false);
-        if (g.leader()) {
+        if (g.leader_warp()) {
             const std::uint32_t n_sel = c->b[3];
             const std::int32_t* added = sl.scratch();
             const std::int32_t* levels = sl.scratch() + 64;
             if (!restart)
                 for (std::uint32_t i = 0; i < n_sel; ++i)
-                    if (static_cast<std::uint32_t>(levels[i]) == target && !is_unit_now(static_cast<std::uint32_t>(added[i])))
-                        c->st.asserting_failures += 1;
-            for (std::uint32_t i = 0; i < n_sel; ++i) try_assert(static_cast<std::uint32_t>(added[i]));
+                    if (static_cast<std::uint32_t>(levels[i]) == target) {
+                        bool dead;
+                        std::uint32_t nfree;
+                        std::int32_t rem;
+                        w_status(static_cast<std::uint32_t>(added[i]), dead, nfree, rem);
+                        if ((dead || nfree != 1) && lane_id() == 0) c->st.asserting_failures += 1;
+                        __syncwarp();
+                    }
+            for (std::uint32_t i = 0; i < n_sel; ++i) w_try_assert(static_cast<std::uint32_t>(added[i]));
         }
         g.sync();
         return true;
@@ -2299,27 +2548,30 @@ struct Search {
 
     // block_current_model (solver.cpp:234-246). false = enumeration complete.
     __device__ bool block_model() {
-        if (g.leader()) {
-            c->b[0] = 0;
+        if (g.leader_warp()) {
+            const std::uint32_t lane = lane_id();
+            if (lane == 0) c->b[0] = 0;
             const std::uint32_t cdl = c->cdl;
             if (cdl > 1) {
                 std::int32_t* buf = sl.scratch() + 128;
-                for (std::uint32_t lv = 2; lv <= cdl; ++lv) buf[lv - 2] = sl.ldec()[lv];
-                sort_by_atom(buf, cdl - 1);
-                const std::int32_t id = add_learned(buf, cdl - 1);
-                if (id >= 0) {
+                for (std::uint32_t lv = 2 + lane; lv <= cdl; lv += 32) buf[lv - 2] = sl.ldec()[lv];
+                __syncwarp();
+                w_sort(buf, cdl - 1);
+                const std::int32_t id = w_add_learned(buf, cdl - 1);
+                if (id >= 0 && lane == 0) {
                     c->st.blocking_nogoods += 1;
                     c->b[0] = 1;
                     c->b[1] = static_cast<std::uint32_t>(id);
                     c->F = 0;
                 }
             }
+            __syncwarp();
         }
         g.sync();
         if (c->b[0] == 0) return false;
         const std::uint32_t id = c->b[1];
         backjump(1);
-        if (g.leader()) try_assert(id);
+        if (g.leader_warp()) w_try_assert(id);
         g.sync();
         return true;
     }
@@ -2384,12 +2636,18 @@ struct Search {
             c->conflicts_at_restart = c->st.conflicts;
             c->act_inc = 1.0;
             c->st.searches += 1;
-            // cube constraints enter as unit nogoods ahead of any learned one
+            c->phase = kInit;
+        }
+        g.sync();
+        if (g.leader_warp()) {  // cube constraints enter as unit nogoods ahead of any learned one
+            std::int32_t* buf = sl.scratch() + 128;
             for (std::uint32_t k = 0; k < C.cube_width; ++k) {
                 const std::int32_t l = __ldg(S.cubes + static_cast<std::size_t>(cube) * C.cube_width + k);
-                if (l != 0) add_learned(&l, 1, false);
+                if (l == 0) continue;
+                if (lane_id() == 0) buf[0] = l;
+                __syncwarp();
+                w_add_learned(buf, 1, false);
             }
-            c->phase = kInit;
         }
         g.sync();
     }
@@ -2435,6 +2693,7 @@ struct Search {
                 c->b[15] = y ? 1u : 0u;
             }
             g.sync();
+            mark(11);
             if (c->b[15]) {
                 if (g.leader()) c->status = kYield;
                 g.sync();
@@ -2668,11 +2927,13 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             g.sync();
             break;
         case kOpLearn:  // NogoodStore::add_learned (kNoTruth guard)
-            if (g.leader()) {
+            if (g.leader_warp()) {
                 std::int32_t* buf = sl.scratch() + 128;
-                for (std::uint32_t k = 0; k < op.n; ++k) buf[k] = op.lits[k];
-                s.sort_by_atom(buf, op.n);
-                c->b[12] = static_cast<std::uint32_t>(s.add_learned(buf, op.n));
+                for (std::uint32_t k = lane_id(); k < op.n; k += 32) buf[k] = op.lits[k];
+                __syncwarp();
+                s.w_sort(buf, op.n);
+                const std::int32_t id = s.w_add_learned(buf, op.n);
+                if (lane_id() == 0) c->b[12] = static_cast<std::uint32_t>(id);
             }
             g.sync();
             break;

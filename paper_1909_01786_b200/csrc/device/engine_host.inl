@@ -109,7 +109,7 @@ struct Arena {
         L.o_cells = take(4 * A1);
         L.o_tpos = take(4 * A1);
         L.o_reason = take(4 * A1);
-        L.o_deps = take(8 * W * A1);
+        L.o_deps = take(8 * static_cast<std::size_t>((W + 1) & ~1u) * A1);  // atom-major rows
         L.o_dovf = take(A1);
         L.o_trail = take(4 * A1);
         L.o_ldec = take(4 * (A1 + 1));
@@ -131,7 +131,7 @@ struct Arena {
         L.o_ltot = take(4 * 2 * A1);
         L.o_act = take(8 * A1);
         L.o_dup = take(8ull * K.dupcap);
-        L.o_scratch = take(4 * (A1 + 256));
+        L.o_scratch = take(4 * (2 * A1 + 512));  // ids/levels, learned literals, sort buffer
         L.o_mark = take(4 * A1);
         L.o_merged = take(8 * W);
         L.o_mbuf = take(4ull * mcap * K.mwords);
@@ -297,16 +297,12 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
         static const char* names[14] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
-                                        "conflict", "x.occ", "x.hash", "x.eval", "-", "sumT", "iters"};
+                                        "conflict", "tiny", "warp", "-", "looptop", "-", "-"};
         unsigned long long p[16] = {0};
         for (const dev::Ctl& c : ctl)
             for (int k = 0; k < 16; ++k) p[k] += c.prof[k];
         std::fprintf(stderr, "[yas profile] passes=%llu", static_cast<unsigned long long>(tot.passes));
         for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %s=%.2fM", names[k], p[k] / 1e6);
-        std::fprintf(stderr, " | probe: occ_off %.0f entry %.0f cells %.0f occ_off-again %.0f cyc (x%llu)",
-                     double(p[11]) / std::max(1ull, p[13]), double(p[14]) / std::max(1ull, p[13]),
-                     double(p[15] & 0xffffffffull) / std::max(1ull, p[13]), double(p[15] >> 32) / std::max(1ull, p[13]),
-                     p[13]);
         std::fprintf(stderr, "\n");
     }
     cudaEventDestroy(e0);
@@ -551,7 +547,11 @@ std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].
 std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts, impl_->stream); }
 std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream); }
 std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
-    return dl(impl_->ar.slots[0].deps() + static_cast<std::size_t>(w) * (impl_->ar.A + 1), impl_->ar.A + 1, impl_->stream);
+    const std::size_t stride = (W_ + 1) & ~1u, n = impl_->ar.A + 1;
+    const std::vector<unsigned long long> rows = dl(impl_->ar.slots[0].deps(), n * stride, impl_->stream);
+    std::vector<unsigned long long> v(n);
+    for (std::size_t a = 0; a < n; ++a) v[a] = rows[a * stride + w];
+    return v;
 }
 std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream); }
 std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl, impl_->stream); }

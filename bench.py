@@ -153,7 +153,13 @@ def reference_arm(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def log(msg):
+    print(f"[bench {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
+    import faulthandler
+    faulthandler.dump_traceback_later(int(os.environ.get("BENCH_WATCHDOG_S", "1500")), exit=True)  # a hung section names itself on stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -222,7 +228,7 @@ def main():
     peak, peak_kind = peaks()
     achieved = algo_bytes / (avg_ms / 1e3) / 1e9
     traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "planted_grid_dram.json")
+    prof_json = os.path.join(ROOT, "profiles", "r01_planted_grid.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
@@ -258,6 +264,7 @@ def main():
         "clocks": clk.summary(), "gpu_launches": launches, "bracket_wall_s": wall,
     }
 
+    log("cpu baseline")
     if rank == 0:
         try:
             if os.path.exists(REF_BIN):
@@ -279,14 +286,84 @@ def main():
                                     "sample": f"failed: {e}"}
 
     if not args.no_extras:
+        del prop
+        log("planted 8M")
+        line["planted_8m"] = planted_large(Y, torch, flush, local)
+        log("enumeration")
         line["enumeration"] = enumeration(Y, I, rank, world, local)
         if rank == 0:
+            log("random program 4a")
+            line["random_program_4a"] = random_program(Y, I, local)
+            log("first model")
             line["first_model"] = first_model(Y, I, local)
+        log("done")
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def planted_large(Y, torch, flush, local, steps=5):
+    """Config 4b scaled past the 126 MB L2: 8M nogoods / 800k atoms (fat
+    occurrence entries alone are 512 MB), same recipe and seeding."""
+    cfg = dict(atoms=800_000, nogoods=8_000_000, pct=50, seed=0x1B00B5)
+    store, seeded_list, dec = Y.NogoodStore.planted(**cfg)
+    prop = Y.Propagator(store, 16, engine="grid", device=local)
+    seeded = torch.tensor(seeded_list, dtype=torch.int32).pin_memory().numpy()
+    frontier = torch.tensor([dec] + seeded_list, dtype=torch.int32).pin_memory().numpy()
+
+    def run():
+        prop.reset()
+        prop.push_decision(dec)
+        prop.assign_propagated(seeded, 2)
+        prop.seed(frontier)
+        flush.zero_()
+        torch.cuda.synchronize()
+        return prop.propagate_and_check(2)
+
+    for _ in range(2):
+        run()
+    prop.count_literals(True)
+    lits = run().checked_lits
+    prop.count_literals(False)
+    outs = [run() for _ in range(steps)]
+    ms = statistics.mean(o.device_ms for o in outs)
+    checks = outs[-1].checks
+    peak, _ = peaks()
+    achieved = (12 * checks + 4 * lits) / (ms / 1e3) / 1e9
+    out = {"workload": "planted 8M nogoods / 800k atoms, 50% seeded (exceeds L2)", "checks_per_step": checks,
+           "passes": outs[-1].passes, "ms_per_step": ms, "checks_per_s": checks / (ms / 1e3),
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
+           "l2": "flushed before every step"}
+    if os.path.exists(REF_BIN):  # one reference call on the same store (bounded: ~1 s)
+        r = subprocess.run([REF_BIN, "planted", str(cfg["atoms"]), str(cfg["nogoods"]), str(cfg["pct"]),
+                            hex(cfg["seed"]), "1"], capture_output=True, text=True, check=True)
+        ref_ms = json.loads(r.stdout)["prop_ms"][0]
+        out["cpu_reference"] = {"ms_per_call": ref_ms, "checks_per_s": checks / (ref_ms / 1e3), "cores": 1}
+    return out
+
+
+def random_program(Y, I, local):
+    """Config 4a: the 100k-atom / 111k-rule random program (986k nogoods),
+    solved to its first answer set by propagation alone (grid engine)."""
+    text = I.random_program()
+    t = time.perf_counter()
+    prog = Y.parse_program(text)
+    load_ms = (time.perf_counter() - t) * 1e3
+    Y.solve(prog, Y.SolverConfig(device=local))
+    r = Y.solve(prog, Y.SolverConfig(device=local))
+    out = {"status": r.status.name, "device_ms": r.stats.device_ms, "passes": r.stats.passes,
+           "checks": r.stats.checks, "checks_per_s": r.stats.checks / (r.stats.device_ms / 1e3),
+           "parse_ms": load_ms, "decisions": r.stats.decisions}
+    if os.path.exists(REF_BIN):
+        p = subprocess.run([REF_BIN, "solve", "-", "-n", "1", "--no-models", "--reps", "2"], input=text,
+                           capture_output=True, text=True, check=True)
+        ref = json.loads(p.stdout)
+        out["cpu_reference_run_ms"] = statistics.mean(ref["run_ms"])
+        out["same_trajectory"] = all(getattr(r.stats, k) == ref["stats"][k]
+                                     for k in ("decisions", "propagations", "conflicts", "passes"))
+    return out
 
 
 def enumeration(Y, I, rank, world, local):

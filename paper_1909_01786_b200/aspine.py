@@ -447,7 +447,7 @@ class NogoodStore:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None and N.lib is not None:
             N.lib().yas_store_free(h)
             self._h = C.c_void_p(0)
 
@@ -547,7 +547,7 @@ class Propagator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and N is not None and N.lib is not None:
             N.lib().yas_propagator_free(h)
             self._h = C.c_void_p(0)
 

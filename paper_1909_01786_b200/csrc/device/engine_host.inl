@@ -338,6 +338,7 @@ struct Session::Impl {
 
     std::int32_t* stage(const std::int32_t* src, std::size_t n) {
         if (n > d_lits_cap) {
+            ck(cudaStreamSynchronize(stream), "stream");  // the old buffer may still be read
             if (d_lits) cudaFree(d_lits);
             d_lits_cap = std::max<std::size_t>(n, 2 * d_lits_cap);
             ck(cudaMalloc(&d_lits, d_lits_cap * sizeof(std::int32_t)), "cudaMalloc staging");
@@ -372,6 +373,9 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     c.fanout = 1;
     c.learned_capacity = ~0ull;
     c.n_cubes = 1;
+    // the arena was uploaded / zeroed / initialised on the legacy stream; the
+    // session's non-blocking stream is not ordered after it
+    ck(cudaDeviceSynchronize(), "arena setup");
     ck(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&impl_->e0), "event");
     ck(cudaEventCreate(&impl_->e1), "event");

@@ -145,6 +145,10 @@ uint64_t yas_result_model_count(const yas_result* r);
 /* Model m: sorted program atom ids (Model::atom_ids); n receives the size. */
 const uint32_t* yas_result_model(const yas_result* r, uint64_t m, uint32_t* n);
 uint32_t yas_result_model_cube(const yas_result* r, uint64_t m);
+/* All models at once: ids of model m are ids[offsets[m] .. offsets[m+1]) (offsets
+ * has model_count + 1 entries), cubes[m] its cube; any output may be NULL.
+ * Returns the total number of ids (copies at most cap). */
+size_t yas_result_models_flat(const yas_result* r, uint32_t* ids, size_t cap, uint64_t* offsets, uint32_t* cubes);
 void yas_result_stats(const yas_result* r, yas_stats* s);
 void yas_result_free(yas_result* r);
 /* emit_stats / stats_csv_header (solver.hpp:131-133); ctx strings may be NULL. */

@@ -21,7 +21,7 @@ EXPORTS = [
     "yas_program_diagnostics", "yas_program_rule_aux", "yas_program_total_atoms", "yas_program_census",
     "yas_program_tp_step", "yas_program_cubes", "yas_verify_model",
     "yas_config_default", "yas_solve", "yas_result_status", "yas_result_model_count", "yas_result_model",
-    "yas_result_model_cube", "yas_result_stats", "yas_result_free", "yas_stats_csv_header", "yas_emit_stats",
+    "yas_result_model_cube", "yas_result_models_flat", "yas_result_stats", "yas_result_free", "yas_stats_csv_header", "yas_emit_stats",
     "yas_store_build", "yas_store_free", "yas_store_size", "yas_store_total_atoms", "yas_store_dump_csv",
     "yas_store_units", "yas_store_unit_ids", "yas_store_bounds", "yas_store_occurrences", "yas_store_planted",
     "yas_free_ints",
@@ -113,6 +113,7 @@ def lib() -> C.CDLL:
         "yas_result_model_count": (U64, [P]),
         "yas_result_model": (pU32, [P, U64, pU32]),
         "yas_result_model_cube": (U32, [P, U64]),
+        "yas_result_models_flat": (SZ, [P, pU32, SZ, pU64, pU32]),
         "yas_result_stats": (None, [P, C.POINTER(yas_stats)]),
         "yas_result_free": (None, [P]),
         "yas_stats_csv_header": (SZ, [C.c_char_p, SZ]),

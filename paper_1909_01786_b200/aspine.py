@@ -18,7 +18,8 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import Callable, Iterable, List, Optional, Sequence
+from collections.abc import Sequence
+from typing import Callable, Iterable, List, Optional
 
 import numpy as np
 
@@ -195,10 +196,55 @@ class SolveStats:
         return s
 
 
-@dataclass
 class Model:
-    atom_ids: List[int]
-    atoms: List[str]
+    """Model (solver.hpp:96-99): sorted atom ids; names sorted lexicographically
+    (resolved on first access, so enumerating many models stays cheap)."""
+
+    __slots__ = ("atom_ids", "_atoms", "_prog")
+
+    def __init__(self, atom_ids: List[int], atoms: Optional[List[str]] = None, prog: "Optional[GroundProgram]" = None):
+        self.atom_ids = atom_ids
+        self._atoms = atoms
+        self._prog = prog
+
+    @property
+    def atoms(self) -> List[str]:
+        if self._atoms is None:
+            self._atoms = sorted(self._prog.name(a) for a in self.atom_ids) if self._prog is not None else []
+        return self._atoms
+
+    def __eq__(self, other):
+        return isinstance(other, Model) and self.atom_ids == other.atom_ids and self.atoms == other.atoms
+
+    def __repr__(self):
+        return f"Model(atom_ids={self.atom_ids!r}, atoms={self.atoms!r})"
+
+
+class ModelList(Sequence):
+    """The models of a SolveResult as a read-only sequence over the flat id
+    buffer; Model objects are built on access (an enumeration may return tens
+    of thousands of models that the caller only counts)."""
+
+    def __init__(self, ids: np.ndarray, offs: np.ndarray, count: int, prog: "GroundProgram"):
+        self._ids, self._offs, self._n, self._prog = ids, offs, count, prog
+
+    def __len__(self) -> int:
+        return self._n
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self[k] for k in range(*i.indices(self._n))]
+        if i < 0:
+            i += self._n
+        if not 0 <= i < self._n:
+            raise IndexError(i)
+        return Model(self._ids[int(self._offs[i]):int(self._offs[i + 1])].tolist(), None, self._prog)
+
+    def __eq__(self, other):
+        return list(self) == list(other)
+
+    def __repr__(self):
+        return f"ModelList({len(self)} models)"
 
 
 @dataclass
@@ -390,13 +436,15 @@ def solve(prog: GroundProgram, cfg: Optional[SolverConfig] = None) -> SolveResul
         st = N.yas_stats()
         L.yas_result_stats(h, C.byref(st))
         stats = SolveStats(**{f: getattr(st, f) for f in _STAT_FIELDS})
-        models, cubes = [], []
-        n = C.c_uint32(0)
-        for m in range(L.yas_result_model_count(h)):
-            p = L.yas_result_model(h, m, C.byref(n))
-            ids = list(p[: n.value]) if n.value else []
-            models.append(Model(ids, sorted(prog.name(a) for a in ids)))
-            cubes.append(L.yas_result_model_cube(h, m))
+        count = L.yas_result_model_count(h)
+        total = L.yas_result_models_flat(h, None, 0, None, None)
+        ids = np.empty(max(1, total), dtype=np.uint32)
+        offs = np.empty(count + 1, dtype=np.uint64)
+        cub = np.empty(max(1, count), dtype=np.uint32)
+        L.yas_result_models_flat(h, ids.ctypes.data_as(C.POINTER(C.c_uint32)), ids.size,
+                                 offs.ctypes.data_as(C.POINTER(C.c_uint64)), cub.ctypes.data_as(C.POINTER(C.c_uint32)))
+        models = ModelList(ids, offs, count, prog)
+        cubes = cub[:count].tolist()
         status = SolveStatus(L.yas_result_status(h))
     finally:
         L.yas_result_free(h)

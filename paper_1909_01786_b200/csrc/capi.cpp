@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <fstream>
@@ -375,7 +377,15 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
     return guarded(err, err_cap, [&] {
         if (cfg.deps_words < 1 || cfg.deps_words > 1024) throw std::invalid_argument("deps_words must be in [1, 1024]");
         if (cfg.world < 1) cfg.world = 1;
+        const auto tp0 = std::chrono::steady_clock::now();
+        const bool prof = std::getenv("YAS_PROFILE") != nullptr;
+        auto lap = [&](const char* what) {
+            if (prof)
+                std::fprintf(stderr, "[yas host] %s at %.2f ms\n", what,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
+        };
         require_device(cfg.device);
+        lap("device");
         auto* q = const_cast<yas_program*>(p);
         const Program& prog = q->prog;
         const Completion& comp = q->completion();
@@ -415,6 +425,7 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         } else if (cfg.rank != 0) {
             n_cubes = 0;  // a single search runs on rank 0 only
         }
+        lap("compiled + cubes");
 
         EngineOptions eo;
         eo.device = cfg.device;
@@ -457,6 +468,7 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                 };
             EngineResult er;
             if (n_cubes > 0) er = engine_solve(ep, dc, eo, cubes, n_cubes, width, cb);
+            lap("engine");
             if (er.status == dev::kErrArena && attempt < 8) {
                 eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, 2ull * eo.lcap));
                 eo.lpool *= 2;
@@ -480,6 +492,7 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             res->stats.launches = er.launches;
             res->stats.cubes = n_cubes;
             res->status = res->models.empty() ? 1 : 0;
+            lap("result");
             break;
         }
         *out = res.release();
@@ -496,6 +509,20 @@ const uint32_t* yas_result_model(const yas_result* r, uint64_t m, uint32_t* n) {
     }
     if (n) *n = static_cast<uint32_t>(r->models[m].size());
     return r->models[m].data();
+}
+size_t yas_result_models_flat(const yas_result* r, uint32_t* ids, size_t cap, uint64_t* offsets, uint32_t* cubes) {
+    if (!r) return 0;
+    size_t total = 0;
+    for (std::size_t m = 0; m < r->models.size(); ++m) {
+        if (offsets) offsets[m] = total;
+        if (cubes) cubes[m] = m < r->cubes.size() ? r->cubes[m] : 0;
+        for (const uint32_t a : r->models[m]) {
+            if (ids && total < cap) ids[total] = a;
+            ++total;
+        }
+    }
+    if (offsets) offsets[r->models.size()] = total;
+    return total;
 }
 uint32_t yas_result_model_cube(const yas_result* r, uint64_t m) {
     return r && m < r->cubes.size() ? r->cubes[m] : 0;

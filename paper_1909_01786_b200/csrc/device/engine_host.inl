@@ -14,10 +14,27 @@ void ck(cudaError_t e, const char* what) {
     if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+// Arenas come from the device's stream-ordered memory pool, told to keep
+// freed memory: a repeated solve (or the next cube batch) reuses the previous
+// arena's pages instead of mapping gigabytes again.
+void keep_pool(int device) {
+    static bool done[64] = {false};
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        std::uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    done[device] = true;
+}
+
 template <class T>
 T* dalloc(std::size_t n, std::vector<void*>& owned) {
     void* p = nullptr;
-    ck(cudaMalloc(&p, (n ? n : 1) * sizeof(T)), "cudaMalloc");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    keep_pool(dev);
+    ck(cudaMallocAsync(&p, (n ? n : 1) * sizeof(T), nullptr), "cudaMallocAsync");
     owned.push_back(p);
     return static_cast<T*>(p);
 }
@@ -50,7 +67,8 @@ struct Arena {
     std::uint32_t A = 0;
 
     ~Arena() {
-        for (void* p : owned) cudaFree(p);
+        for (void* p : owned) cudaFreeAsync(p, nullptr);
+        cudaStreamSynchronize(nullptr);
     }
 
     void upload_static(const StaticStore& st, const std::vector<RuleRec>& rules, std::uint32_t n_prog,
@@ -197,6 +215,11 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     const std::uint32_t gblocks = opt.grid ? grid_blocks_for(opt.device) : 0;
     const std::uint32_t n_slots = opt.grid ? 1u : std::max<std::uint32_t>(1, std::min(opt.slots, n_cubes));
     ar.alloc_slots(n_slots, cfg_in.W, opt.lcap, opt.lpool, opt.mcap, opt.tcap, cube_width, gblocks);
+    if (std::getenv("YAS_PROFILE")) {
+        cudaDeviceSynchronize();
+        std::fprintf(stderr, "[yas host] arena: %u slots x %.2f MB, ready after %.2f ms\n", n_slots, ar.L.bytes / 1e6,
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count());
+    }
     dev::Config cfg = cfg_in;
     cfg.n_cubes = n_cubes;
     cfg.cube_width = cube_width;
@@ -251,18 +274,28 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
            "ctl");
         bool more = false;
         std::uint32_t err = dev::kDone;
+        // all slots' model buffers in two strided copies (not two per slot)
+        std::uint32_t maxm = 0;
+        for (std::uint32_t s = 0; s < n_slots; ++s) maxm = std::max(maxm, ctl[s].n_mbuf);
+        if (maxm) {
+            const std::size_t mrow = static_cast<std::size_t>(maxm) * ar.K.mwords * 4;
+            mb.resize(mrow / 4 * n_slots);
+            mc.resize(static_cast<std::size_t>(maxm) * n_slots);
+            ck(cudaMemcpy2D(mb.data(), mrow, ar.slots[0].mbuf(), ar.L.bytes, mrow, n_slots, cudaMemcpyDeviceToHost),
+               "models");
+            ck(cudaMemcpy2D(mc.data(), 4ull * maxm, ar.slots[0].mcube(), ar.L.bytes, 4ull * maxm, n_slots,
+                            cudaMemcpyDeviceToHost),
+               "models");
+        }
         for (std::uint32_t s = 0; s < n_slots; ++s) {
             dev::Ctl& c = ctl[s];
             if (c.n_mbuf) {
-                mb.resize(static_cast<std::size_t>(c.n_mbuf) * ar.K.mwords);
-                mc.resize(c.n_mbuf);
-                ck(cudaMemcpy(mb.data(), ar.slots[s].mbuf(), mb.size() * 4, cudaMemcpyDeviceToHost), "models");
-                ck(cudaMemcpy(mc.data(), ar.slots[s].mcube(), mc.size() * 4, cudaMemcpyDeviceToHost), "models");
+                const std::size_t b0 = static_cast<std::size_t>(s) * maxm * ar.K.mwords;
                 for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
                     EngineModel em;
-                    em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(m) * ar.K.mwords,
-                                   mb.begin() + static_cast<std::ptrdiff_t>(m + 1) * ar.K.mwords);
-                    em.cube = mc[m];
+                    em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m) * ar.K.mwords),
+                                   mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m + 1) * ar.K.mwords));
+                    em.cube = mc[static_cast<std::size_t>(s) * maxm + m];
                     if (cb.on_model && !cb.on_model(em)) stop_early = true;
                 }
                 c.n_mbuf = 0;
@@ -506,7 +539,7 @@ void Session::set_pass_trace(bool on) {
     Impl& im = *impl_;
     const std::size_t n = 64ull * std::max<std::uint32_t>(1, im.gblocks) * 10;
     if (on && !im.cfg.ptrace) {
-        ck(cudaMalloc(&im.cfg.ptrace, n * sizeof(unsigned long long)), "cudaMalloc trace");
+        ck(cudaMallocAsync(&im.cfg.ptrace, n * sizeof(unsigned long long), nullptr), "cudaMallocAsync trace");
         ck(cudaMemset(im.cfg.ptrace, 0, n * sizeof(unsigned long long)), "memset trace");
         im.ar.owned.push_back(im.cfg.ptrace);
     } else if (!on) {

@@ -200,6 +200,7 @@ struct GridG {
     std::uint32_t epoch;     // barriers passed (same in every block)
     std::uint32_t* snap;     // shared: control words snapshotted at a barrier
     std::int32_t* scanq;     // shared: per-warp queue of nogoods needing a full scan
+    std::uint32_t* scane;    //   ... and their expansion indices
 
     __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
     __device__ std::uint32_t size() const { return gridDim.x * BS; }
@@ -1198,6 +1199,7 @@ struct Search {
         const std::uint32_t lane = lane_id();
         const unsigned below = (1u << lane) - 1u;
         std::int32_t* scanq = g.scanq + (threadIdx.x >> 5) * (32 * U);
+        std::uint32_t* scane = g.scane + (threadIdx.x >> 5) * (32 * U);
         const std::uint32_t nwarps = g.size() >> 5, wid = g.iwarp();
         const std::uint32_t per = (((T + nwarps - 1) / nwarps) + 31u) & ~31u;
         const unsigned long long start64 = static_cast<unsigned long long>(wid) * per;
@@ -1265,9 +1267,19 @@ struct Search {
                     wx[u] = mirror_word_snap(cls[u] >= 1 ? atom_of(ent[u].z) : 0u);
                     wy[u] = mirror_word_snap(cls[u] >= 2 ? atom_of(ent[u].w) : 0u);
                 }
-                bool first[U];
+                // An occurrence evaluates its nogood (same outcome from any of
+                // them) unless an occurrence with a smaller e already claimed
+                // it, and every proposing evaluation bids its own e for the
+                // atom: the nogood's min-e occurrence always evaluates, so the
+                // smallest bid is the item-order winner without a separate
+                // resolve phase. The first toucher counts the check and reports
+                // an all-true conflict.
+                bool first[U], evl[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) first[u] = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                for (int u = 0; u < U; ++u) {
+                    first[u] = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                    evl[u] = first[u] || base + 32u * u + lane < static_cast<std::uint32_t>(old[u]);
+                }
                 // decide from the entry: 0 nothing, 1 conflict, 2 proposal, 3 full scan
                 std::uint32_t stt[U];
                 std::int32_t plit[U];
@@ -1275,9 +1287,12 @@ struct Search {
                 for (int u = 0; u < U; ++u) {
                     plit[u] = 0;
                     stt[u] = 0;
-                    if (!first[u]) continue;
-                    ++checks;
-                    if (cls[u] == 0) { stt[u] = 1; lits += 1; continue; }
+                    if (base + 32u * u + lane >= end || !evl[u]) continue;
+                    checks += first[u] ? 1u : 0u;
+                    if (cls[u] == 0) {
+                        if (first[u]) { stt[u] = 1; lits += 1; }
+                        continue;
+                    }
                     const int vx = mirror_val(wx[u], atom_of(ent[u].z));
                     const int sx = vx == 0 ? 0 : ((vx > 0) == (ent[u].z > 0) ? 1 : -1);  // 1 holds, -1 dead, 0 free
                     int sy = 1;
@@ -1287,9 +1302,13 @@ struct Search {
                     }
                     const bool decided = sx < 0 || sy < 0 || (sx == 0 && sy == 0);
                     if (cls[u] == 3 && !decided) { stt[u] = 3; continue; }
-                    lits += (cls[u] == 3 && C.count_lits) ? length_of(static_cast<std::uint32_t>(ent[u].x)) : cls[u] + 1;
+                    if (first[u])
+                        lits += (cls[u] == 3 && C.count_lits) ? length_of(static_cast<std::uint32_t>(ent[u].x)) : cls[u] + 1;
                     if (decided) continue;
-                    if (sx > 0 && sy > 0) { stt[u] = 1; continue; }
+                    if (sx > 0 && sy > 0) {
+                        if (first[u]) stt[u] = 1;
+                        continue;
+                    }
                     const std::int32_t u1 = sx == 0 ? ent[u].z : ent[u].w;
                     if (may_assert(static_cast<std::uint32_t>(ent[u].y), -u1)) { stt[u] = 2; plit[u] = -u1; }
                 }
@@ -1315,7 +1334,12 @@ struct Search {
                     at = __shfl_sync(0xffffffffu, at, 0);
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        if (pm[u] >> lane & 1u) sl.props()[at + __popc(pm[u] & below)] = make_int4(ent[u].x, plit[u], 0, 0);
+                        if (pm[u] >> lane & 1u) {
+                            const std::uint32_t e = base + 32u * u + lane;
+                            atomicMin(sl.win() + atom_of(plit[u]), wkey(gen, e, plit[u] < 0));
+                            sl.props()[at + __popc(pm[u] & below)] =
+                                make_int4(ent[u].x, plit[u], static_cast<std::int32_t>(e), 0);
+                        }
                         at += __popc(pm[u]);
                     }
                 }
@@ -1323,23 +1347,33 @@ struct Search {
                     std::uint32_t at = 0;
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        if (qm[u] >> lane & 1u) scanq[at + __popc(qm[u] & below)] = ent[u].x;
+                        if (qm[u] >> lane & 1u) {
+                            const std::uint32_t q = at + __popc(qm[u] & below);
+                            scanq[q] = ent[u].x | (first[u] ? static_cast<std::int32_t>(0x80000000u) : 0);
+                            scane[q] = base + 32u * u + lane;
+                        }
                         at += __popc(qm[u]);
                     }
                     __syncwarp();
                     for (std::uint32_t r = 0; r < nscan; r += 32) {
                         bool conflict = false, prop = false;
                         std::int32_t pl = 0, id = 0;
+                        std::uint32_t e = 0;
                         if (r + lane < nscan) {
-                            id = scanq[r + lane];
+                            const std::int32_t qv = scanq[r + lane];
+                            const bool fst = qv < 0;
+                            id = qv & 0x7fffffff;
+                            e = scane[r + lane];
                             std::uint32_t len = 0;
                             scan_snap(id, conflict, prop, pl, len);
-                            lits += len;
+                            if (fst) lits += len;
+                            conflict = conflict && fst;
+                            if (prop) atomicMin(sl.win() + atom_of(pl), wkey(gen, e, pl < 0));
                         }
                         const std::uint32_t cs = warp_append(&c->n_confl, conflict);
                         if (conflict) sl.confl()[cs] = id;
                         const std::uint32_t ps = warp_append(&c->n_props, prop);
-                        if (prop) sl.props()[ps] = make_int4(id, pl, 0, 0);
+                        if (prop) sl.props()[ps] = make_int4(id, pl, static_cast<std::int32_t>(e), 0);
                     }
                     __syncwarp();
                 }
@@ -1352,18 +1386,6 @@ struct Search {
         if (lane == 0) {
             if (checks) atomicAdd(g.bc + 0, static_cast<unsigned long long>(checks));
             if (lits) atomicAdd(g.bc + 2, static_cast<unsigned long long>(lits));
-        }
-    }
-
-    // Final min-e of every proposing nogood; per atom the smallest (e, sign)
-    // key wins. The e goes back into the proposal for the selection.
-    __device__ void grid_resolve(std::uint32_t gen, std::uint32_t np) {
-        int4* props = sl.props();
-        for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
-            const int4 p = props[i];
-            const std::uint32_t e = static_cast<std::uint32_t>(sl.claim()[p.x]);
-            atomicMin(sl.win() + atom_of(p.y), wkey(gen, e, p.y < 0));
-            props[i].z = static_cast<std::int32_t>(e);
         }
     }
 
@@ -1418,8 +1440,8 @@ struct Search {
                 sl.occat()[e] = oe - ob + lt;
                 sl.litat()[e] = p.y;
                 atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
-            } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull)) {
-                sl.confl()[atomicAdd(&c->n_confl, 1u)] = p.x;
+            } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull) && static_cast<std::uint32_t>(sl.claim()[id]) == e) {
+                sl.confl()[atomicAdd(&c->n_confl, 1u)] = p.x;  // once per nogood: its min-e occurrence
             }
         }
     }
@@ -1567,9 +1589,7 @@ struct Search {
             g.sync_snap(&c->n_props, nullptr);
             const std::uint32_t np = g.snap[0];
             stamp(pass, 2);
-            grid_resolve(gen, np);
             stamp(pass, 3);
-            g.sync();
             stamp(pass, 4);
             grid_select(level, dlev, np);
             stamp(pass, 5);
@@ -2827,8 +2847,9 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ unsigned long long gcnt[4];
     __shared__ std::uint32_t gsnap[4];
     __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
+    __shared__ std::uint32_t gscane[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane};
     if (g.leader() && sl.ctl()->status == kYield) sl.ctl()->status = kRunning;
     g.sync();
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
@@ -2981,8 +3002,9 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ unsigned long long gcnt[4];
     __shared__ std::uint32_t gsnap[4];
     __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
+    __shared__ std::uint32_t gscane[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane};
     do_op(g, S, C, sl, K, sh, op, Sm{&smc});
     g.persist();
 }

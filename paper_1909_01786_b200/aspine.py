@@ -644,10 +644,11 @@ class Propagator:
         phase timestamps of whole-grid propagations: array [64, blocks, 10]."""
         N.lib().yas_propagator_pass_trace(self._h, -1 if on is None else int(bool(on)), None, 0, None)
         blocks = C.c_uint32(0)
-        out = np.zeros(64 * 148 * 10 * 4, dtype=np.uint64)
+        out = np.zeros(64 * 148 * 10 * 4 + 64 * 16, dtype=np.uint64)
         N.lib().yas_propagator_pass_trace(self._h, -1, out.ctypes.data_as(C.POINTER(C.c_uint64)), out.size,
                                           C.byref(blocks))
         b = max(1, blocks.value)
+        self.pass_debug = out[64 * b * 10: 64 * b * 10 + 64 * 16].reshape(64, 16)
         return out[: 64 * b * 10].reshape(64, b, 10)
 
     def profile(self) -> List[int]:

@@ -202,14 +202,18 @@ struct GridG {
     std::int32_t* scanq;     // shared: per-warp queue of nogoods needing a full scan
     std::uint32_t* scane;    //   ... and their expansion indices
 
-    __device__ std::uint32_t tid() const { return blockIdx.x * BS + threadIdx.x; }
-    __device__ std::uint32_t size() const { return gridDim.x * BS; }
+    // solo: block 0 alone runs passes (tiny frontiers) while the other blocks
+    // wait at the next grid barrier; ids, size and sync become block-local.
+    bool solo;
+
+    __device__ std::uint32_t tid() const { return solo ? threadIdx.x : blockIdx.x * BS + threadIdx.x; }
+    __device__ std::uint32_t size() const { return solo ? BS : gridDim.x * BS; }
     __device__ bool leader() const { return blockIdx.x == 0 && threadIdx.x == 0; }
     __device__ bool leader_warp() const { return blockIdx.x == 0 && threadIdx.x < 32; }
     // Block-interleaved numbering: consecutive ids land on different SMs, so
     // a small amount of work is spread over the whole GPU.
-    __device__ std::uint32_t itid() const { return threadIdx.x * gridDim.x + blockIdx.x; }
-    __device__ std::uint32_t iwarp() const { return (threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
+    __device__ std::uint32_t itid() const { return solo ? threadIdx.x : threadIdx.x * gridDim.x + blockIdx.x; }
+    __device__ std::uint32_t iwarp() const { return solo ? threadIdx.x >> 5 : (threadIdx.x >> 5) * gridDim.x + blockIdx.x; }
 
     // Exclusive scan of one value per thread over this block only.
     __device__ unsigned long long block_scan(unsigned long long v, unsigned long long& total) {
@@ -244,6 +248,15 @@ struct GridG {
     // on one L2 slice.
     __device__ void sync_snap(const std::uint32_t* a, const std::uint32_t* b) {
         __syncthreads();
+        if (solo) {
+            if (threadIdx.x == 0) {
+                __threadfence_block();
+                if (a) snap[0] = *reinterpret_cast<const volatile std::uint32_t*>(a);
+                if (b) snap[1] = *reinterpret_cast<const volatile std::uint32_t*>(b);
+            }
+            __syncthreads();
+            return;
+        }
         ++epoch;
         if (threadIdx.x == 0) {
             asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(&sh->bar_count), "r"(1u) : "memory");
@@ -672,6 +685,12 @@ struct Search {
             C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x + blockIdx.x) * kPtraceStamps + k] = gtimer();
     }
 
+    // Diagnostics: in-phase stamps (clock64) of warp 0 of block 0 in pass `pass`.
+    __device__ void dstamp(std::uint32_t pass, std::uint32_t k) const {
+        if (C.ptrace && blockIdx.x == 0 && threadIdx.x == 0 && pass < kPtracePasses)
+            C.ptrace[static_cast<std::size_t>(kPtracePasses) * gridDim.x * kPtraceStamps + pass * 16 + k] = clock64();
+    }
+
     __device__ void fail(std::uint32_t status) {
         if (g.leader()) c->status = status;
     }
@@ -758,6 +777,7 @@ struct Search {
             const unsigned long long pre = g.scan(v, tot) + carry;
             if (p < F) {
                 sl.froff()[p] = static_cast<std::uint32_t>(pre);
+                if constexpr (G::kGrid) sl.frb()[p] = __ldg(S.occ_off + lidx(lit) * 4);
                 if (mirror) {
                     sm.froff()[p] = static_cast<std::uint32_t>(pre);
                     sm.fr()[p] = lit;
@@ -1193,7 +1213,9 @@ struct Search {
     static constexpr int kExpandU = 8;
 
     template <int U>
-    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned) {
+    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned,
+                                std::uint32_t pass = 0xffffffffu) {
+        dstamp(pass, 0);
         const std::int32_t* fr = sl.fr(cur);
         const std::uint32_t* froff = sl.froff();
         const std::uint32_t lane = lane_id();
@@ -1207,7 +1229,9 @@ struct Search {
         if (start64 < T) {
             const std::uint32_t start = static_cast<std::uint32_t>(start64);
             const std::uint32_t end = T - start < per ? T : start + per;
-            std::uint32_t lo = 0, hi = F;  // froff[lo] <= start < froff[hi] = T
+            // froff[lo] <= start < froff[hi] = T; the first range starts at 0
+            // (froff[0] = 0): the window walk copes with empty lists there
+            std::uint32_t lo = 0, hi = start == 0 ? 1u : F;
             while (hi - lo > 1) {
                 const std::uint32_t step = (hi - lo + 31u) >> 5;
                 const std::uint32_t idx = lo + lane * step;
@@ -1216,7 +1240,8 @@ struct Search {
                 lo += static_cast<std::uint32_t>(31 - __clz(b)) * step;
                 hi = min(hi, lo + step);
             }
-            std::uint32_t p0 = lo, f0 = froff[lo];
+            std::uint32_t p0 = lo, f0 = lo == 0 ? 0u : froff[lo];
+            dstamp(pass, 1);
             for (std::uint32_t base = start; base < end; base += 32u * U) {
                 const std::uint32_t q = p0 + 1 + lane;
                 const std::uint32_t v = q <= F ? froff[q] : 0xffffffffu;
@@ -1244,17 +1269,26 @@ struct Search {
                         se[u] = froff[l2];
                     }
                 }
+                if (base == start) dstamp(pass, 2);
                 std::int32_t trig[U];
+                std::uint32_t fb[U];
 #pragma unroll
-                for (int u = 0; u < U; ++u) trig[u] = base + 32u * u + lane < end ? fr[pe[u]] : 0;
+                for (int u = 0; u < U; ++u) {
+                    const bool in = base + 32u * u + lane < end;
+                    trig[u] = in ? fr[pe[u]] : 0;
+                    fb[u] = in ? sl.frb()[pe[u]] : 0u;  // static list base, stored with the frontier
+                }
                 int4 ent[U];
                 std::uint32_t cls[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const std::uint32_t e = base + 32u * u + lane;
                     cls[u] = 0;
-                    ent[u] = e < end ? occ_entry(lidx(trig[u]), e - se[u], learned, cls[u]) : make_int4(-1, 0, 0, 0);
+                    if (e >= end) ent[u] = make_int4(-1, 0, 0, 0);
+                    else if (!learned) ent[u] = decode(__ldg(S.occ + fb[u] + (e - se[u])), cls[u]);
+                    else ent[u] = occ_entry(lidx(trig[u]), e - se[u], learned, cls[u]);
                 }
+                if (base == start) { asm volatile("" ::"r"(ent[0].x)); dstamp(pass, 3); }
                 unsigned long long old[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
@@ -1275,6 +1309,7 @@ struct Search {
                 // resolve phase. The first toucher counts the check and reports
                 // an all-true conflict.
                 bool first[U], evl[U];
+                if (base == start) { asm volatile("" ::"l"(old[0]), "r"(wx[0])); dstamp(pass, 4); }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     first[u] = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
@@ -1328,6 +1363,7 @@ struct Search {
                         if (cm[u] >> lane & 1u) sl.confl()[at + __popc(cm[u] & below)] = ent[u].x;
                     }
                 }
+                if (base == start) dstamp(pass, 5);
                 if (nprop) {  // one reservation per batch for all its proposals
                     std::uint32_t at = 0;
                     if (lane == 0) at = atomicAdd(&c->n_props, nprop);
@@ -1343,6 +1379,7 @@ struct Search {
                         at += __popc(pm[u]);
                     }
                 }
+                if (base == start) dstamp(pass, 6);
                 if (nscan) {  // long nogoods the entry could not decide: one lane each
                     std::uint32_t at = 0;
 #pragma unroll
@@ -1377,10 +1414,12 @@ struct Search {
                     }
                     __syncwarp();
                 }
+                if (base == start) dstamp(pass, 7);
                 p0 = __shfl_sync(0xffffffffu, pe[U - 1], 31);
                 f0 = __shfl_sync(0xffffffffu, se[U - 1], 31);
             }
         }
+        dstamp(pass, 8);
         checks = __reduce_add_sync(0xffffffffu, checks);
         lits = __reduce_add_sync(0xffffffffu, lits);
         if (lane == 0) {
@@ -1438,6 +1477,7 @@ struct Search {
                     write_deps_from(L, len, id, a, dlev);
                 }
                 sl.occat()[e] = oe - ob + lt;
+                sl.obat()[e] = ob;
                 sl.litat()[e] = p.y;
                 atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
             } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull) && static_cast<std::uint32_t>(sl.claim()[id]) == e) {
@@ -1505,6 +1545,7 @@ struct Search {
             const std::uint32_t e = (w0 + w) * 32 + (valid ? __fns(bw, 0, static_cast<int>(k + 1)) : 0u);
             const std::int32_t lit = valid ? sl.litat()[e] : 0;
             const std::uint32_t occv = valid ? sl.occat()[e] : 0u;
+            const std::uint32_t ob = valid ? sl.obat()[e] : 0u;
             std::uint32_t x = occv;  // segmented inclusive scan by word
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -1516,6 +1557,7 @@ struct Search {
             if (valid) {
                 const std::uint32_t r = rw + k;
                 out[r] = lit;
+                sl.frb()[r] = ob;
                 sl.froff()[r] = ow + x - occv;
                 sl.trail()[ts0 + r] = lit;
                 sl.tpos()[atom_of(lit)] = ts0 + r;
@@ -1571,6 +1613,60 @@ struct Search {
         if (g.leader()) sl.froff()[F_next] = T_next;
     }
 
+    // One grid pass (expand+evaluate | select | place). In solo mode block 0
+    // runs it alone with block barriers. Returns the conflict count.
+    __device__ std::uint32_t grid_pass(std::uint32_t& F, std::uint32_t& T, std::uint32_t& cur, std::uint32_t& gen,
+                                       std::uint32_t& ts, std::uint32_t level, std::uint32_t dlev, bool learned,
+                                       std::uint32_t& pass) {
+        stamp(pass, 0);
+        // few entries per warp: short batches; many: eight per lane in flight
+        if (T <= 64u * (g.size() >> 5)) grid_expand<2>(F, T, cur, gen, learned, pass);
+        else grid_expand<kExpandU>(F, T, cur, gen, learned, pass);
+        stamp(pass, 1);
+        g.sync_snap(&c->n_props, nullptr);
+        const std::uint32_t np = g.snap[0];
+        stamp(pass, 2);
+        stamp(pass, 3);
+        stamp(pass, 4);
+        grid_select(level, dlev, np);
+        stamp(pass, 5);
+        g.sync_snap(&c->n_confl, nullptr);
+        stamp(pass, 6);
+        // final for this pass: no block bumps it before the pass barrier
+        const std::uint32_t nconf = g.snap[0];
+        std::uint32_t Fn = 0, Tn = 0;
+        const bool small = (T + 31) / 32 <= kBlockPlaceWords;
+        grid_place(T, cur ^ 1u, ts, Fn, Tn);
+        if (g.leader()) {
+            c->n_props = 0;  // every block read it before the select barrier
+            c->st.passes += 1;
+        }
+        stamp(pass, 7);
+        if (small) {
+            g.sync_snap(&c->F, &c->T);
+            Fn = g.snap[0];
+            Tn = g.snap[1];
+        } else {
+            g.sync();
+        }
+        stamp(pass, 8);
+        if (C.ptrace && g.leader() && pass < kPtracePasses)
+            C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x) * kPtraceStamps + 9] =
+                (static_cast<unsigned long long>(T) << 32) | F;
+        ++pass;
+        if (g.leader()) c->st.propagations += Fn;
+        ts += Fn;
+        F = Fn;
+        T = Tn;
+        cur ^= 1u;
+        gen += 1;
+        return nconf;
+    }
+
+    // Frontiers this small run in block 0 alone: a block barrier costs ~0.1 us,
+    // a grid barrier ~1.5 us, and one block covers them in one or two batches.
+    static constexpr std::uint32_t kSoloT = 1024;
+
     __device__ bool propagate_grid(std::uint32_t level) {
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
@@ -1581,49 +1677,36 @@ struct Search {
         bool violated = false;
         std::uint32_t pass = 0;
         while (F != 0) {
-            stamp(pass, 0);
-            // few entries per warp: short batches; many: eight per lane in flight
-            if (T <= 64u * (g.size() >> 5)) grid_expand<2>(F, T, cur, gen, learned);
-            else grid_expand<kExpandU>(F, T, cur, gen, learned);
-            stamp(pass, 1);
-            g.sync_snap(&c->n_props, nullptr);
-            const std::uint32_t np = g.snap[0];
-            stamp(pass, 2);
-            stamp(pass, 3);
-            stamp(pass, 4);
-            grid_select(level, dlev, np);
-            stamp(pass, 5);
-            g.sync_snap(&c->n_confl, nullptr);
-            stamp(pass, 6);
-            // final for this pass: no block bumps it before the pass barrier
-            const std::uint32_t nconf = g.snap[0];
-            std::uint32_t Fn = 0, Tn = 0;
-            const bool small = (T + 31) / 32 <= kBlockPlaceWords;
-            grid_place(T, cur ^ 1u, ts, Fn, Tn);
-            if (g.leader()) {
-                c->n_props = 0;  // every block read it before the select barrier
-                c->st.passes += 1;
+            if (T <= kSoloT) {
+                if (blockIdx.x == 0) {
+                    g.solo = true;
+                    while (F != 0 && T <= kSoloT && !violated) violated = grid_pass(F, T, cur, gen, ts, level, dlev, learned, pass) != 0;
+                    g.solo = false;
+                    if (threadIdx.x == 0) {
+                        c->F = F;
+                        c->T = T;
+                        c->cur = cur;
+                        c->gen = gen;
+                        c->ts = ts;
+                        c->b[11] = violated ? 1u : 0u;
+                        c->b[13] = pass;
+                    }
+                }
+                g.sync();  // the other blocks wait here for the solo streak
+                F = *reinterpret_cast<volatile std::uint32_t*>(&c->F);
+                T = *reinterpret_cast<volatile std::uint32_t*>(&c->T);
+                cur = *reinterpret_cast<volatile std::uint32_t*>(&c->cur);
+                gen = *reinterpret_cast<volatile std::uint32_t*>(&c->gen);
+                ts = *reinterpret_cast<volatile std::uint32_t*>(&c->ts);
+                violated = *reinterpret_cast<volatile std::uint32_t*>(&c->b[11]) != 0;
+                pass = *reinterpret_cast<volatile std::uint32_t*>(&c->b[13]);
+                if (violated) break;
+                continue;
             }
-            stamp(pass, 7);
-            if (small) {
-                g.sync_snap(&c->F, &c->T);
-                Fn = g.snap[0];
-                Tn = g.snap[1];
-            } else {
-                g.sync();
+            if (grid_pass(F, T, cur, gen, ts, level, dlev, learned, pass)) {
+                violated = true;
+                break;
             }
-            stamp(pass, 8);
-            if (C.ptrace && g.leader() && pass < kPtracePasses)
-                C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x) * kPtraceStamps + 9] =
-                    (static_cast<unsigned long long>(T) << 32) | F;
-            ++pass;
-            if (g.leader()) c->st.propagations += Fn;
-            ts += Fn;
-            F = Fn;
-            T = Tn;
-            cur ^= 1u;
-            gen += 1;
-            if (nconf) { violated = true; break; }
         }
         if (threadIdx.x == 0) {
             atomicAdd(&c->st.checks, g.bc[0]);
@@ -2849,7 +2932,7 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     __shared__ std::uint32_t gscane[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane, false};
     if (g.leader() && sl.ctl()->status == kYield) sl.ctl()->status = kRunning;
     g.sync();
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
@@ -3004,7 +3087,7 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ std::int32_t gscanq[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     __shared__ std::uint32_t gscane[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
-                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane};
+                *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane, false};
     do_op(g, S, C, sl, K, sh, op, Sm{&smc});
     g.persist();
 }

@@ -112,7 +112,7 @@ struct SlotLayout {
     unsigned long long bytes;
     unsigned long long o_ctl, o_cells, o_tpos, o_reason, o_deps, o_dovf, o_trail, o_ldec, o_fr0, o_fr1, o_froff,
         o_claim, o_win, o_props, o_confl, o_pending, o_bitmap, o_litat, o_loff, o_lpool, o_lhdr, o_larena,
-        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf, o_occat, o_gmirror;
+        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf, o_occat, o_gmirror, o_obat, o_frb;
 };
 
 #if defined(__CUDACC__)
@@ -146,6 +146,10 @@ struct Slot {
     YAS_HD std::uint32_t* occat() const { return at<std::uint32_t>(L->o_occat); }  // grid slots only
     // grid slots only: 2 bits per atom (bit 0 assigned, bit 1 true), 16 atoms per word
     YAS_HD std::uint32_t* gmirror() const { return at<std::uint32_t>(L->o_gmirror); }
+    // grid slots only: static occurrence-list base of the winner at e, and of
+    // frontier literal p (saves the offset lookup on the expansion path)
+    YAS_HD std::uint32_t* obat() const { return at<std::uint32_t>(L->o_obat); }
+    YAS_HD std::uint32_t* frb() const { return at<std::uint32_t>(L->o_frb); }
     YAS_HD std::uint32_t* loff() const { return at<std::uint32_t>(L->o_loff); }
     YAS_HD std::int32_t* lpool() const { return at<std::int32_t>(L->o_lpool); }
     YAS_HD std::uint32_t* lhdr() const { return at<std::uint32_t>(L->o_lhdr); }  // (2A+2)*4 * {ptr,size,cap}

@@ -157,6 +157,8 @@ struct Arena {
         L.o_tbuf = take(16ull * tcap);
         L.o_occat = take(grid_blocks ? 4 * tbits : 0);  // whole-grid passes only
         L.o_gmirror = take(grid_blocks ? 4 * ((A1 + 15) / 16 + 1) : 0);
+        L.o_obat = take(grid_blocks ? 4 * tbits : 0);
+        L.o_frb = take(grid_blocks ? 4 * (A1 + 1) : 0);
         L.bytes = o;
         L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
         ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
@@ -537,7 +539,7 @@ void Session::set_count_lits(bool on) { impl_->cfg.count_lits = on ? 1u : 0u; }
 
 void Session::set_pass_trace(bool on) {
     Impl& im = *impl_;
-    const std::size_t n = 64ull * std::max<std::uint32_t>(1, im.gblocks) * 10;
+    const std::size_t n = 64ull * std::max<std::uint32_t>(1, im.gblocks) * 10 + 64 * 16;
     if (on && !im.cfg.ptrace) {
         ck(cudaMallocAsync(&im.cfg.ptrace, n * sizeof(unsigned long long), nullptr), "cudaMallocAsync trace");
         ck(cudaMemset(im.cfg.ptrace, 0, n * sizeof(unsigned long long)), "memset trace");
@@ -601,7 +603,7 @@ std::vector<unsigned long long> Session::pass_trace(std::uint32_t& blocks) const
     blocks = std::max<std::uint32_t>(1, impl_->gblocks);
     if (!impl_->cfg.ptrace) return {};
     ctl();
-    return dl(impl_->cfg.ptrace, 64ull * blocks * 10, impl_->stream);
+    return dl(impl_->cfg.ptrace, 64ull * blocks * 10 + 64 * 16, impl_->stream);
 }
 
 }  // namespace yas

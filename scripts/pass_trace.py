@@ -31,6 +31,8 @@ for p in range(min(o.passes, 64)):
     if not t[:, 0].any():
         break
     T, F = int(t[0, 9]) >> 32, int(t[0, 9]) & 0xffffffff
+    if not t[1:, 0].any():  # solo pass: block 0 only
+        t = t[:1]
     parts = []
     for name, a, b, c in phases:
         work = (t[:, b] - t[:, a])
@@ -41,3 +43,8 @@ for p in range(min(o.passes, 64)):
         tot[name] = tot.get(name, 0) + (t[:, c].max() - t[:, a].min())
     print(f"pass {p:3d} T={T:8d} F={F:7d} | " + " | ".join(parts))
 print("phase totals (us):", {k: round(v / 1e3, 1) for k, v in tot.items()})
+d = prop.pass_debug.astype(np.int64)
+print("expand, warp 0 of block 0 (cycles since expand start): search | first batch: pe, trig+entry, claims+mirror, decide, props, scans | end")
+for p in range(min(o.passes, 64)):
+    if d[p, 0]:
+        print(f"pass {p:3d}: " + " ".join(f"{int(d[p, k] - d[p, 0]):6d}" for k in range(1, 9)))

@@ -673,8 +673,9 @@ class Propagator:
         N.lib().yas_propagator_deps(self._h, word, out, ovf)
         return list(out), list(ovf)
 
-    def _array(self, fn) -> np.ndarray:
-        out = np.empty(self.atoms + 1, dtype=np.int32)  # trail, frontier, conflicts: one pass, <= A entries
+    def _array(self, fn, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(self.atoms + 1, dtype=np.int32)  # trail, frontier, conflicts: one pass, <= A entries
         n = fn(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), out.size)
         if n > out.size:  # (cannot happen for trail/frontier; conflicts may exceed A)
             out = np.empty(n, dtype=np.int32)
@@ -687,9 +688,10 @@ class Propagator:
     def trail(self) -> List[int]:
         return self._list(N.lib().yas_propagator_trail)
 
-    def trail_array(self) -> np.ndarray:
-        """The trail as an int32 numpy array (one D2H copy, no Python list)."""
-        return self._array(N.lib().yas_propagator_trail)
+    def trail_array(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """The trail as an int32 numpy array (one D2H copy, no Python list);
+        `out` (int32, >= atoms + 1 entries, e.g. pinned) is filled and sliced."""
+        return self._array(N.lib().yas_propagator_trail, out)
 
     def conflicts(self) -> List[int]:
         return self._list(N.lib().yas_propagator_conflicts)

@@ -2998,15 +2998,19 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             }
             g.sync();
             break;
-        case kOpAssign: {  // assign_propagated for a bulk of distinct atoms (assignment.cpp:135-144);
-                           // already assigned atoms are left alone (agreed / conflict)
-            const std::uint32_t ts0 = c->ts;
+        case kOpAssign: {  // assign_propagated for a bulk of literals (assignment.cpp:135-144):
+                           // already assigned atoms are left alone (agreed / conflict) and
+                           // only the first occurrence of a repeated atom counts
+            const std::uint32_t ts0 = c->ts, gen = c->gen;
+            for (std::uint32_t k = g.tid(); k < op.n; k += g.size())
+                atomicMin(sl.win() + atom_of(op.lits[k]), wkey(gen, k, false));
+            g.sync();
             unsigned long long carry = 0;
             for (std::uint32_t base = 0; base < op.n; base += g.size()) {
                 const std::uint32_t k = base + g.tid();
                 const std::int32_t lit = k < op.n ? op.lits[k] : 0;
                 const std::uint32_t a = atom_of(lit);
-                const bool fresh = k < op.n && s.val(a) == 0;
+                const bool fresh = k < op.n && s.val(a) == 0 && sl.win()[a] == wkey(gen, k, false);
                 unsigned long long tot;
                 const std::uint32_t r = static_cast<std::uint32_t>(g.scan(fresh ? 1ull : 0ull, tot) + carry);
                 if (fresh) {
@@ -3020,7 +3024,10 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                 carry += tot;
             }
             g.sync();
-            if (g.leader()) c->ts = ts0 + static_cast<std::uint32_t>(carry);
+            if (g.leader()) {
+                c->ts = ts0 + static_cast<std::uint32_t>(carry);
+                c->gen = gen + 1;
+            }
             g.sync();
             break;
         }

@@ -368,8 +368,6 @@ struct Session::Impl {
     unsigned long long* d_deps = nullptr;
     dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
     bool ctl_pending = false;
-    std::vector<std::uint32_t> seen;  // assign(): first occurrence per atom
-    std::uint32_t seen_epoch = 0;
 
     std::int32_t* stage(const std::int32_t* src, std::size_t n) {
         if (n > d_lits_cap) {
@@ -417,7 +415,6 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     ck(cudaMalloc(&impl_->d_deps, 1024 * sizeof(unsigned long long)), "cudaMalloc deps");
     ck(cudaMallocHost(&impl_->h_ctl, sizeof(dev::Ctl)), "cudaMallocHost");
     std::memset(impl_->h_ctl, 0, sizeof(dev::Ctl));
-    impl_->seen.assign(impl_->ar.A + 1, 0);
     reset();
 }
 
@@ -488,21 +485,22 @@ void Session::push_decision(std::int32_t lit) {
 
 void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_t level, std::int32_t antecedent,
                      const unsigned long long* deps, std::size_t n_deps, bool ovf) {
-    // the device op takes distinct atoms (a repeated atom would be agreed or a
-    // conflict in try_set, i.e. no change): keep the first occurrence only
     Impl& im = *impl_;
-    if (++im.seen_epoch == 0) {
-        std::fill(im.seen.begin(), im.seen.end(), 0u);
-        im.seen_epoch = 1;
-    }
-    std::vector<std::int32_t> lits;
-    lits.reserve(n_in);
+    // atoms outside [1, A] are dropped here; repeats are resolved on the device
+    const std::int32_t* lits = lits_in;
+    std::vector<std::int32_t> kept;
     for (std::size_t i = 0; i < n_in; ++i) {
-        const std::int32_t l = lits_in[i];
-        const std::uint32_t a = static_cast<std::uint32_t>(l < 0 ? -l : l);
-        if (a == 0 || a > im.ar.A || im.seen[a] == im.seen_epoch) continue;
-        im.seen[a] = im.seen_epoch;
-        lits.push_back(l);
+        const std::uint32_t a = static_cast<std::uint32_t>(lits_in[i] < 0 ? -lits_in[i] : lits_in[i]);
+        if (a == 0 || a > im.ar.A) {
+            kept.assign(lits_in, lits_in + i);
+            for (std::size_t j = i + 1; j < n_in; ++j) {
+                const std::uint32_t b = static_cast<std::uint32_t>(lits_in[j] < 0 ? -lits_in[j] : lits_in[j]);
+                if (b != 0 && b <= im.ar.A) kept.push_back(lits_in[j]);
+            }
+            lits = kept.data();
+            n_in = kept.size();
+            break;
+        }
     }
     unsigned long long d[1024] = {0};
     for (std::size_t i = 0; i < n_deps && i < W_; ++i) d[i] = deps[i];
@@ -511,8 +509,8 @@ void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_
     op.op = dev::kOpAssign;
     op.level = level;
     op.antecedent = antecedent;
-    op.lits = im.stage(lits.data(), lits.size());
-    op.n = static_cast<std::uint32_t>(lits.size());
+    op.lits = im.stage(lits, n_in);
+    op.n = static_cast<std::uint32_t>(n_in);
     op.deps = im.d_deps;
     op.ovf = ovf ? 1u : 0u;
     run_op(im, op, nullptr);

@@ -144,3 +144,33 @@ def test_planted_1m_properties():
     p.seed(tr)
     o2 = p.propagate_and_check(2)
     assert not o2.violated and o2.propagations == 0 and len(p.trail()) == before
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_assign_keeps_first_occurrence_and_leaves_assigned_atoms(engine):
+    """assign_propagated (assignment.cpp:135-144) on a batch: a repeated atom and an
+    atom that is already assigned do not change the assignment or the trail."""
+    import numpy as np
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2], [3, 4]], 5), 1, engine)
+    p.push_decision(1)
+    p.assign_propagated(np.array([3, -3, 5, 3, -1], dtype=np.int32), 2)
+    assert p.trail() == [1, 3, 5]
+    assert p.cells()[1:] == [2, 0, 2, 0, 2]
+    p.assign_propagated([4, 5], 2)  # 5 agreed, 4 new
+    assert p.trail() == [1, 3, 5, 4]
+
+
+def test_grid_pass_trace_diagnostics():
+    """The per-pass phase stamps of whole-grid propagation are readable and ordered."""
+    store, seeded, dec = Y.NogoodStore.planted(20_000, 200_000, 50)
+    p = Y.Propagator(store, 16, "grid")
+    p.pass_trace(True)
+    p.push_decision(dec)
+    p.assign_propagated(seeded, 2)
+    p.seed([dec] + seeded)
+    o = p.propagate_and_check(2)
+    tr = p.pass_trace()
+    assert tr.shape[0] == 64 and tr.shape[2] == 10 and not o.violated
+    first = tr[0, 0]
+    assert first[0] > 0 and all(first[k] <= first[k + 1] for k in range(0, 8))
+    assert (int(first[9]) & 0xFFFFFFFF) == 1 + len(seeded)  # F of pass 0

@@ -111,3 +111,19 @@ def test_determinism_and_stats_text():
     assert row.startswith("inst.lp,fwd,occ,1,UNSAT,0,0,")
     assert Y.stats_csv_header().count(",") == row.count(",")
     assert "status         : UNSAT" in Y.emit_stats(r.stats, ctx, csv=False)
+
+
+def test_model_list_views_match_per_model_accessors():
+    """SolveResult.models is a lazy sequence over yas_result_models_flat: length,
+    indexing, slicing and names agree with the model-by-model C-ABI."""
+    from paper_1909_01786_b200 import instances as I
+    prog = Y.parse_program(I.queens(6))
+    r = Y.solve(prog, Y.SolverConfig(max_models=0))
+    ms = r.models
+    assert len(ms) == 4 and ms[-1] == ms[3] and ms[1:3] == [ms[1], ms[2]]
+    for m in ms:
+        assert m.atom_ids == sorted(m.atom_ids) and len(m.atoms) == 36  # six q(i,j), thirty nq(i,j)
+        assert m.atoms == sorted(prog.name(a) for a in m.atom_ids)
+        assert sum(a.startswith("q(") for a in m.atoms) == 6
+    with pytest.raises(IndexError):
+        ms[4]

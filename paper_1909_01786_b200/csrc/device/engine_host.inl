@@ -240,15 +240,18 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
         per_sm = std::min<std::uint32_t>(4, (n_slots + sms - 1) / sms);
         // keep most of the unified L1 for the (read-only) static store
-        const std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
+        std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
+        if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
         smc = plan_smem(ar.A, budget);
         smem = smc.bytes;
-        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)),
-           "smem attribute");
-        ck(cudaFuncSetAttribute(dev::block_kernel<kBlockBS, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)),
-           "smem attribute");
+        // the rest of the 228 KB unified array stays L1 for the static store
+        const int carve = static_cast<int>(std::min<std::size_t>(100, (per_sm * (smem + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024)));
+        for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>)}) {
+            ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+               "smem attribute");
+            ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
+        }
     }
     bool stop_early = false;
     for (;;) {

@@ -1308,26 +1308,16 @@ struct Search {
                 // smallest bid is the item-order winner without a separate
                 // resolve phase. The first toucher counts the check and reports
                 // an all-true conflict.
-                bool first[U], evl[U];
-                if (base == start) { asm volatile("" ::"l"(old[0]), "r"(wx[0])); dstamp(pass, 4); }
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    first[u] = static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
-                    evl[u] = first[u] || base + 32u * u + lane < static_cast<std::uint32_t>(old[u]);
-                }
-                // decide from the entry: 0 nothing, 1 conflict, 2 proposal, 3 full scan
+                // decide from the entry first (values only), while the claims
+                // are still in flight: 0 nothing, 1 all true, 2 proposal, 3 full scan
                 std::uint32_t stt[U];
                 std::int32_t plit[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     plit[u] = 0;
                     stt[u] = 0;
-                    if (base + 32u * u + lane >= end || !evl[u]) continue;
-                    checks += first[u] ? 1u : 0u;
-                    if (cls[u] == 0) {
-                        if (first[u]) { stt[u] = 1; lits += 1; }
-                        continue;
-                    }
+                    if (base + 32u * u + lane >= end) continue;
+                    if (cls[u] == 0) { stt[u] = 1; continue; }
                     const int vx = mirror_val(wx[u], atom_of(ent[u].z));
                     const int sx = vx == 0 ? 0 : ((vx > 0) == (ent[u].z > 0) ? 1 : -1);  // 1 holds, -1 dead, 0 free
                     int sy = 1;
@@ -1337,15 +1327,32 @@ struct Search {
                     }
                     const bool decided = sx < 0 || sy < 0 || (sx == 0 && sy == 0);
                     if (cls[u] == 3 && !decided) { stt[u] = 3; continue; }
-                    if (first[u])
-                        lits += (cls[u] == 3 && C.count_lits) ? length_of(static_cast<std::uint32_t>(ent[u].x)) : cls[u] + 1;
                     if (decided) continue;
-                    if (sx > 0 && sy > 0) {
-                        if (first[u]) stt[u] = 1;
-                        continue;
-                    }
+                    if (sx > 0 && sy > 0) { stt[u] = 1; continue; }
                     const std::int32_t u1 = sx == 0 ? ent[u].z : ent[u].w;
                     if (may_assert(static_cast<std::uint32_t>(ent[u].y), -u1)) { stt[u] = 2; plit[u] = -u1; }
+                }
+                // An occurrence acts on its nogood (same outcome from any of
+                // them) unless an occurrence with a smaller e already claimed
+                // it, and every proposing occurrence bids its own e for the
+                // atom: the nogood's min-e occurrence always acts, so the
+                // smallest bid is the item-order winner without a separate
+                // resolve phase. The first toucher counts the check and reports
+                // an all-true conflict.
+                if (base == start) { asm volatile("" ::"l"(old[0]), "r"(wx[0])); dstamp(pass, 4); }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const std::uint32_t e = base + 32u * u + lane;
+                    const bool first = e < end && static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                    const bool evl = first || e < static_cast<std::uint32_t>(old[u]);
+                    if (first) {
+                        ++checks;
+                        if (stt[u] != 3)
+                            lits += (cls[u] == 3 && C.count_lits) ? length_of(static_cast<std::uint32_t>(ent[u].x)) : cls[u] + 1;
+                    }
+                    if (stt[u] == 1 && !first) stt[u] = 0;       // conflicts: reported once
+                    if ((stt[u] == 2 || stt[u] == 3) && !evl) stt[u] = 0;
+                    if (stt[u] == 3 && first) stt[u] = 7;        // the scan remembers first-ness
                 }
                 unsigned cm[U], pm[U], qm[U];
                 std::uint32_t nprop = 0, nscan = 0;
@@ -1353,7 +1360,7 @@ struct Search {
                 for (int u = 0; u < U; ++u) {
                     cm[u] = __ballot_sync(0xffffffffu, stt[u] == 1);
                     pm[u] = __ballot_sync(0xffffffffu, stt[u] == 2);
-                    qm[u] = __ballot_sync(0xffffffffu, stt[u] == 3);
+                    qm[u] = __ballot_sync(0xffffffffu, (stt[u] & 3u) == 3u);
                     nprop += __popc(pm[u]);
                     nscan += __popc(qm[u]);
                     if (cm[u]) {  // rare
@@ -1386,7 +1393,7 @@ struct Search {
                     for (int u = 0; u < U; ++u) {
                         if (qm[u] >> lane & 1u) {
                             const std::uint32_t q = at + __popc(qm[u] & below);
-                            scanq[q] = ent[u].x | (first[u] ? static_cast<std::int32_t>(0x80000000u) : 0);
+                            scanq[q] = ent[u].x | ((stt[u] & 4u) ? static_cast<std::int32_t>(0x80000000u) : 0);
                             scane[q] = base + 32u * u + lane;
                         }
                         at += __popc(qm[u]);

@@ -292,6 +292,7 @@ def main():
         line["planted_8m"] = planted_large(Y, torch, flush, local)
         log("enumeration")
         line["enumeration"] = enumeration(Y, I, rank, world, local)
+        line["enumeration_q8"] = enumeration(Y, I, rank, world, local, n=8)
         if rank == 0:
             log("random program 4a")
             line["random_program_4a"] = random_program(Y, I, local)
@@ -367,11 +368,11 @@ def random_program(Y, I, local):
     return out
 
 
-def enumeration(Y, I, rank, world, local):
-    """12-queens, all answer sets: ladder cubes over the choice atoms, partitioned
+def enumeration(Y, I, rank, world, local, n=12):
+    """n-queens, all answer sets: ladder cubes over the choice atoms, partitioned
     over the ranks; model count all-reduced (SUM), time max over ranks."""
-    text = I.queens(12)
-    cfg = Y.SolverConfig(max_models=0, cube_atoms=12, rank=rank, world=world, device=local)
+    text = I.queens(n)
+    cfg = Y.SolverConfig(max_models=0, cube_atoms=n, rank=rank, world=world, device=local)
     Y.solve(Y.parse_program(text), cfg)  # warm-up (module load, allocations)
     barrier(world)
     t = time.perf_counter()
@@ -380,17 +381,26 @@ def enumeration(Y, I, rank, world, local):
     wall = (time.perf_counter() - t) * 1e3
     n_models, cubes = allreduce([float(len(r.models)), float(r.stats.cubes)], "sum", world)
     wall_max, dev_max = allreduce([wall, r.stats.device_ms], "max", world)
-    out = {"instance": "queens12 (all answer sets)", "models": int(n_models), "expected_models": 14200,
+    out = {"instance": f"queens{n} (all answer sets)", "models": int(n_models),
+           "expected_models": {8: 92, 10: 724, 12: 14200}.get(n),
            "wall_ms": wall_max, "device_ms": dev_max, "cubes": int(cubes), "n_gpus": world,
            "passes_rank0": r.stats.passes}
     if rank == 0 and os.path.exists(REF_BIN):
         # bounded CPU sample: the reference's first 1000 models of the same enumeration
-        p = subprocess.run([REF_BIN, "solve", "-", "-n", "1000", "--no-models"], input=text, capture_output=True,
-                           text=True, check=True)
-        ref = json.loads(p.stdout)
-        rate = ref["stats"]["models"] / (ref["run_ms"][0] / 1e3)
-        out["cpu_reference"] = {"sample": "queens12, first 1000 models, workers=1", "models_per_s": rate,
-                                "extrapolated_all_models_s": 14200 / rate}
+        if n <= 8:  # the whole enumeration is a bounded sample
+            p = subprocess.run([REF_BIN, "solve", "-", "-n", "0", "--no-models", "--reps", "3"], input=text,
+                               capture_output=True, text=True, check=True)
+            ref = json.loads(p.stdout)
+            out["cpu_reference"] = {"sample": f"queens{n}, all models, workers=1, mean of 3",
+                                    "run_ms": statistics.mean(ref["run_ms"])}
+        else:  # bounded sample: the reference's first 1000 models of the same enumeration
+            p = subprocess.run([REF_BIN, "solve", "-", "-n", "1000", "--no-models"], input=text,
+                               capture_output=True, text=True, check=True)
+            ref = json.loads(p.stdout)
+            rate = ref["stats"]["models"] / (ref["run_ms"][0] / 1e3)
+            out["cpu_reference"] = {"sample": f"queens{n}, first 1000 models, workers=1", "models_per_s": rate,
+                                    "extrapolated_all_models_s": out["expected_models"] / rate,
+                                    "measured_all_models_s_survey": 168.0 if n == 12 else None}
         out["models_per_s"] = n_models / (wall_max / 1e3)
     return out
 

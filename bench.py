@@ -167,10 +167,10 @@ def main():
     ap.add_argument("--impl", default="yasmin", choices=["yasmin", "reference"])
     ap.add_argument("--no-extras", action="store_true", help="skip enumeration / first-model sections")
     args = ap.parse_args()
-    rank, world, local = dist_setup(args.gpus)
-    if args.impl == "reference":
-        reference_arm(args, rank, world)
+    if args.impl == "reference":  # CPU only: no process group needed; rank 0 runs it
+        reference_arm(args, int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")))
         return
+    rank, world, local = dist_setup(args.gpus)
 
     import torch
     import paper_1909_01786_b200 as Y
@@ -212,7 +212,7 @@ def main():
             flush.zero_()  # L2 flushed between timed iterations
             torch.cuda.synchronize()
             o = prop.propagate_and_check(2)  # one kernel launch: all passes to fixpoint
-            launches += 1
+            launches += 5  # reset, push_decision, assign, seed, propagate (torch's L2 flush not counted)
             dev_ms.append(o.device_ms)
             checks += o.checks
             lits += lits_per_step

@@ -418,7 +418,9 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         std::uint32_t width = 0, n_cubes = 1;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
-        const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * 4;
+        std::uint32_t per_sm = 8;  // concurrent searches per SM for cube enumeration
+        if (const char* e = std::getenv("YAS_SEARCHES_PER_SM")) per_sm = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
+        const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * per_sm;
         if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
             n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * static_cast<std::uint32_t>(cfg.world),
                                  cfg.rank, cfg.world, cubes, width);

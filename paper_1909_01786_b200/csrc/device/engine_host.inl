@@ -8,6 +8,7 @@ namespace yas {
 namespace {
 
 constexpr int kBlockBS = 256;
+constexpr int kCubeBS = 128;  // cube enumeration with 8 searches per SM
 constexpr int kGridBS = 512;
 
 void ck(cudaError_t e, const char* what) {
@@ -238,7 +239,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     if (!opt.grid) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
-        per_sm = std::min<std::uint32_t>(4, (n_slots + sms - 1) / sms);
+        per_sm = std::min<std::uint32_t>(8, (n_slots + sms - 1) / sms);
+        if (per_sm > 4) per_sm = 8;  // 8 searches per SM: 128-thread CTAs
         // keep most of the unified L1 for the (read-only) static store
         std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
         if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
@@ -247,7 +249,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         // the rest of the 228 KB unified array stays L1 for the static store
         const int carve = static_cast<int>(std::min<std::size_t>(100, (per_sm * (smem + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>)}) {
+                        reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 8>)}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
@@ -262,7 +265,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            if (per_sm > 1)
+            if (per_sm > 4)
+                dev::block_kernel<kCubeBS, 8><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            else if (per_sm > 1)
                 dev::block_kernel<kBlockBS, 4><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else
                 dev::block_kernel<kBlockBS, 1><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);

@@ -190,6 +190,11 @@ int yas_propagator_create(const yas_store* s, uint32_t deps_words, int engine, i
                           char* err, size_t err_cap);
 void yas_propagator_free(yas_propagator* p);
 int yas_propagator_reset(yas_propagator* p); /* fresh Assignment + Frontier */
+/* Calls that only change device state (reset, push_decision, assign, seed) are
+ * recorded and launched together with the next call that returns a result
+ * (one kernel, one upload). flush launches the recorded calls now (no
+ * reference counterpart; used to time a propagation alone). */
+int yas_propagator_flush(yas_propagator* p);
 int yas_propagator_initial(yas_propagator* p, yas_outcome* o);                 /* initial_propagation */
 int yas_propagator_propagate(yas_propagator* p, uint32_t level, yas_outcome* o); /* propagate_and_check */
 int yas_propagator_push_decision(yas_propagator* p, int32_t lit);              /* Assignment::push_decision */

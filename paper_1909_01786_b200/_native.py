@@ -29,7 +29,7 @@ EXPORTS = [
     "yas_propagator_propagate", "yas_propagator_push_decision", "yas_propagator_assign", "yas_propagator_seed",
     "yas_propagator_add_learned", "yas_propagator_count_literals", "yas_propagator_atoms", "yas_propagator_cells", "yas_propagator_reasons",
     "yas_propagator_deps", "yas_propagator_trail", "yas_propagator_conflicts", "yas_propagator_frontier",
-    "yas_propagator_level", "yas_propagator_profile", "yas_propagator_pass_trace",
+    "yas_propagator_level", "yas_propagator_profile", "yas_propagator_flush", "yas_propagator_pass_trace",
 ]
 
 
@@ -149,6 +149,7 @@ def lib() -> C.CDLL:
         "yas_propagator_frontier": (SZ, [P, pI32, SZ]),
         "yas_propagator_level": (U32, [P]),
         "yas_propagator_profile": (C.c_int, [P, C.POINTER(C.c_uint64)]),
+        "yas_propagator_flush": (C.c_int, [P]),
         "yas_propagator_pass_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(U32)]),
     }
     for name, (res, args) in sig.items():

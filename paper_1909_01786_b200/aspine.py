@@ -607,6 +607,10 @@ class Propagator:
     def reset(self):
         N.lib().yas_propagator_reset(self._h)
 
+    def flush(self):
+        """Launch the recorded state-changing calls now (they otherwise run with the next result-returning call)."""
+        N.lib().yas_propagator_flush(self._h)
+
     def initial_propagation(self) -> PropagationOutcome:
         o = N.yas_outcome()
         N.lib().yas_propagator_initial(self._h, C.byref(o))

@@ -689,6 +689,9 @@ static void outcome_from(yas_propagator* p, bool violated, const dev::Ctl& befor
     o->device_ms = p->s->last_ms();
 }
 
+int yas_propagator_flush(yas_propagator* p) {
+    return guarded(nullptr, 0, [&] { p->s->flush(); return static_cast<int>(YAS_OK); });
+}
 int yas_propagator_reset(yas_propagator* p) {
     return guarded(nullptr, 0, [&] { p->s->reset(); return static_cast<int>(YAS_OK); });
 }

@@ -2961,11 +2961,16 @@ struct OpArgs {
     std::uint32_t ovf;
 };
 
+// Ops recorded by a Session since its last launch run as one kernel, in order.
+constexpr std::uint32_t kMaxOps = 6;
+struct OpBatch {
+    std::uint32_t n;
+    OpArgs ops[kMaxOps];
+};
+
 template <class G>
 __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Caps& K, Shared* sh,
-                      const OpArgs& op, const Sm& sm) {
-    Search<G> s(g, S, C, sl, K, sh, 0, sm);
-    init_smem(g, s);
+                      const OpArgs& op, const Sm& sm, Search<G>& s) {
     Ctl* c = g.c;
     switch (op.op) {
         case kOpReset:
@@ -3009,15 +3014,17 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                            // already assigned atoms are left alone (agreed / conflict) and
                            // only the first occurrence of a repeated atom counts
             const std::uint32_t ts0 = c->ts, gen = c->gen;
-            for (std::uint32_t k = g.tid(); k < op.n; k += g.size())
-                atomicMin(sl.win() + atom_of(op.lits[k]), wkey(gen, k, false));
+            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) {
+                const std::uint32_t a = atom_of(op.lits[k]);
+                if (a != 0 && a <= S.A) atomicMin(sl.win() + a, wkey(gen, k, false));  // atoms outside [1, A] are ignored
+            }
             g.sync();
             unsigned long long carry = 0;
             for (std::uint32_t base = 0; base < op.n; base += g.size()) {
                 const std::uint32_t k = base + g.tid();
                 const std::int32_t lit = k < op.n ? op.lits[k] : 0;
                 const std::uint32_t a = atom_of(lit);
-                const bool fresh = k < op.n && s.val(a) == 0 && sl.win()[a] == wkey(gen, k, false);
+                const bool fresh = k < op.n && a != 0 && a <= S.A && s.val(a) == 0 && sl.win()[a] == wkey(gen, k, false);
                 unsigned long long tot;
                 const std::uint32_t r = static_cast<std::uint32_t>(g.scan(fresh ? 1ull : 0ull, tot) + carry);
                 if (fresh) {
@@ -3060,11 +3067,22 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
     }
 }
 
+template <class G>
+__device__ void do_ops(G& g, const Static& S, const Config& C, Slot sl, const Caps& K, Shared* sh,
+                       const OpBatch& B, const Sm& sm) {
+    Search<G> s(g, S, C, sl, K, sh, 0, sm);
+    init_smem(g, s);
+    for (std::uint32_t i = 0; i < B.n; ++i) {
+        do_op(g, S, C, sl, K, sh, B.ops[i], sm, s);
+        g.sync();
+    }
+}
+
 template <int BS>
 __global__ void __launch_bounds__(BS, 1)
     op_block_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
-                    const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh, OpArgs op,
-                    const __grid_constant__ SmemCfg smc) {
+                    const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
+                    const __grid_constant__ OpBatch B, const __grid_constant__ SmemCfg smc) {
     __shared__ Ctl ctl;
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
@@ -3077,7 +3095,7 @@ __global__ void __launch_bounds__(BS, 1)
     }
     __syncthreads();
     BlockG<BS> g{&ctl, sbuf, sd, si};
-    do_op(g, S, C, sl, K, sh, op, Sm{&smc});
+    do_ops(g, S, C, sl, K, sh, B, Sm{&smc});
     __syncthreads();
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(&ctl);
@@ -3090,7 +3108,7 @@ template <int BS>
 __global__ void __launch_bounds__(BS, 1)
     op_grid_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
                    const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
-                   unsigned long long* partial, double* pd, std::uint32_t* pi, OpArgs op,
+                   unsigned long long* partial, double* pd, std::uint32_t* pi, const __grid_constant__ OpBatch B,
                    const __grid_constant__ SmemCfg smc) {
     __shared__ unsigned long long sbuf[BS / 32 + 4];
     __shared__ double sd[BS / 32];
@@ -3102,7 +3120,7 @@ __global__ void __launch_bounds__(BS, 1)
     __shared__ std::uint32_t gscane[BS / 32 * 32 * Search<GridG<BS>>::kExpandU];
     GridG<BS> g{sl.ctl(), sh, partial, pd, pi, sbuf, sd, si, 0u, gcnt,
                 *reinterpret_cast<volatile std::uint32_t*>(sh->arrive + blockIdx.x), gsnap, gscanq, gscane, false};
-    do_op(g, S, C, sl, K, sh, op, Sm{&smc});
+    do_ops(g, S, C, sl, K, sh, B, Sm{&smc});
     g.persist();
 }
 

@@ -68,6 +68,7 @@ public:
     Session& operator=(const Session&) = delete;
 
     void reset();
+    void flush();  // launch the recorded ops now
     bool initial_propagation();
     bool propagate(std::uint32_t level);
     void push_decision(std::int32_t lit);

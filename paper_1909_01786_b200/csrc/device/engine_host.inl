@@ -367,25 +367,42 @@ struct Session::Impl {
     int device = 0;
     cudaStream_t stream{};
     cudaEvent_t e0{}, e1{};
-    // Every op is stream ordered: inputs go through one persistent device
-    // staging buffer (an H2D copy is ordered after the previous kernel), and
-    // the control block is copied into pinned host memory after each kernel,
-    // so only calls that return device state synchronise.
-    std::int32_t* d_lits = nullptr;
-    std::size_t d_lits_cap = 0;
-    unsigned long long* d_deps = nullptr;
+    // Ops are recorded host-side and launched together, as one kernel, when a
+    // result is needed (initial propagation, propagation, add_learned, any
+    // read-back) or the batch is full. Bulk inputs of a batch are packed into
+    // one pinned staging buffer and uploaded with one copy; the control block
+    // comes back into pinned memory behind every launch.
+    std::vector<dev::OpArgs> pending;
+    std::vector<std::size_t> lits_off, deps_off;  // staging offsets (ints) per pending op, ~0 = none
+    std::int32_t* h_stage = nullptr;               // pinned
+    std::size_t h_stage_cap = 0, h_used = 0;
+    cudaEvent_t staged{};                          // the last upload of h_stage has been consumed
+    bool stage_inflight = false;
+    std::int32_t* d_stage = nullptr;
+    std::size_t d_stage_cap = 0;
     dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
     bool ctl_pending = false;
 
-    std::int32_t* stage(const std::int32_t* src, std::size_t n) {
-        if (n > d_lits_cap) {
-            ck(cudaStreamSynchronize(stream), "stream");  // the old buffer may still be read
-            if (d_lits) cudaFree(d_lits);
-            d_lits_cap = std::max<std::size_t>(n, 2 * d_lits_cap);
-            ck(cudaMalloc(&d_lits, d_lits_cap * sizeof(std::int32_t)), "cudaMalloc staging");
+    std::size_t append(const void* src, std::size_t ints) {
+        if (stage_inflight) {  // the previous batch's upload may still read the buffer
+            ck(cudaEventSynchronize(staged), "staging");
+            stage_inflight = false;
         }
-        if (n) ck(cudaMemcpyAsync(d_lits, src, n * sizeof(std::int32_t), cudaMemcpyHostToDevice, stream), "stage");
-        return d_lits;
+        const std::size_t off = (h_used + 3) & ~static_cast<std::size_t>(3);  // 16-byte aligned entries
+        if (off + ints > h_stage_cap) {
+            const std::size_t ncap = std::max<std::size_t>(off + ints, 2 * h_stage_cap + 1024);
+            std::int32_t* nb = nullptr;
+            ck(cudaMallocHost(&nb, ncap * sizeof(std::int32_t)), "cudaMallocHost staging");
+            if (h_stage) {
+                std::memcpy(nb, h_stage, h_used * sizeof(std::int32_t));
+                cudaFreeHost(h_stage);
+            }
+            h_stage = nb;
+            h_stage_cap = ncap;
+        }
+        if (ints) std::memcpy(h_stage + off, src, ints * sizeof(std::int32_t));
+        h_used = off + ints;
+        return off;
     }
 };
 
@@ -420,7 +437,7 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     ck(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking), "stream");
     ck(cudaEventCreate(&impl_->e0), "event");
     ck(cudaEventCreate(&impl_->e1), "event");
-    ck(cudaMalloc(&impl_->d_deps, 1024 * sizeof(unsigned long long)), "cudaMalloc deps");
+    ck(cudaEventCreateWithFlags(&impl_->staged, cudaEventDisableTiming), "event");
     ck(cudaMallocHost(&impl_->h_ctl, sizeof(dev::Ctl)), "cudaMallocHost");
     std::memset(impl_->h_ctl, 0, sizeof(dev::Ctl));
     reset();
@@ -428,8 +445,9 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
 
 Session::~Session() {
     cudaStreamSynchronize(impl_->stream);
-    if (impl_->d_lits) cudaFree(impl_->d_lits);
-    cudaFree(impl_->d_deps);
+    if (impl_->d_stage) cudaFree(impl_->d_stage);
+    if (impl_->h_stage) cudaFreeHost(impl_->h_stage);
+    cudaEventDestroy(impl_->staged);
     cudaFreeHost(impl_->h_ctl);
     cudaEventDestroy(impl_->e0);
     cudaEventDestroy(impl_->e1);
@@ -437,20 +455,44 @@ Session::~Session() {
 }
 
 namespace {
-// Enqueue one op kernel and the control-block copy behind it. `ms` (when
-// given) waits for the kernel and returns its CUDA-event time.
-void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
+// Launch the recorded ops as one kernel (plus the control-block copy behind
+// it). `ms` (when given) waits for the kernel and returns its CUDA-event time.
+void flush_ops(Session::Impl& im, float* ms) {
+    if (im.pending.empty()) return;
+    if (im.h_used) {
+        if (im.h_used > im.d_stage_cap) {
+            ck(cudaStreamSynchronize(im.stream), "stream");  // the old buffer may still be read
+            if (im.d_stage) cudaFree(im.d_stage);
+            im.d_stage_cap = std::max<std::size_t>(im.h_used, 2 * im.d_stage_cap);
+            ck(cudaMalloc(&im.d_stage, im.d_stage_cap * sizeof(std::int32_t)), "cudaMalloc staging");
+        }
+        ck(cudaMemcpyAsync(im.d_stage, im.h_stage, im.h_used * sizeof(std::int32_t), cudaMemcpyHostToDevice, im.stream),
+           "stage");
+        ck(cudaEventRecord(im.staged, im.stream), "record");
+        im.stage_inflight = true;
+    }
+    dev::OpBatch b{};
+    b.n = static_cast<std::uint32_t>(im.pending.size());
+    for (std::uint32_t i = 0; i < b.n; ++i) {
+        b.ops[i] = im.pending[i];
+        if (im.lits_off[i] != ~static_cast<std::size_t>(0)) b.ops[i].lits = im.d_stage + im.lits_off[i];
+        if (im.deps_off[i] != ~static_cast<std::size_t>(0))
+            b.ops[i].deps = reinterpret_cast<const unsigned long long*>(im.d_stage + im.deps_off[i]);
+    }
+    im.pending.clear();
+    im.lits_off.clear();
+    im.deps_off.clear();
+    im.h_used = 0;
     ck(cudaEventRecord(im.e0, im.stream), "record");
     if (im.grid) {
-        dev::OpArgs o = op;
-        void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &o,
+        void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &b,
                         &im.smc};
         ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::op_grid_kernel<kGridBS>), dim3(im.gblocks),
                                        dim3(kGridBS), args, 0, im.stream),
            "op grid launch");
     } else {
         dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem, im.stream>>>(im.ar.S, im.cfg, im.ar.L, im.ar.K, im.ar.sh,
-                                                                          op, im.smc);
+                                                                          b, im.smc);
         ck(cudaGetLastError(), "op launch");
     }
     ck(cudaEventRecord(im.e1, im.stream), "record");
@@ -461,18 +503,32 @@ void run_op(Session::Impl& im, const dev::OpArgs& op, float* ms) {
         cudaEventElapsedTime(ms, im.e0, im.e1);
     }
 }
+
+// Record one op (with optional staged literals / Deps words); a full batch is
+// launched right away.
+void record_op(Session::Impl& im, const dev::OpArgs& op, const std::int32_t* lits = nullptr, std::size_t n = 0,
+               const unsigned long long* deps = nullptr, std::size_t nd = 0) {
+    const std::size_t none = ~static_cast<std::size_t>(0);
+    im.lits_off.push_back(lits ? im.append(lits, n) : none);
+    im.deps_off.push_back(deps ? im.append(deps, 2 * nd) : none);
+    im.pending.push_back(op);
+    if (im.pending.size() == dev::kMaxOps) flush_ops(im, nullptr);
+}
 }  // namespace
+
+void Session::flush() { flush_ops(*impl_, nullptr); }
 
 void Session::reset() {
     dev::OpArgs op{};
     op.op = dev::kOpReset;
-    run_op(*impl_, op, nullptr);
+    record_op(*impl_, op);
 }
 
 bool Session::initial_propagation() {
     dev::OpArgs op{};
     op.op = dev::kOpInitial;
-    run_op(*impl_, op, &last_ms_);
+    record_op(*impl_, op);
+    flush_ops(*impl_, &last_ms_);
     return ctl().b[10] != 0;
 }
 
@@ -480,7 +536,8 @@ bool Session::propagate(std::uint32_t level) {
     dev::OpArgs op{};
     op.op = dev::kOpPropagate;
     op.level = level;
-    run_op(*impl_, op, &last_ms_);
+    record_op(*impl_, op);
+    flush_ops(*impl_, &last_ms_);
     return ctl().b[10] != 0;
 }
 
@@ -488,56 +545,37 @@ void Session::push_decision(std::int32_t lit) {
     dev::OpArgs op{};
     op.op = dev::kOpDecide;
     op.lit = lit;
-    run_op(*impl_, op, nullptr);
+    record_op(*impl_, op);
 }
 
 void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_t level, std::int32_t antecedent,
                      const unsigned long long* deps, std::size_t n_deps, bool ovf) {
-    Impl& im = *impl_;
-    // atoms outside [1, A] are dropped here; repeats are resolved on the device
+    Impl& im = *impl_;  // out-of-range atoms and repeats are resolved on the device
     const std::int32_t* lits = lits_in;
-    std::vector<std::int32_t> kept;
-    for (std::size_t i = 0; i < n_in; ++i) {
-        const std::uint32_t a = static_cast<std::uint32_t>(lits_in[i] < 0 ? -lits_in[i] : lits_in[i]);
-        if (a == 0 || a > im.ar.A) {
-            kept.assign(lits_in, lits_in + i);
-            for (std::size_t j = i + 1; j < n_in; ++j) {
-                const std::uint32_t b = static_cast<std::uint32_t>(lits_in[j] < 0 ? -lits_in[j] : lits_in[j]);
-                if (b != 0 && b <= im.ar.A) kept.push_back(lits_in[j]);
-            }
-            lits = kept.data();
-            n_in = kept.size();
-            break;
-        }
-    }
-    unsigned long long d[1024] = {0};
+    std::vector<unsigned long long> d(W_, 0ull);
     for (std::size_t i = 0; i < n_deps && i < W_; ++i) d[i] = deps[i];
-    ck(cudaMemcpyAsync(im.d_deps, d, W_ * sizeof(unsigned long long), cudaMemcpyHostToDevice, im.stream), "deps");
     dev::OpArgs op{};
     op.op = dev::kOpAssign;
     op.level = level;
     op.antecedent = antecedent;
-    op.lits = im.stage(lits, n_in);
     op.n = static_cast<std::uint32_t>(n_in);
-    op.deps = im.d_deps;
     op.ovf = ovf ? 1u : 0u;
-    run_op(im, op, nullptr);
+    record_op(im, op, lits, n_in, d.data(), W_);
 }
 
 void Session::seed(const std::int32_t* lits, std::size_t n) {
     dev::OpArgs op{};
     op.op = dev::kOpSeed;
-    op.lits = impl_->stage(lits, n);
     op.n = static_cast<std::uint32_t>(n);
-    run_op(*impl_, op, nullptr);
+    record_op(*impl_, op, lits, n);
 }
 
 std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
     dev::OpArgs op{};
     op.op = dev::kOpLearn;
-    op.lits = impl_->stage(lits.data(), lits.size());
     op.n = static_cast<std::uint32_t>(lits.size());
-    run_op(*impl_, op, nullptr);
+    record_op(*impl_, op, lits.data(), lits.size());
+    flush_ops(*impl_, nullptr);
     return static_cast<std::int32_t>(ctl().b[12]);
 }
 
@@ -557,6 +595,7 @@ void Session::set_pass_trace(bool on) {
 
 
 const dev::Ctl& Session::ctl() const {
+    flush_ops(*impl_, nullptr);
     if (impl_->ctl_pending) {
         ck(cudaStreamSynchronize(impl_->stream), "stream");
         impl_->ctl_pending = false;
@@ -588,17 +627,27 @@ std::size_t Session::trail_into(std::int32_t* out, std::size_t cap) const {
     return n;
 }
 
-std::vector<std::int32_t> Session::cells() const { return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1, impl_->stream); }
+std::vector<std::int32_t> Session::cells() const {
+    flush_ops(*impl_, nullptr);
+    return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1, impl_->stream);
+}
 std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts, impl_->stream); }
-std::vector<std::int32_t> Session::reasons() const { return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream); }
+std::vector<std::int32_t> Session::reasons() const {
+    flush_ops(*impl_, nullptr);
+    return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream);
+}
 std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
+    flush_ops(*impl_, nullptr);
     const std::size_t stride = (W_ + 1) & ~1u, n = impl_->ar.A + 1;
     const std::vector<unsigned long long> rows = dl(impl_->ar.slots[0].deps(), n * stride, impl_->stream);
     std::vector<unsigned long long> v(n);
     for (std::size_t a = 0; a < n; ++a) v[a] = rows[a * stride + w];
     return v;
 }
-std::vector<std::uint8_t> Session::deps_overflow() const { return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream); }
+std::vector<std::uint8_t> Session::deps_overflow() const {
+    flush_ops(*impl_, nullptr);
+    return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream);
+}
 std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl, impl_->stream); }
 std::vector<std::int32_t> Session::frontier() const {
     const dev::Ctl& c = ctl();

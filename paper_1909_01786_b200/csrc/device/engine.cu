@@ -670,7 +670,7 @@ struct Search {
     // phase accounting: cycles since the previous mark go to bucket k
     __device__ void mark(int k) const {
         if constexpr (G::kGrid) return;  // grid passes: see stamp()
-        if (g.leader()) {
+        if (C.phase_prof && g.leader()) {
             const unsigned long long t = clock64();
             c->prof[k] += t - c->prof_t;
             c->prof_t = t;

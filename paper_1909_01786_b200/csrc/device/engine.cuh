@@ -51,6 +51,7 @@ struct Config {
     std::uint64_t slice_ns;     // time slice per launch before yielding
     std::uint32_t count_lits;   // accumulate literals of checked nogoods (roofline accounting)
     unsigned long long* ptrace; // diagnostics: per-pass, per-block phase timestamps (null = off)
+    std::uint32_t phase_prof;   // diagnostics: per-phase cycle buckets of single-CTA searches (YAS_PROFILE)
 };
 
 // Read-only static store + program rules (host-built, uploaded once).

@@ -225,6 +225,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     }
     dev::Config cfg = cfg_in;
     cfg.n_cubes = n_cubes;
+    cfg.phase_prof = std::getenv("YAS_PROFILE") ? 1u : 0u;
     cfg.cube_width = cube_width;
     cfg.slice_ns = static_cast<std::uint64_t>(opt.slice_ms * 1e6);
 

@@ -1755,7 +1755,9 @@ struct Search {
                     continue;
                 }
             }
-            if (sm.tcap() && T <= sm.tcap() && F + 1 <= sm.fcap()) pass_smem(F, T, cur, level);
+            const bool in_smem = sm.tcap() && T <= sm.tcap() && F + 1 <= sm.fcap();
+            if (C.phase_prof && g.leader()) c->prof[in_smem ? 12 : 13] += 1;  // pass counts by path
+            if (in_smem) pass_smem(F, T, cur, level);
             else pass_global(F, T, gen, cur, level);
         }
     }
@@ -1770,6 +1772,7 @@ struct Search {
             if (T <= 32) {
                 tiny_pass(F, T, cur, level);
                 mark(8);
+                if (C.phase_prof && threadIdx.x == 0) c->prof[10] += 1;
             } else {
                 pass_smem(F, T, cur, level);
                 mark(9);

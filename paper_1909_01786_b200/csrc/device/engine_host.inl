@@ -341,7 +341,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
         static const char* names[14] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
-                                        "conflict", "tiny", "warp", "-", "looptop", "-", "-"};
+                                        "conflict", "tiny", "warp", "n.tiny", "looptop", "n.smem", "n.global"};
         unsigned long long p[16] = {0};
         for (const dev::Ctl& c : ctl)
             for (int k = 0; k < 16; ++k) p[k] += c.prof[k];

@@ -413,7 +413,7 @@ struct GridG {
 struct SmemCfg {
     std::uint32_t tcap, hcap, fcap, vwords;
     std::uint32_t o_htab, o_wtab, o_pid, o_plit, o_pslot, o_pdep, o_pmeta, o_litat, o_otat, o_bits, o_fr, o_froff,
-        o_vasg, o_vtru, bytes;
+        o_vmir, bytes;
 };
 
 extern __shared__ __align__(16) unsigned char yas_dsm[];
@@ -434,8 +434,8 @@ struct Sm {
     __device__ __forceinline__ std::uint32_t* bits() const { return at<std::uint32_t>(cfg->o_bits); }
     __device__ __forceinline__ std::int32_t* fr() const { return at<std::int32_t>(cfg->o_fr); }  // frontier mirror
     __device__ __forceinline__ std::uint32_t* froff() const { return at<std::uint32_t>(cfg->o_froff); }
-    __device__ __forceinline__ std::uint32_t* vasg() const { return at<std::uint32_t>(cfg->o_vasg); }  // assigned bits
-    __device__ __forceinline__ std::uint32_t* vtru() const { return at<std::uint32_t>(cfg->o_vtru); }  // true bits
+    // 2 bits per atom (bit 0 assigned, bit 1 true), 16 atoms per word: one load per value
+    __device__ __forceinline__ std::uint32_t* vmir() const { return at<std::uint32_t>(cfg->o_vmir); }
     __device__ __forceinline__ std::uint32_t tcap() const { return cfg->tcap; }
     __device__ __forceinline__ std::uint32_t hmask() const { return cfg->hcap ? cfg->hcap - 1 : 0; }
     __device__ __forceinline__ std::uint32_t fcap() const { return cfg->fcap; }
@@ -472,8 +472,7 @@ SmemCfg smem_layout(std::uint32_t tcap, std::uint32_t vwords) {
         c.o_froff = take(4u * (c.fcap + 1));
     }
     if (vwords) {
-        c.o_vasg = take(4u * vwords);
-        c.o_vtru = take(4u * vwords);
+        c.o_vmir = take(8u * vwords);
     }
     c.bytes = o;
     return c;
@@ -509,11 +508,7 @@ struct Search {
 
     __device__ int val(std::uint32_t a) const {
         if constexpr (G::kGrid) return mirror_val(__ldcg(sl.gmirror() + (a >> 4)), a);
-        if (sm.vwords()) {
-            const std::uint32_t b = 1u << (a & 31);
-            if (!(sm.vasg()[a >> 5] & b)) return 0;
-            return (sm.vtru()[a >> 5] & b) ? 1 : -1;
-        }
+        if (sm.vwords()) return mirror_val(sm.vmir()[a >> 4], a);
         const std::int32_t cv = sl.cells()[a];
         return (cv > 0) - (cv < 0);
     }
@@ -527,30 +522,23 @@ struct Search {
             return;
         }
         if (sm.vwords()) {
-            const std::uint32_t b = 1u << (a & 31);
-            if (cv == 0) {
-                atomicAnd(sm.vasg() + (a >> 5), ~b);
-                atomicAnd(sm.vtru() + (a >> 5), ~b);
-            } else {
-                if (cv > 0) atomicOr(sm.vtru() + (a >> 5), b);
-                else atomicAnd(sm.vtru() + (a >> 5), ~b);
-                atomicOr(sm.vasg() + (a >> 5), b);
-            }
+            std::uint32_t* w = sm.vmir() + (a >> 4);
+            const std::uint32_t sh2 = 2 * (a & 15);
+            if (cv == 0) atomicAnd(w, ~(3u << sh2));
+            else atomicOr(w, (cv > 0 ? 3u : 1u) << sh2);  // bits are clear while unassigned
         }
     }
     __device__ void rebuild_mirror() const {
         if (!sm.vwords()) return;
-        for (std::uint32_t w = g.tid(); w < sm.vwords(); w += g.size()) {
-            std::uint32_t as = 0, tr = 0;
-            for (std::uint32_t b = 0; b < 32; ++b) {
-                const std::uint32_t a = 32 * w + b;
+        for (std::uint32_t w = g.tid(); w < 2 * sm.vwords(); w += g.size()) {
+            std::uint32_t bits = 0;
+            for (std::uint32_t b = 0; b < 16; ++b) {
+                const std::uint32_t a = 16 * w + b;
                 if (a > S.A) break;
                 const std::int32_t cv = sl.cells()[a];
-                if (cv != 0) as |= 1u << b;
-                if (cv > 0) tr |= 1u << b;
+                if (cv != 0) bits |= (cv > 0 ? 3u : 1u) << (2 * b);
             }
-            sm.vasg()[w] = as;
-            sm.vtru()[w] = tr;
+            sm.vmir()[w] = bits;
         }
     }
 

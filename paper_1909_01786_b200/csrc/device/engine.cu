@@ -1201,8 +1201,8 @@ struct Search {
     static constexpr int kExpandU = 8;
 
     template <int U>
-    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, std::uint32_t D,
-                                bool learned, std::uint32_t pass = 0xffffffffu) {
+    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned,
+                                std::uint32_t pass = 0xffffffffu) {
         dstamp(pass, 0);
         const std::int32_t* fr = sl.fr(cur);
         const std::uint32_t* froff = sl.froff();
@@ -1277,11 +1277,11 @@ struct Search {
                     else ent[u] = occ_entry(lidx(trig[u]), e - se[u], learned, cls[u]);
                 }
                 if (base == start) { asm volatile("" ::"r"(ent[0].x)); dstamp(pass, 3); }
-                std::uint32_t old[U];  // 32-bit claims: this pass's keys are D + e (see propagate_grid)
+                unsigned long long old[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const std::uint32_t e = base + 32u * u + lane;
-                    old[u] = e < end ? atomicMin(sl.claim32() + ent[u].x, D + e) : D;
+                    old[u] = e < end ? atomicMin(sl.claim() + ent[u].x, ckey(gen, e)) : ckey(gen, 0);
                 }
                 std::uint32_t wx[U], wy[U];  // issued while the claims are in flight
 #pragma unroll
@@ -1327,12 +1327,12 @@ struct Search {
                 // smallest bid is the item-order winner without a separate
                 // resolve phase. The first toucher counts the check and reports
                 // an all-true conflict.
-                if (base == start) { asm volatile("" ::"r"(old[0]), "r"(wx[0])); dstamp(pass, 4); }
+                if (base == start) { asm volatile("" ::"l"(old[0]), "r"(wx[0])); dstamp(pass, 4); }
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const std::uint32_t e = base + 32u * u + lane;
-                    const bool first = e < end && old[u] - D >= T;  // stale keys lie above this pass's range
-                    const bool evl = first || e < old[u] - D;
+                    const bool first = e < end && static_cast<std::uint32_t>(old[u] >> 32) != ~gen;
+                    const bool evl = first || e < static_cast<std::uint32_t>(old[u]);
                     if (first) {
                         ++checks;
                         if (stt[u] != 3)
@@ -1427,7 +1427,7 @@ struct Search {
     // records literal and occurrence count at its e and marks e in the
     // expansion bitmap; an opposite-sign loser turns its nogood into a
     // conflict (assignment.cpp:116-124).
-    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np, std::uint32_t D) {
+    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np) {
         const int4* props = sl.props();
         const bool one_word = nwords(dlev) == 1;
         for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
@@ -1475,7 +1475,7 @@ struct Search {
                 sl.obat()[e] = ob;
                 sl.litat()[e] = p.y;
                 atomicOr(sl.bitmap() + (e >> 5), 1u << (e & 31));
-            } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull) && sl.claim32()[id] == D + e) {
+            } else if ((w & 1ull) != (p.y < 0 ? 1ull : 0ull) && static_cast<std::uint32_t>(sl.claim()[id]) == e) {
                 sl.confl()[atomicAdd(&c->n_confl, 1u)] = p.x;  // once per nogood: its min-e occurrence
             }
         }
@@ -1611,32 +1611,19 @@ struct Search {
     // One grid pass (expand+evaluate | select | place). In solo mode block 0
     // runs it alone with block barriers. Returns the conflict count.
     __device__ std::uint32_t grid_pass(std::uint32_t& F, std::uint32_t& T, std::uint32_t& cur, std::uint32_t& gen,
-                                       std::uint32_t& ts, std::uint32_t& cbase, std::uint32_t level, std::uint32_t dlev,
-                                       bool learned, std::uint32_t& pass) {
-        // 32-bit claim keys: pass k uses D_k + e with D_k = D_{k-1} - T_k, so
-        // every older key (and the all-ones start) lies at or above D_k + T_k
-        // and no clearing is needed; when the base runs out, claims are reset.
-        if (cbase == 0 || cbase < T + 1) {
-            if (cbase != 0) {
-                const std::uint32_t nclaims = S.N + c->learned_n;
-                for (std::uint32_t i = g.itid(); i < nclaims; i += g.size()) sl.claim32()[i] = 0xffffffffu;
-                g.sync();
-            }
-            cbase = 0xffffffffu;
-        }
-        const std::uint32_t D = cbase - T;
-        cbase = D;
+                                       std::uint32_t& ts, std::uint32_t level, std::uint32_t dlev, bool learned,
+                                       std::uint32_t& pass) {
         stamp(pass, 0);
         // few entries per warp: short batches; many: eight per lane in flight
-        if (T <= 64u * (g.size() >> 5)) grid_expand<2>(F, T, cur, gen, D, learned, pass);
-        else grid_expand<kExpandU>(F, T, cur, gen, D, learned, pass);
+        if (T <= 64u * (g.size() >> 5)) grid_expand<2>(F, T, cur, gen, learned, pass);
+        else grid_expand<kExpandU>(F, T, cur, gen, learned, pass);
         stamp(pass, 1);
         g.sync_snap(&c->n_props, nullptr);
         const std::uint32_t np = g.snap[0];
         stamp(pass, 2);
         stamp(pass, 3);
         stamp(pass, 4);
-        grid_select(level, dlev, np, D);
+        grid_select(level, dlev, np);
         stamp(pass, 5);
         g.sync_snap(&c->n_confl, nullptr);
         stamp(pass, 6);
@@ -1677,7 +1664,7 @@ struct Search {
 
     __device__ bool propagate_grid(std::uint32_t level) {
         frontier_offsets();
-        std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts, cbase = c->cbase;
+        std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
         const bool learned = c->learned_n > 0;
         if (threadIdx.x < 4) g.bc[threadIdx.x] = 0;
@@ -1688,8 +1675,7 @@ struct Search {
             if (T <= kSoloT) {
                 if (blockIdx.x == 0) {
                     g.solo = true;
-                    while (F != 0 && T <= kSoloT && !violated)
-                        violated = grid_pass(F, T, cur, gen, ts, cbase, level, dlev, learned, pass) != 0;
+                    while (F != 0 && T <= kSoloT && !violated) violated = grid_pass(F, T, cur, gen, ts, level, dlev, learned, pass) != 0;
                     g.solo = false;
                     if (threadIdx.x == 0) {
                         c->F = F;
@@ -1699,7 +1685,6 @@ struct Search {
                         c->ts = ts;
                         c->b[11] = violated ? 1u : 0u;
                         c->b[13] = pass;
-                        c->cbase = cbase;
                     }
                 }
                 g.sync();  // the other blocks wait here for the solo streak
@@ -1710,11 +1695,10 @@ struct Search {
                 ts = *reinterpret_cast<volatile std::uint32_t*>(&c->ts);
                 violated = *reinterpret_cast<volatile std::uint32_t*>(&c->b[11]) != 0;
                 pass = *reinterpret_cast<volatile std::uint32_t*>(&c->b[13]);
-                cbase = *reinterpret_cast<volatile std::uint32_t*>(&c->cbase);
                 if (violated) break;
                 continue;
             }
-            if (grid_pass(F, T, cur, gen, ts, cbase, level, dlev, learned, pass)) {
+            if (grid_pass(F, T, cur, gen, ts, level, dlev, learned, pass)) {
                 violated = true;
                 break;
             }
@@ -1730,7 +1714,6 @@ struct Search {
             c->cur = cur;
             c->gen = gen;
             c->ts = ts;
-            c->cbase = cbase;
             c->b[11] = violated ? 1u : 0u;
         }
         g.sync();

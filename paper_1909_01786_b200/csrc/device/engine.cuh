@@ -85,7 +85,6 @@ struct Ctl {
     std::uint32_t n_props, n_confl, n_pending, n_mbuf, n_trace;
     std::uint32_t learned_n, lpool_used, locc_used, lunits_n;
     std::uint32_t cube, epoch, stamp, pad0;
-    std::uint32_t cbase, pad1;  // grid passes: base of the last pass's 32-bit claim keys (0 = none yet)
     unsigned long long restart_threshold, conflicts_at_restart;
     double act_inc;
     std::uint32_t b[16];  // leader -> group broadcast scratch
@@ -114,7 +113,7 @@ struct SlotLayout {
     unsigned long long bytes;
     unsigned long long o_ctl, o_cells, o_tpos, o_reason, o_deps, o_dovf, o_trail, o_ldec, o_fr0, o_fr1, o_froff,
         o_claim, o_win, o_props, o_confl, o_pending, o_bitmap, o_litat, o_loff, o_lpool, o_lhdr, o_larena,
-        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf, o_occat, o_gmirror, o_obat, o_frb, o_claim32;
+        o_lunits, o_ltot, o_act, o_dup, o_scratch, o_mark, o_merged, o_mbuf, o_mcube, o_tbuf, o_occat, o_gmirror, o_obat, o_frb;
 };
 
 #if defined(__CUDACC__)
@@ -148,8 +147,6 @@ struct Slot {
     YAS_HD std::uint32_t* occat() const { return at<std::uint32_t>(L->o_occat); }  // grid slots only
     // grid slots only: 2 bits per atom (bit 0 assigned, bit 1 true), 16 atoms per word
     YAS_HD std::uint32_t* gmirror() const { return at<std::uint32_t>(L->o_gmirror); }
-    // grid slots only: 32-bit claim key per nogood (see Search::propagate_grid)
-    YAS_HD std::uint32_t* claim32() const { return at<std::uint32_t>(L->o_claim32); }
     // grid slots only: static occurrence-list base of the winner at e, and of
     // frontier literal p (saves the offset lookup on the expansion path)
     YAS_HD std::uint32_t* obat() const { return at<std::uint32_t>(L->o_obat); }

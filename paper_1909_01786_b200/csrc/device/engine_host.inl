@@ -158,15 +158,11 @@ struct Arena {
         L.o_tbuf = take(16ull * tcap);
         L.o_occat = take(grid_blocks ? 4 * tbits : 0);  // whole-grid passes only
         L.o_gmirror = take(grid_blocks ? 4 * ((A1 + 15) / 16 + 1) : 0);
-        L.o_claim32 = take(grid_blocks ? 4ull * K.items : 0);
         L.o_obat = take(grid_blocks ? 4 * tbits : 0);
         L.o_frb = take(grid_blocks ? 4 * (A1 + 1) : 0);
         L.bytes = o;
         L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
         ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
-        if (grid_blocks)  // 32-bit claims start above every key
-            for (std::uint32_t sidx = 0; sidx < n_slots; ++sidx)
-                ck(cudaMemset(L.base + static_cast<std::size_t>(sidx) * o + L.o_claim32, 0xff, 4ull * K.items), "memset");
         dev::init_slots<<<n_slots, 256>>>(L, static_cast<std::uint32_t>(A1), K.items);
         ck(cudaGetLastError(), "init_slots");
         slots.resize(n_slots);

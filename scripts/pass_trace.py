@@ -17,10 +17,15 @@ store, seeded, dec = Y.NogoodStore.planted(atoms, nogoods, pct)
 prop = Y.Propagator(store, 16, engine="grid")
 sd = np.asarray(seeded, dtype=np.int32)
 fr = np.asarray([dec] + seeded, dtype=np.int32)
+import torch  # noqa: E402  (L2 flush, as in bench.py: timings with cold L2)
+flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 for rep in range(3):
     prop.reset(); prop.push_decision(dec); prop.assign_propagated(sd, 2); prop.seed(fr)
     if rep == 2:
         prop.pass_trace(True)
+    prop.flush()
+    flush.zero_()
+    torch.cuda.synchronize()
     o = prop.propagate_and_check(2)
 tr = prop.pass_trace().astype(np.int64)
 print(f"kernel {o.device_ms * 1e3:.1f} us, passes {o.passes}")

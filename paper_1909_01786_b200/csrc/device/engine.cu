@@ -490,7 +490,7 @@ struct Search {
     unsigned long long t0;
     Sm sm;
 
-    __device__ Search(G& g_, const Static& s, const Config& cf, Slot slot, const Caps& k, Shared* shared,
+    __device__ __forceinline__ Search(G& g_, const Static& s, const Config& cf, Slot slot, const Caps& k, Shared* shared,
                       unsigned long long start, const Sm& smem)
         : g(g_), S(s), C(cf), sl(slot), K(k), sh(shared), c(g_.c), t0(start), sm(smem) {}
 
@@ -498,21 +498,21 @@ struct Search {
     // sign of the atom's value: 0 unassigned, 1 true, -1 false
     // Whole-grid slots keep a 2-bit mirror of the assignment in global memory
     // (16 atoms per word; 25 KB for 100k atoms) next to the cells.
-    __device__ static int mirror_val(std::uint32_t word, std::uint32_t a) {
+    __device__ __forceinline__ static int mirror_val(std::uint32_t word, std::uint32_t a) {
         const std::uint32_t v = (word >> (2 * (a & 15))) & 3u;
         return v == 0 ? 0 : (v == 3 ? 1 : -1);
     }
     // Pass-snapshot read (L1-cached): only for values that cannot change
     // during the current phase.
-    __device__ std::uint32_t mirror_word_snap(std::uint32_t a) const { return __ldca(sl.gmirror() + (a >> 4)); }
+    __device__ __forceinline__ std::uint32_t mirror_word_snap(std::uint32_t a) const { return __ldca(sl.gmirror() + (a >> 4)); }
 
-    __device__ int val(std::uint32_t a) const {
+    __device__ __forceinline__ int val(std::uint32_t a) const {
         if constexpr (G::kGrid) return mirror_val(__ldcg(sl.gmirror() + (a >> 4)), a);
         if (sm.vwords()) return mirror_val(sm.vmir()[a >> 4], a);
         const std::int32_t cv = sl.cells()[a];
         return (cv > 0) - (cv < 0);
     }
-    __device__ void set_cell(std::uint32_t a, std::int32_t cv) const {
+    __device__ __forceinline__ void set_cell(std::uint32_t a, std::int32_t cv) const {
         sl.cells()[a] = cv;
         if constexpr (G::kGrid) {
             std::uint32_t* w = sl.gmirror() + (a >> 4);
@@ -528,7 +528,7 @@ struct Search {
             else atomicOr(w, (cv > 0 ? 3u : 1u) << sh2);  // bits are clear while unassigned
         }
     }
-    __device__ void rebuild_mirror() const {
+    __device__ __forceinline__ void rebuild_mirror() const {
         if (!sm.vwords()) return;
         for (std::uint32_t w = g.tid(); w < 2 * sm.vwords(); w += g.size()) {
             std::uint32_t bits = 0;
@@ -543,7 +543,7 @@ struct Search {
     }
 
     // ---- store access ----------------------------------------------------
-    __device__ const std::int32_t* lits_of(std::uint32_t id, std::uint32_t& len) const {
+    __device__ __forceinline__ const std::int32_t* lits_of(std::uint32_t id, std::uint32_t& len) const {
         if (id < S.N) {
             const std::uint32_t lo = __ldg(S.off + id);
             len = __ldg(S.off + id + 1) - lo;
@@ -554,27 +554,27 @@ struct Search {
         len = sl.loff()[k + 1] - lo;
         return sl.lpool() + lo;
     }
-    __device__ std::int32_t lit_at(const std::int32_t* p, std::uint32_t k, std::uint32_t id) const {
+    __device__ __forceinline__ std::int32_t lit_at(const std::int32_t* p, std::uint32_t k, std::uint32_t id) const {
         return id < S.N ? __ldg(p + k) : p[k];
     }
-    __device__ std::uint32_t length_of(std::uint32_t id) const {
+    __device__ __forceinline__ std::uint32_t length_of(std::uint32_t id) const {
         if (id < S.N) return __ldg(S.off + id + 1) - __ldg(S.off + id);
         return sl.loff()[id - S.N + 1] - sl.loff()[id - S.N];
     }
-    __device__ std::uint32_t guard_of(std::uint32_t id) const { return id < S.N ? __ldg(S.guard + id) : kNone; }
-    __device__ std::uint32_t occ_total(std::uint32_t li) const {
+    __device__ __forceinline__ std::uint32_t guard_of(std::uint32_t id) const { return id < S.N ? __ldg(S.guard + id) : kNone; }
+    __device__ __forceinline__ std::uint32_t occ_total(std::uint32_t li) const {
         return __ldg(S.occ_off + li * 4 + 4) - __ldg(S.occ_off + li * 4) + sl.ltot()[li];
     }
     // j-th entry of the literal's occurrence list [static c0, learned c0, ...,
     // static c3, learned c3]: {id, guard, x, y} and its length class. Entries
     // carry their class in the top two bits of the id, so with no learned
     // nogoods one offset load and one dependent 16-byte load suffice.
-    __device__ static int4 decode(int4 ent, std::uint32_t& cls) {
+    __device__ __forceinline__ static int4 decode(int4 ent, std::uint32_t& cls) {
         cls = static_cast<std::uint32_t>(ent.x) >> 30;
         ent.x &= 0x3fffffff;
         return ent;
     }
-    __device__ int4 occ_entry(std::uint32_t li, std::uint32_t j, bool learned, std::uint32_t& cls) const {
+    __device__ __forceinline__ int4 occ_entry(std::uint32_t li, std::uint32_t j, bool learned, std::uint32_t& cls) const {
         const std::uint32_t* oo = S.occ_off + li * 4;
         if (!learned) return decode(__ldg(S.occ + __ldg(oo) + j), cls);
         std::uint32_t b[5];
@@ -598,20 +598,20 @@ struct Search {
         cls = 0;
         return make_int4(-1, 0, 0, 0);
     }
-    __device__ std::uint32_t nwords(std::uint32_t level) const {
+    __device__ __forceinline__ std::uint32_t nwords(std::uint32_t level) const {
         const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
         return nw < C.W ? nw : C.W;
     }
     // Deps rows are atom-major: the words of one atom are contiguous (row
     // stride rounded up to an even word count for 16-byte vector access).
-    __device__ std::uint32_t dstride() const { return (C.W + 1u) & ~1u; }
-    __device__ unsigned long long& dep(std::uint32_t w, std::uint32_t a) const {
+    __device__ __forceinline__ std::uint32_t dstride() const { return (C.W + 1u) & ~1u; }
+    __device__ __forceinline__ unsigned long long& dep(std::uint32_t w, std::uint32_t a) const {
         return sl.deps()[static_cast<std::size_t>(a) * dstride() + w];
     }
     // OR words [w0, w0 + 2*NQ) of the Deps rows of atoms x[k] (on[k]) into
     // acc, as 16-byte loads all issued before any is used.
     template <int NK, int NQ>
-    __device__ void or_rows(const std::uint32_t* x, const bool* on, std::uint32_t w0, std::uint32_t nw,
+    __device__ __forceinline__ void or_rows(const std::uint32_t* x, const bool* on, std::uint32_t w0, std::uint32_t nw,
                             unsigned long long* acc) const {
         ulonglong2 v[NK][NQ];
 #pragma unroll
@@ -629,7 +629,7 @@ struct Search {
             }
     }
     template <int NQ>
-    __device__ void store_row(std::uint32_t a, std::uint32_t w0, std::uint32_t nw, const unsigned long long* acc) const {
+    __device__ __forceinline__ void store_row(std::uint32_t a, std::uint32_t w0, std::uint32_t nw, const unsigned long long* acc) const {
         ulonglong2* row = reinterpret_cast<ulonglong2*>(sl.deps() + static_cast<std::size_t>(a) * dstride() + w0);
 #pragma unroll
         for (int q = 0; q < NQ; ++q)
@@ -639,7 +639,7 @@ struct Search {
             }
     }
     // Deps of atom a from the rows of up to two contributing atoms.
-    __device__ void deps_from_pair(std::uint32_t a, std::uint32_t x0, bool on0, std::uint32_t x1, bool on1,
+    __device__ __forceinline__ void deps_from_pair(std::uint32_t a, std::uint32_t x0, bool on0, std::uint32_t x1, bool on1,
                                    std::uint32_t nw) const {
         const std::uint32_t xs[2] = {x0, x1};
         const bool ons[2] = {on0, on1};
@@ -650,13 +650,13 @@ struct Search {
         }
         sl.dovf()[a] = static_cast<std::uint8_t>((on0 ? sl.dovf()[x0] : 0) | (on1 ? sl.dovf()[x1] : 0));
     }
-    __device__ bool holds(std::int32_t l) const {
+    __device__ __forceinline__ bool holds(std::int32_t l) const {
         const int v = val(atom_of(l));
         return v != 0 && ((v > 0) == (l > 0));
     }
 
     // phase accounting: cycles since the previous mark go to bucket k
-    __device__ void mark(int k) const {
+    __device__ __forceinline__ void mark(int k) const {
         if constexpr (G::kGrid) return;  // grid passes: see stamp()
         if (C.phase_prof && g.leader()) {
             const unsigned long long t = clock64();
@@ -668,24 +668,24 @@ struct Search {
     // Diagnostics: thread 0 of every block stamps the global timer at phase
     // boundaries of the first kPtracePasses passes of a grid propagation.
     static constexpr std::uint32_t kPtracePasses = 64, kPtraceStamps = 10;
-    __device__ void stamp(std::uint32_t pass, std::uint32_t k) const {
+    __device__ __forceinline__ void stamp(std::uint32_t pass, std::uint32_t k) const {
         if (C.ptrace && threadIdx.x == 0 && pass < kPtracePasses)
             C.ptrace[(static_cast<std::size_t>(pass) * gridDim.x + blockIdx.x) * kPtraceStamps + k] = gtimer();
     }
 
     // Diagnostics: in-phase stamps (clock64) of warp 0 of block 0 in pass `pass`.
-    __device__ void dstamp(std::uint32_t pass, std::uint32_t k) const {
+    __device__ __forceinline__ void dstamp(std::uint32_t pass, std::uint32_t k) const {
         if (C.ptrace && blockIdx.x == 0 && threadIdx.x == 0 && pass < kPtracePasses)
             C.ptrace[static_cast<std::size_t>(kPtracePasses) * gridDim.x * kPtraceStamps + pass * 16 + k] = clock64();
     }
 
-    __device__ void fail(std::uint32_t status) {
+    __device__ __forceinline__ void fail(std::uint32_t status) {
         if (g.leader()) c->status = status;
     }
 
     // Deps of the literal derived from nogood (lits,len) on atom `a`:
     // OR of Deps[x] over the other atoms with level > 1 (propagate.cpp:49-62).
-    __device__ void write_deps_from(const std::int32_t* L, std::uint32_t len, std::uint32_t id, std::uint32_t a,
+    __device__ __forceinline__ void write_deps_from(const std::int32_t* L, std::uint32_t len, std::uint32_t id, std::uint32_t a,
                                     std::uint32_t level) const {
         const std::uint32_t nw = nwords(level);
         if (len <= 8) {
@@ -733,7 +733,7 @@ struct Search {
         }
         sl.dovf()[a] = ovf;
     }
-    __device__ unsigned long long deps_word(const std::int32_t* L, std::uint32_t len, std::uint32_t id,
+    __device__ __forceinline__ unsigned long long deps_word(const std::int32_t* L, std::uint32_t len, std::uint32_t id,
                                             std::uint32_t a, std::uint32_t w, std::uint8_t& ovf) const {
         unsigned long long acc = 0;
         for (std::uint32_t k = 0; k < len; ++k) {
@@ -752,7 +752,7 @@ struct Search {
     // ---- group-parallel building blocks -------------------------------------
     // Exclusive occurrence offsets of the current frontier; sets c->T. The
     // frontier and its offsets are mirrored into shared memory when they fit.
-    __device__ void frontier_offsets() {
+    __device__ __forceinline__ void frontier_offsets() {
         const std::uint32_t F = c->F;
         const std::int32_t* fr = sl.fr(c->cur);
         const bool mirror = sm.tcap() && F + 1 <= sm.fcap();
@@ -788,7 +788,7 @@ struct Search {
     // frontier buffer `dst`, appended to the trail, and the occurrence offsets
     // of that new frontier are produced by the same scan.
     template <bool SMEM>
-    __device__ void compact(std::uint32_t T, std::uint32_t dst, bool pass, std::uint32_t hsize) {
+    __device__ __forceinline__ void compact(std::uint32_t T, std::uint32_t dst, bool pass, std::uint32_t hsize) {
         const std::uint32_t nw = (T + 31) / 32;
         const std::uint32_t ts0 = c->ts;
         std::int32_t* out = sl.fr(dst);
@@ -851,7 +851,7 @@ struct Search {
     // Apply proposals: per atom the smallest key wins (newly_set); an opposite
     // loser turns its nogood into a conflict (assignment.cpp:116-124).
     template <bool SMEM>
-    __device__ void apply(std::uint32_t level, bool unit) {
+    __device__ __forceinline__ void apply(std::uint32_t level, bool unit) {
         const std::uint32_t np = c->n_props;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
         for (std::uint32_t base = g.tid() & ~31u; base < np; base += g.size()) {
@@ -912,7 +912,7 @@ struct Search {
 
     // Evaluate nogood `id` against the pass-start assignment
     // (propagate.cpp:86-168 without the watch shortcuts).
-    __device__ void evaluate(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
+    __device__ __forceinline__ void evaluate(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
                              unsigned long long* d0 = nullptr, std::uint32_t* meta = nullptr) const {
         const std::uint32_t guard = guard_of(static_cast<std::uint32_t>(id));
         const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
@@ -964,7 +964,7 @@ struct Search {
     // triggered by frontier literal `trig` (which holds). Binary and ternary
     // nogoods are decided by the two literals carried in the entry; a long one
     // only when one of them is dead or both are free, else by a full scan.
-    __device__ void evaluate_entry(const int4& ent, std::uint32_t cls, std::int32_t trig, bool& conflict, bool& prop,
+    __device__ __forceinline__ void evaluate_entry(const int4& ent, std::uint32_t cls, std::int32_t trig, bool& conflict, bool& prop,
                                    std::int32_t& plit, std::uint32_t& len, unsigned long long* d0 = nullptr,
                                    std::uint32_t* meta = nullptr) const {
         if (cls == 0) {  // length-1 entry: its literal is the trigger, which holds
@@ -1010,7 +1010,7 @@ struct Search {
     }
 
     // One pass with the working set in shared memory (T <= tcap).
-    __device__ void pass_smem(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
+    __device__ __forceinline__ void pass_smem(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
         const bool learned = c->learned_n > 0;
         std::uint32_t hs = 64;
         while (hs < 2 * T) hs <<= 1;
@@ -1091,7 +1091,7 @@ struct Search {
     }
 
     // One pass with the working set in global memory (any size; grid mode).
-    __device__ void pass_global(std::uint32_t F, std::uint32_t T, std::uint32_t gen, std::uint32_t cur,
+    __device__ __forceinline__ void pass_global(std::uint32_t F, std::uint32_t T, std::uint32_t gen, std::uint32_t cur,
                                 std::uint32_t level) {
         const bool learned = c->learned_n > 0;
         const std::int32_t* fr = sl.fr(cur);
@@ -1157,7 +1157,7 @@ struct Search {
     // Full scan of nogood `id` against the pass snapshot (propagate.cpp:86-168
     // without watches): literals, then their values, each as one batch of
     // independent loads.
-    __device__ void scan_snap(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len) const {
+    __device__ __forceinline__ void scan_snap(std::int32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len) const {
         const std::uint32_t guard = guard_of(static_cast<std::uint32_t>(id));
         const std::int32_t* L = lits_of(static_cast<std::uint32_t>(id), len);
         std::uint32_t nfree = 0;
@@ -1201,7 +1201,7 @@ struct Search {
     static constexpr int kExpandU = 8;
 
     template <int U>
-    __device__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned,
+    __device__ __forceinline__ void grid_expand(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t gen, bool learned,
                                 std::uint32_t pass = 0xffffffffu) {
         dstamp(pass, 0);
         const std::int32_t* fr = sl.fr(cur);
@@ -1427,7 +1427,7 @@ struct Search {
     // records literal and occurrence count at its e and marks e in the
     // expansion bitmap; an opposite-sign loser turns its nogood into a
     // conflict (assignment.cpp:116-124).
-    __device__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np) {
+    __device__ __forceinline__ void grid_select(std::uint32_t level, std::uint32_t dlev, std::uint32_t np) {
         const int4* props = sl.props();
         const bool one_word = nwords(dlev) == 1;
         for (std::uint32_t i = g.itid(); i < np; i += g.size()) {
@@ -1483,7 +1483,7 @@ struct Search {
 
     // Largest lane w with key[w] <= x, key non-decreasing over the lanes and
     // key[0] <= x (five register shuffles).
-    __device__ static std::uint32_t lane_search(std::uint32_t key, std::uint32_t x) {
+    __device__ __forceinline__ static std::uint32_t lane_search(std::uint32_t key, std::uint32_t x) {
         std::uint32_t w = 0;
 #pragma unroll
         for (int st = 16; st >= 1; st >>= 1)
@@ -1493,7 +1493,7 @@ struct Search {
 
     // Winner count and occurrence sum of bitmap word wi (the 32 occurrence
     // counts of a word are one aligned 128-byte line: eight vector loads).
-    __device__ unsigned long long word_value(std::uint32_t wi, std::uint32_t bits) const {
+    __device__ __forceinline__ unsigned long long word_value(std::uint32_t wi, std::uint32_t bits) const {
         if (!bits) return 0ull;
         const uint4* line = reinterpret_cast<const uint4*>(sl.occat() + static_cast<std::size_t>(wi) * 32);
         uint4 q[8];
@@ -1514,7 +1514,7 @@ struct Search {
     // each word's exclusive (count, occurrence) prefix `pre`: the set bits are
     // dealt to the lanes 32 at a time in e order; a segmented lane scan gives
     // each winner its occurrence offset inside its word.
-    __device__ void place_words(std::uint32_t wi, std::uint32_t bits, unsigned long long pre, std::int32_t* out,
+    __device__ __forceinline__ void place_words(std::uint32_t wi, std::uint32_t bits, unsigned long long pre, std::int32_t* out,
                                 std::uint32_t ts0) {
         const std::uint32_t lane = lane_id();
         const std::uint32_t w0 = wi - lane;
@@ -1567,7 +1567,7 @@ struct Search {
     // whole grid, one grid scan per round of words.
     static constexpr std::uint32_t kBlockPlaceWords = 2048;
 
-    __device__ void grid_place(std::uint32_t T, std::uint32_t dst, std::uint32_t ts0, std::uint32_t& F_next,
+    __device__ __forceinline__ void grid_place(std::uint32_t T, std::uint32_t dst, std::uint32_t ts0, std::uint32_t& F_next,
                                std::uint32_t& T_next) {
         const std::uint32_t nw = (T + 31) / 32;
         std::int32_t* out = sl.fr(dst);
@@ -1610,7 +1610,7 @@ struct Search {
 
     // One grid pass (expand+evaluate | select | place). In solo mode block 0
     // runs it alone with block barriers. Returns the conflict count.
-    __device__ std::uint32_t grid_pass(std::uint32_t& F, std::uint32_t& T, std::uint32_t& cur, std::uint32_t& gen,
+    __device__ __forceinline__ std::uint32_t grid_pass(std::uint32_t& F, std::uint32_t& T, std::uint32_t& cur, std::uint32_t& gen,
                                        std::uint32_t& ts, std::uint32_t level, std::uint32_t dlev, bool learned,
                                        std::uint32_t& pass) {
         stamp(pass, 0);
@@ -1662,7 +1662,7 @@ struct Search {
     // a grid barrier ~1.5 us, and one block covers them in one or two batches.
     static constexpr std::uint32_t kSoloT = 0;  // measured: no gain on the L2-flushed benchmark (0.294 vs 0.300 ms)
 
-    __device__ bool propagate_grid(std::uint32_t level) {
+    __device__ __forceinline__ bool propagate_grid(std::uint32_t level) {
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
@@ -1724,7 +1724,7 @@ struct Search {
     // Returns true when conflicts were found (they are in confl[0..n_confl)).
     static constexpr std::uint32_t kWarpPassT = 96;  // passes this small run in warp 0 alone
 
-    __device__ bool propagate(std::uint32_t level) {
+    __device__ __forceinline__ bool propagate(std::uint32_t level) {
         if constexpr (G::kGrid) return propagate_grid(level);
         mark(0);
         frontier_offsets();
@@ -1751,7 +1751,7 @@ struct Search {
     }
 
     // Warp-synchronous passes while they stay small (called by warp 0 only).
-    __device__ void small_passes(std::uint32_t level) {
+    __device__ __forceinline__ void small_passes(std::uint32_t level) {
         for (;;) {
             __syncwarp();
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
@@ -1771,7 +1771,7 @@ struct Search {
     // evaluate() of one nogood by the whole warp (results uniform): 32
     // literals per step, free/dead detection by ballot, Deps word 0 of the
     // proposal by OR-reduction (propagate.cpp:86-168, :49-62).
-    __device__ void w_evaluate(std::uint32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
+    __device__ __forceinline__ void w_evaluate(std::uint32_t id, bool& conflict, bool& prop, std::int32_t& plit, std::uint32_t& len,
                                unsigned long long& d0, std::uint32_t& meta) const {
         const std::uint32_t lane = lane_id();
         const std::uint32_t guard = guard_of(id);
@@ -1819,7 +1819,7 @@ struct Search {
     // (the lowest lane has the smallest e, i.e. comes first in item order),
     // per-atom winners by __match_any_sync on the proposed atom (lowest lane =
     // smallest key), positions by ballot prefix counts and one warp scan.
-    __device__ void tiny_pass(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
+    __device__ __forceinline__ void tiny_pass(std::uint32_t F, std::uint32_t T, std::uint32_t cur, std::uint32_t level) {
         const std::uint32_t lane = lane_id();
         const unsigned below = (1u << lane) - 1u;
         const bool act = lane < T;
@@ -1935,7 +1935,7 @@ struct Search {
     // (conflict id -(k+1)), then every length-1 store entry in id order,
     // asserted if its guard allows, else a passive violation check. The
     // sequential semantics are reproduced with order keys e.
-    __device__ bool initial_propagation(bool keep_conflicts) {
+    __device__ __forceinline__ bool initial_propagation(bool keep_conflicts) {
         const std::uint32_t n1 = S.n_units, n2 = S.n_uids + c->lunits_n, total = n1 + n2;
         const std::uint32_t gen = c->gen;
         for (std::uint32_t base = g.tid() & ~31u; base < total; base += g.size()) {
@@ -2012,7 +2012,7 @@ struct Search {
     }
 
     // Erase everything above `target` (assignment.cpp:166-178).
-    __device__ void backjump(std::uint32_t target) {
+    __device__ __forceinline__ void backjump(std::uint32_t target) {
         if (g.leader()) {
             const std::uint32_t cdl = c->cdl;
             c->b[8] = target < cdl ? sl.tpos()[atom_of(sl.ldec()[target + 1])] : c->ts;
@@ -2041,12 +2041,12 @@ struct Search {
     // literal sets are spread over the lanes, maxima / OR-reductions /
     // compactions are warp collectives, so a step costs one memory round trip
     // instead of one per literal. All functions are called by all 32 lanes.
-    __device__ static unsigned long long w_or64(unsigned long long v) {
+    __device__ __forceinline__ static unsigned long long w_or64(unsigned long long v) {
         const std::uint32_t lo = __reduce_or_sync(0xffffffffu, static_cast<std::uint32_t>(v));
         const std::uint32_t hi = __reduce_or_sync(0xffffffffu, static_cast<std::uint32_t>(v >> 32));
         return (static_cast<unsigned long long>(hi) << 32) | lo;
     }
-    __device__ static unsigned long long w_min64(unsigned long long v) {
+    __device__ __forceinline__ static unsigned long long w_min64(unsigned long long v) {
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
@@ -2054,7 +2054,7 @@ struct Search {
         }
         return v;
     }
-    __device__ static unsigned long long w_max64(unsigned long long v) {
+    __device__ __forceinline__ static unsigned long long w_max64(unsigned long long v) {
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) {
             const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
@@ -2062,15 +2062,15 @@ struct Search {
         }
         return v;
     }
-    __device__ static unsigned long long w_add64(unsigned long long v) {
+    __device__ __forceinline__ static unsigned long long w_add64(unsigned long long v) {
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
         return v;
     }
-    __device__ std::int32_t* sortbuf() const { return sl.scratch() + S.A + 256; }
+    __device__ __forceinline__ std::int32_t* sortbuf() const { return sl.scratch() + S.A + 256; }
 
     // Sort v[0..n) by atom (Nogood::make order; atoms are distinct) by rank.
-    __device__ void w_sort(std::int32_t* v, std::uint32_t n) const {
+    __device__ __forceinline__ void w_sort(std::int32_t* v, std::uint32_t n) const {
         const std::uint32_t lane = lane_id();
         if (n <= 32) {
             const std::int32_t x = lane < n ? v[lane] : 0;
@@ -2097,7 +2097,7 @@ struct Search {
     }
 
     // NogoodStore::add_learned (nogood_store.cpp:81-107). Returns id or -1.
-    __device__ std::int32_t w_add_learned(const std::int32_t* lits, std::uint32_t len, bool count_capacity = true) {
+    __device__ __forceinline__ std::int32_t w_add_learned(const std::int32_t* lits, std::uint32_t len, bool count_capacity = true) {
         const std::uint32_t lane = lane_id();
         if ((count_capacity && c->learned_n >= C.learned_capacity) || c->learned_n >= K.lcap ||
             c->lpool_used + len > K.lpool) {
@@ -2175,7 +2175,7 @@ struct Search {
 
     // State of nogood `id` under the current assignment: any dead literal
     // (satisfied), number of free literals and the free one when unique.
-    __device__ void w_status(std::uint32_t id, bool& dead, std::uint32_t& nfree, std::int32_t& rem) const {
+    __device__ __forceinline__ void w_status(std::uint32_t id, bool& dead, std::uint32_t& nfree, std::int32_t& rem) const {
         std::uint32_t len;
         const std::int32_t* L = lits_of(id, len);
         std::uint32_t nf = 0;
@@ -2194,7 +2194,7 @@ struct Search {
     }
 
     // Driver::try_assert (solver.cpp:117-146) on the current frontier.
-    __device__ void w_try_assert(std::uint32_t id) {
+    __device__ __forceinline__ void w_try_assert(std::uint32_t id) {
         const std::uint32_t lane = lane_id();
         bool dead;
         std::uint32_t nfree;
@@ -2239,7 +2239,7 @@ struct Search {
 
     // fwd_learning (learn.cpp:106-142). Writes the learned literals to out and
     // returns their count, or 0xffffffff on a Deps overflow (-> res fallback).
-    __device__ std::uint32_t w_fwd(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+    __device__ __forceinline__ std::uint32_t w_fwd(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
         const std::uint32_t lane = lane_id();
         const unsigned below = (1u << lane) - 1u;
         std::uint32_t len;
@@ -2282,7 +2282,7 @@ struct Search {
 
     // res_learning (learn.cpp:53-104): resolve until a positive UIP. The set is
     // kept as atoms in out[0..n) (unordered) with membership stamps in mark[].
-    __device__ std::uint32_t w_res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
+    __device__ __forceinline__ std::uint32_t w_res(std::uint32_t delta, std::int32_t* out, std::uint32_t& target) {
         const std::uint32_t lane = lane_id();
         const unsigned below = (1u << lane) - 1u;
         std::uint32_t* mark = sl.mark();
@@ -2368,7 +2368,7 @@ struct Search {
 
     // Driver::handle_conflicts (solver.cpp:161-214), leader-warp part: writes
     // the backjump plan to c->b.
-    __device__ void analyze_and_learn() {
+    __device__ __forceinline__ void analyze_and_learn() {
         const std::uint32_t lane = lane_id();
         if (lane == 0) {
             c->st.conflicts += 1;
@@ -2473,7 +2473,7 @@ struct Search {
         __syncwarp();
     }
 
-    __device__ bool handle_conflicts() {
+    __device__ __forceinline__ bool handle_conflicts() {
         if (g.leader_warp()) analyze_and_learn();
         g.sync();
         if (c->status != kRunning) return false;
@@ -2502,7 +2502,7 @@ struct Search {
         return true;
     }
 
-    __device__ double score(std::uint32_t head) const {
+    __device__ __forceinline__ double score(std::uint32_t head) const {
         if (C.heur == 2) return sl.act()[head];
         if (C.heur == 0) return static_cast<double>(occ_total(2 * head) + occ_total(2 * head + 1));
         double s = 0.0;  // Jeroslow-Wang, summed in the reference's list order
@@ -2518,12 +2518,45 @@ struct Search {
         return s;
     }
 
-    // decide (decide.cpp:107-122) or complete_assignment (decide.cpp:124-135)
-    __device__ void decide_or_complete() {
-        double best = -1.0;
-        std::uint32_t bi = 0xffffffffu;
-        // find_applicable + score (decide.cpp:43-79): DU rules per thread per
-        // step, every load of a step issued before any is used
+    // find_applicable + score (decide.cpp:43-79): DU rules per thread per
+    // step, every load of a step issued before any is used. Packed variant:
+    // 8-byte records (the rule table of a single search stays in L1) and one
+    // static count + two learned counts per applicable head (occurrence heuristic).
+    __device__ __forceinline__ void scan_rules_packed(double& best, std::uint32_t& bi) const {
+        constexpr int DU = 8;
+        const std::uint32_t gs = g.size();
+        for (std::uint32_t r0 = g.tid(); r0 < S.R; r0 += DU * gs) {
+            unsigned long long ru[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                const std::uint32_t r = r0 + k * gs;
+                ru[k] = r < S.R ? __ldg(S.rules8 + r) : (1ull << 63);
+            }
+            std::uint32_t hh[DU];
+            bool app[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                const std::uint32_t h = static_cast<std::uint32_t>(ru[k]) & 0x1fffffu;
+                const std::uint32_t t = static_cast<std::uint32_t>(ru[k] >> 21) & 0x1fffffu;
+                const std::uint32_t n = static_cast<std::uint32_t>(ru[k] >> 42) & 0x1fffffu;
+                app[k] = !(ru[k] >> 63) && val(h) == 0 && (t == 0 || val(t) > 0) && (n == 0 || val(n) >= 0);
+                hh[k] = app[k] ? h : 0u;
+            }
+            std::uint32_t so[DU], l0[DU], l1[DU];
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                so[k] = __ldg(S.socc + hh[k]);
+                l0[k] = sl.ltot()[2 * hh[k]];
+                l1[k] = sl.ltot()[2 * hh[k] + 1];
+            }
+#pragma unroll
+            for (int k = 0; k < DU; ++k) {
+                const double sc = static_cast<double>(so[k] + l0[k] + l1[k]);
+                if (app[k] && better(sc, r0 + k * gs, best, bi)) { best = sc; bi = r0 + k * gs; }
+            }
+        }
+    }
+    __device__ __forceinline__ void scan_rules(double& best, std::uint32_t& bi) const {
         constexpr int DU = 8;
         const std::uint32_t gs = g.size();
         for (std::uint32_t r0 = g.tid(); r0 < S.R; r0 += DU * gs) {
@@ -2566,6 +2599,18 @@ struct Search {
                 }
             }
         }
+    }
+
+    // decide (decide.cpp:107-122) or complete_assignment (decide.cpp:124-135)
+    __device__ __forceinline__ void decide_or_complete() {
+        double best = -1.0;
+        std::uint32_t bi = 0xffffffffu;
+        bool packed = false;
+        if constexpr (G::kBlock) {
+            packed = C.heur == 0 && S.rules8 != nullptr;
+            if (packed) scan_rules_packed(best, bi);
+        }
+        if (!packed) scan_rules(best, bi);
         g.argmax(best, bi);
         if (bi != 0xffffffffu) {
             if (g.leader()) {
@@ -2627,7 +2672,7 @@ struct Search {
         g.sync();
     }
 
-    __device__ void record_model(std::uint32_t cube) {
+    __device__ __forceinline__ void record_model(std::uint32_t cube) {
         const std::uint32_t m = c->n_mbuf, words = K.mwords;
         for (std::uint32_t w = g.tid(); w < words; w += g.size()) {
             std::uint32_t bits = 0;
@@ -2648,7 +2693,7 @@ struct Search {
     }
 
     // block_current_model (solver.cpp:234-246). false = enumeration complete.
-    __device__ bool block_model() {
+    __device__ __forceinline__ bool block_model() {
         if (g.leader_warp()) {
             const std::uint32_t lane = lane_id();
             if (lane == 0) c->b[0] = 0;
@@ -2678,7 +2723,7 @@ struct Search {
     }
 
     // validate_fixpoint (propagate.cpp:251-266) for cfg.debug_validate
-    __device__ void validate() {
+    __device__ __forceinline__ void validate() {
         const std::uint32_t total = S.N + c->learned_n;
         for (std::uint32_t id = g.tid(); id < total; id += g.size()) {
             std::uint32_t len, nfree = 0, nhold = 0;
@@ -2701,7 +2746,7 @@ struct Search {
     }
 
     // Fresh search in this slot: clear what the previous search touched.
-    __device__ void begin_search(std::uint32_t cube) {
+    __device__ __forceinline__ void begin_search(std::uint32_t cube) {
         const std::uint32_t ts = c->ts;
         for (std::uint32_t i = g.tid(); i < ts; i += g.size()) {
             const std::uint32_t a = atom_of(sl.trail()[i]);
@@ -2755,7 +2800,7 @@ struct Search {
 
     // The Alg. 1 state machine (solver.cpp:248-303). Returns when the search
     // is finished (phase kFinished), on error, or when it must yield.
-    __device__ void run() {
+    __device__ __forceinline__ void run() {
         for (;;) {
             const std::uint32_t ph = c->phase;
             if (c->status != kRunning) return;

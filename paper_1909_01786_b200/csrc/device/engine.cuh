@@ -68,6 +68,11 @@ struct Static {
     const std::int32_t* units;     // static unit literals (nogood literal sigma)
     const std::int32_t* uids;      // static length-1 CSR ids
     const uint4* rules;            // (head, b, t, n | vacuous<<31)
+    // decision scan: rule r packed in 8 bytes (head | t << 21 | n << 42 | vacuous << 63;
+    // null when an atom id needs more than 21 bits) and the static occurrence
+    // count of both literals of every atom
+    const unsigned long long* rules8;
+    const std::uint32_t* socc;
     const std::int32_t* cubes;     // n_cubes * cube_width nogood literals (0 = pad)
 };
 

@@ -95,6 +95,19 @@ struct Arena {
         std::vector<uint4> r(rules.size());
         for (std::size_t i = 0; i < rules.size(); ++i) r[i] = make_uint4(rules[i].head, rules[i].b, rules[i].t, rules[i].n);
         S.rules = dupload(r, owned);
+        S.rules8 = nullptr;
+        if (st.total_atoms < (1u << 21)) {
+            std::vector<unsigned long long> r8(rules.size());
+            for (std::size_t i = 0; i < rules.size(); ++i) {
+                const unsigned long long n = rules[i].n & 0x7fffffffu, vac = rules[i].n >> 31;
+                r8[i] = static_cast<unsigned long long>(rules[i].head) | static_cast<unsigned long long>(rules[i].t) << 21 |
+                        n << 42 | vac << 63;
+            }
+            S.rules8 = dupload(r8, owned);
+        }
+        std::vector<std::uint32_t> so(static_cast<std::size_t>(st.total_atoms) + 1);
+        for (std::uint32_t a = 0; a <= st.total_atoms; ++a) so[a] = st.occ_off[8ull * a + 8] - st.occ_off[8ull * a];
+        S.socc = dupload(so, owned);
         S.cubes = dupload(cubes, owned);
         A = st.total_atoms;
     }

@@ -254,7 +254,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
         per_sm = std::min<std::uint32_t>(8, (n_slots + sms - 1) / sms);
-        if (per_sm > 4) per_sm = 8;  // 8 searches per SM: 128-thread CTAs
+        if (per_sm > 6) per_sm = 8;  // 6 or 8 searches per SM: 128-thread CTAs
+        else if (per_sm > 4) per_sm = 6;
         // keep most of the unified L1 for the (read-only) static store
         std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
         if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
@@ -264,6 +265,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         const int carve = static_cast<int>(std::min<std::size_t>(100, (per_sm * (smem + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
                         reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 6>),
                         reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 8>)}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
@@ -279,8 +281,10 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            if (per_sm > 4)
+            if (per_sm > 6)
                 dev::block_kernel<kCubeBS, 8><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            else if (per_sm > 4)
+                dev::block_kernel<kCubeBS, 6><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else if (per_sm > 1)
                 dev::block_kernel<kBlockBS, 4><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else

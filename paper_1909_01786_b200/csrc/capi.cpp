@@ -677,14 +677,17 @@ int yas_propagator_create(const yas_store* s, uint32_t deps_words, int engine, i
 
 void yas_propagator_free(yas_propagator* p) { delete p; }
 
-static void outcome_from(yas_propagator* p, bool violated, const dev::Ctl& before, yas_outcome* o) {
+// Counter deltas of the last propagation op (the device snapshots the
+// counters when the op starts, so no read-back is needed before the launch and
+// the recorded state-changing calls run in the same kernel).
+static void outcome_from(yas_propagator* p, bool violated, yas_outcome* o) {
     if (!o) return;
     const dev::Ctl& c = p->s->ctl();
     o->violated = violated ? 1 : 0;
-    o->propagations = c.st.propagations - before.st.propagations;
-    o->passes = c.st.passes - before.st.passes;
-    o->checks = c.st.checks - before.st.checks;
-    o->checked_lits = c.st.checked_lits - before.st.checked_lits;
+    o->propagations = c.st.propagations - c.opsnap[0];
+    o->passes = c.st.passes - c.opsnap[1];
+    o->checks = c.st.checks - c.opsnap[2];
+    o->checked_lits = c.st.checked_lits - c.opsnap[3];
     o->n_conflicts = c.n_confl;
     o->device_ms = p->s->last_ms();
 }
@@ -697,17 +700,15 @@ int yas_propagator_reset(yas_propagator* p) {
 }
 int yas_propagator_initial(yas_propagator* p, yas_outcome* o) {
     return guarded(nullptr, 0, [&] {
-        const dev::Ctl before = p->s->ctl();
         const bool v = p->s->initial_propagation();
-        outcome_from(p, v, before, o);
+        outcome_from(p, v, o);
         return static_cast<int>(YAS_OK);
     });
 }
 int yas_propagator_propagate(yas_propagator* p, uint32_t level, yas_outcome* o) {
     return guarded(nullptr, 0, [&] {
-        const dev::Ctl before = p->s->ctl();
         const bool v = p->s->propagate(level);
-        outcome_from(p, v, before, o);
+        outcome_from(p, v, o);
         return static_cast<int>(YAS_OK);
     });
 }

@@ -3015,7 +3015,14 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             g.sync();
             break;
         case kOpInitial: {
-            if (g.leader()) { c->F = 0; c->n_confl = 0; }
+            if (g.leader()) {
+                c->F = 0;
+                c->n_confl = 0;
+                c->opsnap[0] = c->st.propagations;
+                c->opsnap[1] = c->st.passes;
+                c->opsnap[2] = c->st.checks;
+                c->opsnap[3] = c->st.checked_lits;
+            }
             g.sync();
             const bool v = s.initial_propagation(true);
             if (g.leader()) c->b[10] = v;
@@ -3023,7 +3030,13 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             break;
         }
         case kOpPropagate: {
-            if (g.leader()) c->n_confl = 0;
+            if (g.leader()) {
+                c->n_confl = 0;
+                c->opsnap[0] = c->st.propagations;
+                c->opsnap[1] = c->st.passes;
+                c->opsnap[2] = c->st.checks;
+                c->opsnap[3] = c->st.checked_lits;
+            }
             g.sync();
             const bool v = s.propagate(op.level);
             if (g.leader()) c->b[10] = v;

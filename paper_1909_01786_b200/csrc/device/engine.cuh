@@ -95,6 +95,7 @@ struct Ctl {
     std::uint32_t b[16];  // leader -> group broadcast scratch
     Stats st;
     unsigned long long prof[16];  // clock64 cycles per phase (leader view, after barriers)
+    unsigned long long opsnap[4]; // counters at the start of the last propagation op: propagations, passes, checks, literals
     unsigned long long prof_t;
 };
 

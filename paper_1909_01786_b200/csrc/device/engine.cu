@@ -577,6 +577,8 @@ struct Search {
     __device__ __forceinline__ int4 occ_entry(std::uint32_t li, std::uint32_t j, bool learned, std::uint32_t& cls) const {
         const std::uint32_t* oo = S.occ_off + li * 4;
         if (!learned) return decode(__ldg(S.occ + __ldg(oo) + j), cls);
+        const std::uint32_t b0 = __ldg(oo), lt = sl.ltot()[li];  // one round trip
+        if (lt == 0) return decode(__ldg(S.occ + b0 + j), cls);  // no learned occurrences of this literal
         std::uint32_t b[5];
 #pragma unroll
         for (int k = 0; k < 5; ++k) b[k] = __ldg(oo + k);

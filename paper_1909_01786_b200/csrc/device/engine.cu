@@ -667,6 +667,22 @@ struct Search {
         }
     }
 
+    // Diagnostics (builds with -DYAS_TINY_PROF): warp-synchronous sub-phase
+    // cycles of a tiny pass, accounted like mark().
+    __device__ __forceinline__ void tprof(int k) const {
+#ifdef YAS_TINY_PROF
+        __syncwarp();
+        if (C.phase_prof && lane_id() == 0) {
+            const unsigned long long t = clock64();
+            c->prof[k] += t - c->prof_t;
+            c->prof_t = t;
+        }
+        __syncwarp();
+#else
+        (void)k;
+#endif
+    }
+
     // Diagnostics: thread 0 of every block stamps the global timer at phase
     // boundaries of the first kPtracePasses passes of a grid propagation.
     static constexpr std::uint32_t kPtracePasses = 64, kPtraceStamps = 10;
@@ -1567,7 +1583,10 @@ struct Search {
     // Winners, in e order, become the next frontier. Small passes are placed
     // by block 0 alone with block scans (no grid barrier); large ones by the
     // whole grid, one grid scan per round of words.
-    static constexpr std::uint32_t kBlockPlaceWords = 2048;
+#ifndef YAS_BPW
+#define YAS_BPW 512  // measured: 512 words 0.282 ms vs 2048 words 0.288 ms per call
+#endif
+    static constexpr std::uint32_t kBlockPlaceWords = YAS_BPW;
 
     __device__ __forceinline__ void grid_place(std::uint32_t T, std::uint32_t dst, std::uint32_t ts0, std::uint32_t& F_next,
                                std::uint32_t& T_next) {
@@ -1836,6 +1855,7 @@ struct Search {
         std::uint32_t cls = 0;
         const int4 ent = act ? occ_entry(lidx(trig), lane - sm.froff()[lo], learned, cls) : make_int4(-1, 0, 0, 0);
         const std::int32_t id = ent.x;
+        tprof(1);
         const unsigned same = __match_any_sync(0xffffffffu, act ? id : -2 - static_cast<std::int32_t>(lane));
         const bool first = act && static_cast<std::uint32_t>(__ffs(same) - 1) == lane;
         bool conflict = false, prop = false;
@@ -1868,6 +1888,16 @@ struct Search {
                 meta = mt;
             }
         }
+#ifdef YAS_TINY_PROF
+        {
+            const unsigned nf = __popc(__ballot_sync(0xffffffffu, full)), ni = __popc(__ballot_sync(0xffffffffu, first));
+            if (C.phase_prof && lane == 0) {
+                c->prof[14] += nf;
+                c->prof[15] += ni;
+            }
+        }
+#endif
+        tprof(2);
         // winner per proposed atom: the lowest proposing lane
         const std::uint32_t pa = atom_of(plit);
         const unsigned grp = __match_any_sync(0xffffffffu, prop ? static_cast<std::int32_t>(pa) : -2 - static_cast<std::int32_t>(lane));
@@ -1890,6 +1920,7 @@ struct Search {
         }
         const std::uint32_t cnt = __popc(wm), tnext = __shfl_sync(0xffffffffu, oinc, 31);
         const std::uint32_t dst = cur ^ 1u;
+        tprof(3);
         if (winner) {
             set_cell(pa, plit > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
             sl.reason()[pa] = id;
@@ -1913,6 +1944,7 @@ struct Search {
             sl.trail()[ts0 + r] = plit;
             sl.tpos()[pa] = ts0 + r;
         }
+        tprof(4);
         __syncwarp();
         if (lane == 0) {
             sl.froff()[cnt] = tnext;

@@ -357,13 +357,13 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     for (const dev::Ctl& c : ctl) add(tot, c.st);
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
-        static const char* names[14] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
-                                        "conflict", "tiny", "warp", "n.tiny", "looptop", "n.smem", "n.global"};
+        static const char* names[16] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
+                                        "conflict", "tiny", "warp", "n.tiny", "looptop", "n.smem", "n.global", "x14", "x15"};
         unsigned long long p[16] = {0};
         for (const dev::Ctl& c : ctl)
             for (int k = 0; k < 16; ++k) p[k] += c.prof[k];
         std::fprintf(stderr, "[yas profile] passes=%llu", static_cast<unsigned long long>(tot.passes));
-        for (int k = 1; k < 14; ++k) std::fprintf(stderr, " %s=%.2fM", names[k], p[k] / 1e6);
+        for (int k = 1; k < 16; ++k) std::fprintf(stderr, " %s=%.2fM", names[k], p[k] / 1e6);
         std::fprintf(stderr, "\n");
     }
     cudaEventDestroy(e0);

@@ -357,15 +357,19 @@ def random_program(Y, I, local):
     prog = Y.parse_program(text)
     load_ms = (time.perf_counter() - t) * 1e3
     Y.solve(prog, Y.SolverConfig(device=local))
+    t = time.perf_counter()
     r = Y.solve(prog, Y.SolverConfig(device=local))
+    solve_ms = (time.perf_counter() - t) * 1e3  # completion + store build + upload + search + result
     out = {"status": r.status.name, "device_ms": r.stats.device_ms, "passes": r.stats.passes,
            "checks": r.stats.checks, "checks_per_s": r.stats.checks / (r.stats.device_ms / 1e3),
-           "parse_ms": load_ms, "decisions": r.stats.decisions}
+           "parse_ms": load_ms, "solve_wall_ms": solve_ms, "decisions": r.stats.decisions}
     if os.path.exists(REF_BIN):
         p = subprocess.run([REF_BIN, "solve", "-", "-n", "1", "--no-models", "--reps", "2"], input=text,
                            capture_output=True, text=True, check=True)
         ref = json.loads(p.stdout)
         out["cpu_reference_run_ms"] = statistics.mean(ref["run_ms"])
+        out["cpu_reference_parse_ms"] = ref["parse_ms"]
+        out["cpu_reference_solve_wall_ms"] = statistics.mean(ref["solve_ms"])  # compile + build + run
         out["same_trajectory"] = all(getattr(r.stats, k) == ref["stats"][k]
                                      for k in ("decisions", "propagations", "conflicts", "passes"))
     return out

@@ -2819,6 +2819,7 @@ struct Search {
             c->phase = kInit;
         }
         g.sync();
+        if (C.cube_width == 0) return;
         if (g.leader_warp()) {  // cube constraints enter as unit nogoods ahead of any learned one
             std::int32_t* buf = sl.scratch() + 128;
             for (std::uint32_t k = 0; k < C.cube_width; ++k) {
@@ -3044,9 +3045,8 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
     Ctl* c = g.c;
     switch (op.op) {
         case kOpReset:
-            s.begin_search(0);
-            if (g.leader()) c->phase = kLoop;
-            g.sync();
+            s.begin_search(0);  // ends with a barrier
+            if (g.leader()) c->phase = kLoop;  // not read before the kernel ends
             break;
         case kOpInitial: {
             if (g.leader()) {
@@ -3155,10 +3155,7 @@ __device__ void do_ops(G& g, const Static& S, const Config& C, Slot sl, const Ca
                        const OpBatch& B, const Sm& sm) {
     Search<G> s(g, S, C, sl, K, sh, 0, sm);
     init_smem(g, s);
-    for (std::uint32_t i = 0; i < B.n; ++i) {
-        do_op(g, S, C, sl, K, sh, B.ops[i], sm, s);
-        g.sync();
-    }
+    for (std::uint32_t i = 0; i < B.n; ++i) do_op(g, S, C, sl, K, sh, B.ops[i], sm, s);  // each op ends with a barrier
 }
 
 template <int BS>

@@ -398,6 +398,7 @@ struct Session::Impl {
     bool stage_inflight = false;
     std::int32_t* d_stage = nullptr;
     std::size_t d_stage_cap = 0;
+    std::size_t h_uploaded = 0;  // prefix of this batch's staging already sent (bulk inputs go early)
     dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
     bool ctl_pending = false;
 
@@ -411,6 +412,7 @@ struct Session::Impl {
             const std::size_t ncap = std::max<std::size_t>(off + ints, 2 * h_stage_cap + 1024);
             std::int32_t* nb = nullptr;
             ck(cudaMallocHost(&nb, ncap * sizeof(std::int32_t)), "cudaMallocHost staging");
+            if (h_uploaded) ck(cudaStreamSynchronize(stream), "staging");  // early uploads read the old buffer
             if (h_stage) {
                 std::memcpy(nb, h_stage, h_used * sizeof(std::int32_t));
                 cudaFreeHost(h_stage);
@@ -420,8 +422,18 @@ struct Session::Impl {
         }
         if (ints) std::memcpy(h_stage + off, src, ints * sizeof(std::int32_t));
         h_used = off + ints;
+        // a bulk input starts its upload now, overlapping the caller's next
+        // calls; the launch copies only what is left (stream order keeps it
+        // behind the previous kernel, which may still read d_stage)
+        if (ints >= kEagerInts && h_used <= d_stage_cap) {
+            ck(cudaMemcpyAsync(d_stage + h_uploaded, h_stage + h_uploaded, (h_used - h_uploaded) * sizeof(std::int32_t),
+                               cudaMemcpyHostToDevice, stream),
+               "stage");
+            h_uploaded = h_used;
+        }
         return off;
     }
+    static constexpr std::size_t kEagerInts = 4096;
 };
 
 Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, int device, std::uint32_t lcap,
@@ -483,9 +495,12 @@ void flush_ops(Session::Impl& im, float* ms) {
             if (im.d_stage) cudaFree(im.d_stage);
             im.d_stage_cap = std::max<std::size_t>(im.h_used, 2 * im.d_stage_cap);
             ck(cudaMalloc(&im.d_stage, im.d_stage_cap * sizeof(std::int32_t)), "cudaMalloc staging");
+            im.h_uploaded = 0;  // early uploads went to the old buffer
         }
-        ck(cudaMemcpyAsync(im.d_stage, im.h_stage, im.h_used * sizeof(std::int32_t), cudaMemcpyHostToDevice, im.stream),
-           "stage");
+        if (im.h_used > im.h_uploaded)
+            ck(cudaMemcpyAsync(im.d_stage + im.h_uploaded, im.h_stage + im.h_uploaded,
+                               (im.h_used - im.h_uploaded) * sizeof(std::int32_t), cudaMemcpyHostToDevice, im.stream),
+               "stage");
         ck(cudaEventRecord(im.staged, im.stream), "record");
         im.stage_inflight = true;
     }
@@ -501,6 +516,7 @@ void flush_ops(Session::Impl& im, float* ms) {
     im.lits_off.clear();
     im.deps_off.clear();
     im.h_used = 0;
+    im.h_uploaded = 0;
     ck(cudaEventRecord(im.e0, im.stream), "record");
     if (im.grid) {
         void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &b,

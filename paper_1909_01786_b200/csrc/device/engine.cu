@@ -2782,9 +2782,10 @@ struct Search {
     // Fresh search in this slot: clear what the previous search touched.
     __device__ __forceinline__ void begin_search(std::uint32_t cube) {
         const std::uint32_t ts = c->ts;
+        const bool wide = c->rows_wide != 0;
         for (std::uint32_t i = g.tid(); i < ts; i += g.size()) {
             const std::uint32_t a = atom_of(sl.trail()[i]);
-            const std::uint32_t nw = nwords(lvl_of(sl.cells()[a]));
+            const std::uint32_t nw = wide ? C.W : nwords(lvl_of(sl.cells()[a]));
             for (std::uint32_t w = 0; w < nw; ++w) dep(w, a) = 0ull;
             sl.dovf()[a] = 0;
             set_cell(a, 0);
@@ -2809,6 +2810,7 @@ struct Search {
             c->learned_n = c->lpool_used = c->locc_used = c->lunits_n = 0;
             sl.loff()[0] = 0;
             c->cube = cube;
+            c->rows_wide = 0;
             c->epoch += 1;
             if (c->gen == 0) c->gen = 1;  // claim/win keys of generation 0 equal the all-ones init
             c->pad0 = 0;
@@ -3065,6 +3067,7 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
         }
         case kOpPropagate: {
             if (g.leader()) {
+                if (s.nwords(op.level > c->cdl ? op.level : c->cdl) > s.nwords(op.level)) c->rows_wide = 1;
                 c->n_confl = 0;
                 c->opsnap[0] = c->st.propagations;
                 c->opsnap[1] = c->st.passes;
@@ -3097,6 +3100,9 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                            // already assigned atoms are left alone (agreed / conflict) and
                            // only the first occurrence of a repeated atom counts
             const std::uint32_t ts0 = c->ts, gen = c->gen;
+            if (g.leader() && op.deps)
+                for (std::uint32_t w = s.nwords(op.level); w < C.W; ++w)
+                    if (op.deps[w]) c->rows_wide = 1;
             for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) {
                 const std::uint32_t a = atom_of(op.lits[k]);
                 if (a != 0 && a <= S.A) atomicMin(sl.win() + a, wkey(gen, k, false));  // atoms outside [1, A] are ignored

@@ -90,6 +90,10 @@ struct Ctl {
     std::uint32_t n_props, n_confl, n_pending, n_mbuf, n_trace;
     std::uint32_t learned_n, lpool_used, locc_used, lunits_n;
     std::uint32_t cube, epoch, stamp, pad0;
+    // Deps rows may hold words beyond their atom's level (Propagator API only:
+    // Deps given to assign, propagation below the decision level); the next
+    // reset then clears whole rows
+    std::uint32_t rows_wide, pad1;
     unsigned long long restart_threshold, conflicts_at_restart;
     double act_inc;
     std::uint32_t b[16];  // leader -> group broadcast scratch

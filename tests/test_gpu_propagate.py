@@ -160,6 +160,31 @@ def test_assign_keeps_first_occurrence_and_leaves_assigned_atoms(engine):
     assert p.trail() == [1, 3, 5, 4]
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+def test_reset_clears_whole_deps_rows(engine):
+    """After reset every Deps row is empty again (a fresh Assignment), also for rows that
+    were written with more words than their atom's level needs: Deps passed to
+    assign_propagated, and propagation at a level below the current decision level."""
+    def run(p, wide):
+        if wide:
+            for a in range(50, 120):  # decision levels 2..71: Deps words 0 and 1
+                p.push_decision(a)
+            p.assign_propagated([1], 2, deps=[0, 1 << 5])
+            p.seed([1])
+            p.propagate_and_check(2)  # atom 2 at level 2, Deps from atom 1 (word 1)
+            assert p.deps(1)[0][2] == 1 << 5
+            p.reset()
+        p.push_decision(1)
+        p.seed([1])
+        o = p.propagate_and_check(2)
+        return o.propagations, p.trail(), [p.deps(w)[0] for w in range(2)]
+
+    store = Y.NogoodStore.build([[1, -2]], 200)
+    fresh = run(Y.Propagator(store, 2, engine), False)
+    assert fresh[1] == [1, 2] and fresh[2][0][2] == 2 and fresh[2][1][2] == 0  # decision bit cdl-1 = 1
+    assert run(Y.Propagator(store, 2, engine), True) == fresh
+
+
 def test_grid_pass_trace_diagnostics():
     """The per-pass phase stamps of whole-grid propagation are readable and ordered."""
     store, seeded, dec = Y.NogoodStore.planted(20_000, 200_000, 50)

@@ -356,13 +356,16 @@ def random_program(Y, I, local):
     t = time.perf_counter()
     prog = Y.parse_program(text)
     load_ms = (time.perf_counter() - t) * 1e3
+    t = time.perf_counter()
     Y.solve(prog, Y.SolverConfig(device=local))
+    solve_ms = (time.perf_counter() - t) * 1e3  # first call: completion + store build + upload + search + result
     t = time.perf_counter()
     r = Y.solve(prog, Y.SolverConfig(device=local))
-    solve_ms = (time.perf_counter() - t) * 1e3  # completion + store build + upload + search + result
+    solve_cached_ms = (time.perf_counter() - t) * 1e3  # the program keeps its compiled store
     out = {"status": r.status.name, "device_ms": r.stats.device_ms, "passes": r.stats.passes,
            "checks": r.stats.checks, "checks_per_s": r.stats.checks / (r.stats.device_ms / 1e3),
-           "parse_ms": load_ms, "solve_wall_ms": solve_ms, "decisions": r.stats.decisions}
+           "parse_ms": load_ms, "solve_wall_ms": solve_ms, "solve_wall_ms_compiled": solve_cached_ms,
+           "decisions": r.stats.decisions}
     if os.path.exists(REF_BIN):
         p = subprocess.run([REF_BIN, "solve", "-", "-n", "1", "--no-models", "--reps", "2"], input=text,
                            capture_output=True, text=True, check=True)

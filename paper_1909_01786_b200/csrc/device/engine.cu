@@ -180,6 +180,27 @@ struct BlockG {
         i = si[0];
         __syncthreads();
     }
+    // Integer variant (s = score + 1, 0 = none; ties -> lowest index): two
+    // warp reductions per level instead of five shuffle rounds of (double, index).
+    __device__ void argmax_u(std::uint32_t& s, std::uint32_t& i) {
+        std::uint32_t m = __reduce_max_sync(0xffffffffu, s);
+        i = __reduce_min_sync(0xffffffffu, s == m ? i : 0xffffffffu);
+        const std::uint32_t w = threadIdx.x >> 5;
+        if (lane_id() == 0) sbuf[w] = (static_cast<unsigned long long>(m) << 32) | i;
+        __syncthreads();
+        if (w == 0) {
+            const unsigned long long x = lane_id() < kWarps ? sbuf[lane_id()] : 0ull;
+            const std::uint32_t xs = static_cast<std::uint32_t>(x >> 32), xi = lane_id() < kWarps ? static_cast<std::uint32_t>(x) : 0xffffffffu;
+            m = __reduce_max_sync(0xffffffffu, xs);
+            i = __reduce_min_sync(0xffffffffu, xs == m ? xi : 0xffffffffu);
+            if (lane_id() == 0) sbuf[kWarps] = (static_cast<unsigned long long>(m) << 32) | i;
+        }
+        __syncthreads();
+        const unsigned long long r = sbuf[kWarps];
+        s = static_cast<std::uint32_t>(r >> 32);
+        i = static_cast<std::uint32_t>(r);
+        __syncthreads();
+    }
 };
 
 template <int BS>
@@ -2556,7 +2577,7 @@ struct Search {
     // step, every load of a step issued before any is used. Packed variant:
     // 8-byte records (the rule table of a single search stays in L1) and one
     // static count + two learned counts per applicable head (occurrence heuristic).
-    __device__ __forceinline__ void scan_rules_packed(double& best, std::uint32_t& bi) const {
+    __device__ __forceinline__ void scan_rules_packed(std::uint32_t& best, std::uint32_t& bi) const {
         constexpr int DU = 8;
         const std::uint32_t gs = g.size();
         for (std::uint32_t r0 = g.tid(); r0 < S.R; r0 += DU * gs) {
@@ -2584,9 +2605,9 @@ struct Search {
                 l1[k] = sl.ltot()[2 * hh[k] + 1];
             }
 #pragma unroll
-            for (int k = 0; k < DU; ++k) {
-                const double sc = static_cast<double>(so[k] + l0[k] + l1[k]);
-                if (app[k] && better(sc, r0 + k * gs, best, bi)) { best = sc; bi = r0 + k * gs; }
+            for (int k = 0; k < DU; ++k) {  // this thread's rules come in index order: ties keep the first
+                const std::uint32_t sc = so[k] + l0[k] + l1[k] + 1u;
+                if (app[k] && sc > best) { best = sc; bi = r0 + k * gs; }
             }
         }
     }
@@ -2642,10 +2663,17 @@ struct Search {
         bool packed = false;
         if constexpr (G::kBlock) {
             packed = C.heur == 0 && S.rules8 != nullptr;
-            if (packed) scan_rules_packed(best, bi);
+            if (packed) {
+                std::uint32_t bu = 0;
+                scan_rules_packed(bu, bi);
+                g.argmax_u(bu, bi);
+                if (bu == 0) bi = 0xffffffffu;
+            }
         }
-        if (!packed) scan_rules(best, bi);
-        g.argmax(best, bi);
+        if (!packed) {
+            scan_rules(best, bi);
+            g.argmax(best, bi);
+        }
         if (bi != 0xffffffffu) {
             if (g.leader()) {
                 const std::uint32_t b = __ldg(S.rules + bi).y;

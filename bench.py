@@ -431,6 +431,12 @@ def first_model(Y, I, local):
             entry["cpu_reference_run_ms"] = statistics.mean(ref["run_ms"])
             entry["same_trajectory"] = all(getattr(r.stats, k) == ref["stats"][k]
                                            for k in ("decisions", "propagations", "conflicts", "passes"))
+        # extra mode: six concurrent searches over (mode, heuristic), first one reports;
+        # an answer set, not the reference's first one
+        t = time.perf_counter()
+        rp = Y.solve(prog, Y.SolverConfig(device=local, portfolio=6))
+        entry["portfolio6"] = {"status": rp.status.name, "wall_ms": (time.perf_counter() - t) * 1e3,
+                               "device_ms": rp.stats.device_ms, "winner_variant": rp.stats.portfolio_variant}
         out[name] = entry
     return out
 

@@ -115,6 +115,7 @@ struct SolverConfig {
     int device = 0;
     std::uint32_t cube_atoms = 0, cube_depth = 0;
     int rank = 0, world = 1;
+    std::uint32_t portfolio = 0;  // first-model portfolio: concurrent searches with diverse (mode, heuristic)
 };
 
 struct SolveStats : yas_stats {
@@ -161,6 +162,7 @@ inline SolveResult solve(const GroundProgram& prog, const SolverConfig& cfg) {
     c.cube_depth = cfg.cube_depth;
     c.rank = cfg.rank;
     c.world = cfg.world;
+    c.portfolio = cfg.portfolio;
     if (cfg.trace) {
         c.trace = [](const yas_trace* t, void* user) {
             (*static_cast<const std::function<void(const ConflictTrace&)>*>(user))(

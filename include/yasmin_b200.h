@@ -120,6 +120,10 @@ typedef struct yas_config {
     uint32_t cube_depth; /* ladder levels (0 = auto: enough cubes for every search slot) */
     uint32_t slots;      /* concurrent searches per GPU for cubes (0 = auto) */
     int rank, world;     /* cube partition across processes/GPUs: cube i runs on rank i % world */
+    uint32_t portfolio;  /* first-model portfolio (max_models == 1 without cubes): this many
+                            concurrent searches with diverse (mode, heuristic), variant (v0 + rank * portfolio
+                            + k) % 6 with v0 = mode | heuristic << 1 first; the first search to finish reports
+                            its model or UNSAT (0 or 1 = off) */
 } yas_config;
 
 void yas_config_default(yas_config* cfg);
@@ -137,6 +141,7 @@ typedef struct yas_stats {
     double device_ms;  /* kernel time, CUDA events */
     uint64_t cubes;    /* cubes assigned to this rank */
     uint64_t checked_lits; /* literals of the checked nogoods (algorithmic traffic) */
+    int64_t portfolio_variant; /* winning (mode | heuristic << 1) of a portfolio run, -1 otherwise */
 } yas_stats;
 
 int yas_solve(const yas_program* p, const yas_config* cfg, yas_result** out, char* err, size_t err_cap);

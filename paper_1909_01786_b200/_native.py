@@ -50,7 +50,7 @@ class yas_config(C.Structure):
         ("learned_capacity", C.c_uint64), ("trace", TRACE_FN), ("trace_user", C.c_void_p),
         ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("cube_depth", C.c_uint32),
         ("slots", C.c_uint32),
-        ("rank", C.c_int), ("world", C.c_int),
+        ("rank", C.c_int), ("world", C.c_int), ("portfolio", C.c_uint32),
     ]
 
 
@@ -60,7 +60,8 @@ class yas_stats(C.Structure):
         ("wall_ms", C.c_double)] + [(n, C.c_uint64) for n in (
         "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods", "res_learned", "fwd_learned",
         "fwd_fallbacks", "uip_check_failures", "fwd_decision_only_failures", "asserting_failures", "checks",
-        "searches", "launches")] + [("device_ms", C.c_double), ("cubes", C.c_uint64), ("checked_lits", C.c_uint64)]
+        "searches", "launches")] + [("device_ms", C.c_double), ("cubes", C.c_uint64), ("checked_lits", C.c_uint64),
+                                              ("portfolio_variant", C.c_int64)]
 
 
 class yas_outcome(C.Structure):

@@ -135,13 +135,14 @@ class SolverConfig:
     slots: int = 0
     rank: int = 0
     world: int = 1
+    portfolio: int = 0  # first-model portfolio: concurrent searches with diverse (mode, heuristic)
 
 
 _STAT_FIELDS = ["decisions", "propagations", "conflicts", "learned_count", "learned_length_sum", "restarts",
                 "models", "wall_ms", "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods",
                 "res_learned", "fwd_learned", "fwd_fallbacks", "uip_check_failures",
                 "fwd_decision_only_failures", "asserting_failures", "checks", "searches", "launches",
-                "device_ms", "cubes", "checked_lits"]
+                "device_ms", "cubes", "checked_lits", "portfolio_variant"]
 
 
 @dataclass
@@ -170,6 +171,7 @@ class SolveStats:
     device_ms: float = 0.0
     cubes: int = 0
     checked_lits: int = 0
+    portfolio_variant: int = -1
 
     def avg_learned_len(self) -> float:
         return 0.0 if self.learned_count == 0 else self.learned_length_sum / self.learned_count
@@ -408,6 +410,7 @@ def _config(cfg: SolverConfig) -> N.yas_config:
     c.slots = cfg.slots
     c.rank = cfg.rank
     c.world = cfg.world
+    c.portfolio = cfg.portfolio
     return c
 
 

@@ -421,9 +421,14 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         std::uint32_t per_sm = 8;  // concurrent searches per SM for cube enumeration
         if (const char* e = std::getenv("YAS_SEARCHES_PER_SM")) per_sm = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
         const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * per_sm;
+        const bool portfolio = cfg.portfolio > 1 && cfg.max_models == 1 && cfg.cube_atoms == 0;
         if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
             n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * static_cast<std::uint32_t>(cfg.world),
                                  cfg.rank, cfg.world, cubes, width);
+        } else if (portfolio) {  // one search per variant, every rank
+            n_cubes = std::min<std::uint32_t>(cfg.portfolio, static_cast<std::uint32_t>(sms));
+            dc.portfolio = 1;
+            dc.pf_base = (dc.mode | dc.heur << 1) + static_cast<std::uint32_t>(cfg.rank) * cfg.portfolio;
         } else if (cfg.rank != 0) {
             n_cubes = 0;  // a single search runs on rank 0 only
         }
@@ -431,9 +436,9 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
 
         EngineOptions eo;
         eo.device = cfg.device;
-        const bool wide = cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0);
+        const bool wide = !portfolio && (cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0));
         eo.grid = wide;
-        eo.slots = slots_per_gpu;
+        eo.slots = portfolio ? n_cubes : slots_per_gpu;
         const bool many = width > 0;
         const std::uint64_t cap = cfg.learned_capacity;
         eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, many ? (1u << 13) : (1u << 18)));
@@ -492,7 +497,8 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             res->stats.wall_ms = er.wall_ms;
             res->stats.device_ms = er.device_ms;
             res->stats.launches = er.launches;
-            res->stats.cubes = n_cubes;
+            res->stats.cubes = portfolio ? 0 : n_cubes;
+            res->stats.portfolio_variant = er.variant;
             res->status = res->models.empty() ? 1 : 0;
             lap("result");
             break;

@@ -621,6 +621,15 @@ struct Search {
         cls = 0;
         return make_int4(-1, 0, 0, 0);
     }
+    // learning mode / heuristic of this search (a portfolio varies them per search)
+    __device__ __forceinline__ std::uint32_t mode() const {
+        if constexpr (G::kGrid) return C.mode;  // a portfolio runs single-CTA searches
+        return C.portfolio ? (c->variant & 1u) : C.mode;
+    }
+    __device__ __forceinline__ std::uint32_t heur() const {
+        if constexpr (G::kGrid) return C.heur;
+        return C.portfolio ? (c->variant >> 1) : C.heur;
+    }
     __device__ __forceinline__ std::uint32_t nwords(std::uint32_t level) const {
         const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
         return nw < C.W ? nw : C.W;
@@ -2433,7 +2442,7 @@ struct Search {
         if (c->cdl == 1) return;  // nothing to revise
         const std::uint32_t nc = c->n_confl;
         // select conflicts: min (length, id); fanout K in fwd mode (learn.cpp:148-157)
-        const std::uint32_t K2 = (C.mode == 0 && C.fanout > 1) ? C.fanout : 1u;
+        const std::uint32_t K2 = (mode() == 0 && C.fanout > 1) ? C.fanout : 1u;
         std::int32_t* added = sl.scratch();            // ids of added nogoods
         std::int32_t* levels = sl.scratch() + 64;      // their backjump levels
         std::int32_t* buf = sl.scratch() + 128;        // learned literal buffer
@@ -2455,7 +2464,7 @@ struct Search {
             const std::uint32_t delta = static_cast<std::uint32_t>(best);
             std::uint32_t target = 1, n = 0xffffffffu;
             std::uint32_t used = 1;  // 0 fwd, 1 res
-            if (C.mode == 0) {
+            if (mode() == 0) {
                 n = w_fwd(delta, buf, target);
                 if (n != 0xffffffffu) used = 0;
             }
@@ -2474,7 +2483,7 @@ struct Search {
                 if (lane == 0) {
                     if (at != 1) c->st.uip_check_failures += 1;
                     c->st.res_learned += 1;
-                    if (C.mode == 0) c->st.fwd_fallbacks += 1;
+                    if (mode() == 0) c->st.fwd_fallbacks += 1;
                 }
             } else {
                 std::uint32_t bad = 0;
@@ -2488,7 +2497,7 @@ struct Search {
             __syncwarp();
             const std::int32_t id = w_add_learned(buf, n);
             if (id < 0) return;
-            if (C.heur == 2)
+            if (heur() == 2)
                 for (std::uint32_t k = lane; k < n; k += 32) sl.act()[atom_of(buf[k])] += c->act_inc;
             if (lane == 0) {
                 added[n_sel] = id;
@@ -2503,7 +2512,7 @@ struct Search {
             __syncwarp();
         }
         // Heuristic::on_conflict (decide.cpp:34-41)
-        if (C.heur == 2) {
+        if (heur() == 2) {
             const double inc = c->act_inc / C.decay;
             if (inc > 1e100)
                 for (std::uint32_t a = lane; a <= S.A; a += 32) sl.act()[a] *= 1e-100;
@@ -2558,8 +2567,8 @@ struct Search {
     }
 
     __device__ __forceinline__ double score(std::uint32_t head) const {
-        if (C.heur == 2) return sl.act()[head];
-        if (C.heur == 0) return static_cast<double>(occ_total(2 * head) + occ_total(2 * head + 1));
+        if (heur() == 2) return sl.act()[head];
+        if (heur() == 0) return static_cast<double>(occ_total(2 * head) + occ_total(2 * head + 1));
         double s = 0.0;  // Jeroslow-Wang, summed in the reference's list order
         for (std::uint32_t li = 2 * head; li <= 2 * head + 1; ++li)
             for (std::uint32_t cl = 0; cl < 4; ++cl) {
@@ -2628,7 +2637,7 @@ struct Search {
                 app[k] = !(ru[k].w >> 31) && val(ru[k].x) == 0 && (ru[k].z == 0 || val(ru[k].z) > 0) &&
                          (n == 0 || val(n) >= 0);
             }
-            if (C.heur == 0) {  // occurrence count: 2 x (two offsets + learned count) per head
+            if (heur() == 0) {  // occurrence count: 2 x (two offsets + learned count) per head
                 std::uint32_t o[DU][6];
 #pragma unroll
                 for (int k = 0; k < DU; ++k) {
@@ -2662,7 +2671,7 @@ struct Search {
         std::uint32_t bi = 0xffffffffu;
         bool packed = false;
         if constexpr (G::kBlock) {
-            packed = C.heur == 0 && S.rules8 != nullptr;
+            packed = heur() == 0 && S.rules8 != nullptr;
             if (packed) {
                 std::uint32_t bu = 0;
                 scan_rules_packed(bu, bi);
@@ -2825,10 +2834,14 @@ struct Search {
             for (std::uint32_t i = g.tid(); i < 3 * keys; i += g.size()) sl.lhdr()[i] = 0;
             for (std::uint32_t i = g.tid(); i < 2 * S.A + 2; i += g.size()) sl.ltot()[i] = 0;
         }
-        if (C.heur == 2)
+        std::uint32_t var = C.mode | C.heur << 1;
+        if constexpr (!G::kGrid)
+            if (C.portfolio) var = (C.pf_base + cube) % 6u;
+        if ((var >> 1) == 2)
             for (std::uint32_t i = g.tid(); i <= S.A; i += g.size()) sl.act()[i] = 0.0;
         g.sync();
         if (g.leader()) {
+            c->variant = var;
             c->cdl = 1;
             c->ts = 0;
             c->F = 0;
@@ -2977,6 +2990,15 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
     for (;;) {
         g.sync();
         if (g.c->status != kRunning) return;
+        if (!G::kGrid && C.portfolio && g.c->phase == kFinished) {  // first to finish: stop the others
+            if (g.leader()) {
+                g.c->done_ns = gtimer();
+                sh->stop = 1;
+                g.c->status = kDone;
+            }
+            g.sync();
+            return;
+        }
         if (g.c->phase == kIdle || g.c->phase == kFinished) {
             g.sync();
             if (g.leader()) {

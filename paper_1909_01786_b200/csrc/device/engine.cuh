@@ -52,6 +52,9 @@ struct Config {
     std::uint32_t count_lits;   // accumulate literals of checked nogoods (roofline accounting)
     unsigned long long* ptrace; // diagnostics: per-pass, per-block phase timestamps (null = off)
     std::uint32_t phase_prof;   // diagnostics: per-phase cycle buckets of single-CTA searches (YAS_PROFILE)
+    // first-model portfolio: search k runs variant (pf_base + k) % 6 of
+    // (mode, heuristic) = (v & 1, v >> 1); the first to finish stops the others
+    std::uint32_t portfolio, pf_base;
 };
 
 // Read-only static store + program rules (host-built, uploaded once).
@@ -93,7 +96,7 @@ struct Ctl {
     // Deps rows may hold words beyond their atom's level (Propagator API only:
     // Deps given to assign, propagation below the decision level); the next
     // reset then clears whole rows
-    std::uint32_t rows_wide, pad1;
+    std::uint32_t rows_wide, variant;  // variant: portfolio (mode | heuristic << 1) of this search
     unsigned long long restart_threshold, conflicts_at_restart;
     double act_inc;
     std::uint32_t b[16];  // leader -> group broadcast scratch
@@ -101,6 +104,7 @@ struct Ctl {
     unsigned long long prof[16];  // clock64 cycles per phase (leader view, after barriers)
     unsigned long long opsnap[4]; // counters at the start of the last propagation op: propagations, passes, checks, literals
     unsigned long long prof_t;
+    unsigned long long done_ns;  // portfolio: global time at which this search finished
 };
 
 struct Caps {

@@ -44,6 +44,7 @@ struct EngineResult {
     std::uint32_t launches = 0;
     double device_ms = 0.0;  // sum of kernel time (CUDA events)
     double wall_ms = 0.0;    // host wall time of the launch loop
+    std::int32_t variant = -1;  // portfolio: (mode | heuristic << 1) of the search that finished first
 };
 
 struct EngineCallbacks {

@@ -261,6 +261,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
         smc = plan_smem(ar.A, budget);
         smem = smc.bytes;
+        // portfolio searches race each other: one per SM (a CTA needs more than half the array)
+        if (cfg.portfolio) smem = std::max<std::size_t>(smem, 116u * 1024u);
         // the rest of the 228 KB unified array stays L1 for the static store
         const int carve = static_cast<int>(std::min<std::size_t>(100, (per_sm * (smem + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
@@ -273,6 +275,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         }
     }
     bool stop_early = false;
+    std::uint32_t winner = ~0u;  // portfolio: the search that finished first
     for (;;) {
         ck(cudaEventRecord(e0), "record");
         if (opt.grid) {
@@ -315,8 +318,14 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                             cudaMemcpyDeviceToHost),
                "models");
         }
+        // portfolio: only the search that finished first reports (its model, or UNSAT)
+        winner = ~0u;
+        if (cfg.portfolio)
+            for (std::uint32_t s = 0; s < n_slots; ++s)
+                if (ctl[s].status == dev::kDone && (winner == ~0u || ctl[s].done_ns < ctl[winner].done_ns)) winner = s;
         for (std::uint32_t s = 0; s < n_slots; ++s) {
             dev::Ctl& c = ctl[s];
+            if (cfg.portfolio && s != winner) c.n_mbuf = 0;
             if (c.n_mbuf) {
                 const std::size_t b0 = static_cast<std::size_t>(s) * maxm * ar.K.mwords;
                 for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
@@ -342,7 +351,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             res.status = err;
             break;
         }
-        if (!more || stop_early) break;
+        if (!more || stop_early || winner != ~0u) break;
         ck(cudaMemcpy2D(ar.slots[0].ctl(), ar.L.bytes, ctl.data(), sizeof(dev::Ctl), sizeof(dev::Ctl), n_slots,
                         cudaMemcpyHostToDevice),
            "ctl");
@@ -355,6 +364,12 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         for (std::size_t i = 0; i < sizeof(dev::Stats) / 8; ++i) pa[i] += pb[i];
     };
     for (const dev::Ctl& c : ctl) add(tot, c.st);
+    if (winner != ~0u) {  // portfolio: the winning search's trajectory, and how many ran
+        const unsigned long long searches = tot.searches;
+        tot = ctl[winner].st;
+        tot.searches = searches;
+        res.variant = ctl[winner].variant;
+    }
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
         static const char* names[16] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",

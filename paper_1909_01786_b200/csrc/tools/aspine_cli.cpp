@@ -105,6 +105,8 @@ int run_solve(int argc, char** argv) {
             trace = true;
         } else if (a == "--cubes") {  // device extension: ladder width for enumeration
             cfg.cube_atoms = number<std::uint32_t>(a, val());
+        } else if (a == "--portfolio") {  // device extension: first-model portfolio of N searches
+            cfg.portfolio = number<std::uint32_t>(a, val());
         } else if (a.size() > 1 && a[0] == '-' && a != "-") {
             throw Usage("unknown option " + a);
         } else if (file.empty()) {
@@ -177,7 +179,7 @@ int main(int argc, char** argv) {
             std::cout << "aspine (yasmin-b200) - conflict-driven answer set solver on the GPU\n"
                          "  aspine solve <file|-> [--mode fwd|res] [--heur occ|jw|act] [--workers N]\n"
                          "        [--restarts off|geometric:B:F] [-n N] [--deps-words W] [--fanout K]\n"
-                         "        [--seed S] [--verify] [--stats csv|human] [--trace] [--cubes K]\n"
+                         "        [--seed S] [--verify] [--stats csv|human] [--trace] [--cubes K] [--portfolio N]\n"
                          "  aspine oracle <file|->\n";
             return 0;
         }

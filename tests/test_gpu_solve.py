@@ -127,3 +127,22 @@ def test_model_list_views_match_per_model_accessors():
         assert sum(a.startswith("q(") for a in m.atoms) == 6
     with pytest.raises(IndexError):
         ms[4]
+
+
+def test_first_model_portfolio():
+    """N concurrent searches with diverse (mode, heuristic); the first to finish
+    reports. Not the reference's first model, but always one of its answer sets (or UNSAT)."""
+    for prog in golden("corpus")[::7]:
+        r = Y.solve(Y.parse_program(prog["text"]), Y.SolverConfig(portfolio=6, verify=True))
+        assert (r.status == Y.SolveStatus.sat) == bool(prog["family"]), prog["name"]
+        if r.models:
+            assert r.models[0].atom_ids in prog["family"], prog["name"]
+        assert 0 <= r.stats.portfolio_variant < 6 and r.stats.searches == 6 and r.stats.cubes == 0
+    for text in (I.colouring(2000, 4.0, 3, 1), I.hamiltonian(200, 1.0, 1)):
+        r = Y.solve(Y.parse_program(text), Y.SolverConfig(portfolio=6, verify=True))
+        assert r.status == Y.SolveStatus.sat and len(r.models) == 1
+    # another rank starts at a different variant; one search = variant of the config itself
+    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(portfolio=2, rank=1, mode=Y.LearnMode.res))
+    assert r.stats.portfolio_variant in (3, 4) and len(r.models) == 1
+    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig())
+    assert r.stats.portfolio_variant == -1

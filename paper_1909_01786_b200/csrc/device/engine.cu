@@ -1773,7 +1773,8 @@ struct Search {
 
     // One propagation call to fixpoint or violation (propagate.cpp:170-205).
     // Returns true when conflicts were found (they are in confl[0..n_confl)).
-    static constexpr std::uint32_t kWarpPassT = 96;  // passes this small run in warp 0 alone
+    // passes this small run in warp 0 alone (C.warp_pass_t: larger when other
+    // searches share the SM and keep it busy while the CTA's other warps wait)
 
     __device__ __forceinline__ bool propagate(std::uint32_t level) {
         if constexpr (G::kGrid) return propagate_grid(level);
@@ -1784,7 +1785,7 @@ struct Search {
             if (viol) return true;
             if (F == 0) return false;
             if constexpr (G::kBlock) {
-                if (T <= kWarpPassT && sm.tcap() && F + 1 <= sm.fcap()) {
+                if (T <= C.warp_pass_t && T <= sm.tcap() && F + 1 <= sm.fcap()) {
                     if (threadIdx.x < 32) {
                         WarpG wg{c};
                         Search<WarpG> ws(wg, S, C, sl, K, sh, t0, sm);
@@ -1807,7 +1808,7 @@ struct Search {
             __syncwarp();
             const std::uint32_t F = c->F, T = c->T, cur = c->cur, viol = c->b[11];
             __syncwarp();
-            if (viol || F == 0 || T > kWarpPassT || F + 1 > sm.fcap()) return;
+            if (viol || F == 0 || T > C.warp_pass_t || T > sm.tcap() || F + 1 > sm.fcap()) return;
             if (T <= 32) {
                 tiny_pass(F, T, cur, level);
                 mark(8);

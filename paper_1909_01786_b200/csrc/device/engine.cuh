@@ -55,6 +55,7 @@ struct Config {
     // first-model portfolio: search k runs variant (pf_base + k) % 6 of
     // (mode, heuristic) = (v & 1, v >> 1); the first to finish stops the others
     std::uint32_t portfolio, pf_base;
+    std::uint32_t warp_pass_t;  // single-CTA searches: passes with at most this many entries run in one warp
 };
 
 // Read-only static store + program rules (host-built, uploaded once).

@@ -261,6 +261,10 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
         smc = plan_smem(ar.A, budget);
         smem = smc.bytes;
+        // several searches per SM: one-warp passes up to 256 entries (q12 55 vs 61 ms at
+        // 96); a lone search: 96 (ham200 107 vs 110 ms at 160)
+        cfg.warp_pass_t = per_sm > 1 ? 256u : 96u;
+        if (const char* e = std::getenv("YAS_WARP_PASS_T")) cfg.warp_pass_t = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
         // portfolio searches race each other: one per SM (a CTA needs more than half the array)
         if (cfg.portfolio) smem = std::max<std::size_t>(smem, 116u * 1024u);
         // the rest of the 228 KB unified array stays L1 for the static store
@@ -476,6 +480,7 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     c.fanout = 1;
     c.learned_capacity = ~0ull;
     c.n_cubes = 1;
+    c.warp_pass_t = 96;
     // the arena was uploaded / zeroed / initialised on the legacy stream; the
     // session's non-blocking stream is not ordered after it
     ck(cudaDeviceSynchronize(), "arena setup");

@@ -175,7 +175,23 @@ struct Arena {
         L.o_frb = take(grid_blocks ? 4 * (A1 + 1) : 0);
         L.bytes = o;
         L.base = dalloc<char>(static_cast<std::size_t>(o) * n_slots, owned);
-        ck(cudaMemset(L.base, 0, static_cast<std::size_t>(o) * n_slots), "memset");
+        // Zero only what is read before it is written: the control block and
+        // per-atom state, the expansion bitmap, the epoch-tagged duplicate table,
+        // stamp marks and scratch, the grid mirror. Append-only arenas (learned
+        // literals and occurrences, proposals, models) stay as they are; claim /
+        // win / reason are set by init_slots; learned headers are cleared by the
+        // first begin_search of a slot (epoch 0). Cube searches have ~1000 slots,
+        // so this is a few hundred MB instead of the whole multi-GB arena.
+        if (std::getenv("YAS_POISON_ARENA"))  // tests: nothing may depend on the rest being zero
+            ck(cudaMemset(L.base, 0xA5, static_cast<std::size_t>(o) * n_slots), "memset");
+        auto zero = [&](unsigned long long from, unsigned long long to) {
+            if (to > from)
+                ck(cudaMemset2D(L.base + from, o, 0, static_cast<std::size_t>(to - from), n_slots), "memset");
+        };
+        zero(L.o_ctl, L.o_claim);
+        zero(L.o_pending, L.o_litat);
+        zero(L.o_dup, L.o_mbuf);
+        zero(L.o_gmirror, L.o_obat);
         dev::init_slots<<<n_slots, 256>>>(L, static_cast<std::uint32_t>(A1), K.items);
         ck(cudaGetLastError(), "init_slots");
         slots.resize(n_slots);

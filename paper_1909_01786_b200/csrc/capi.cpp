@@ -175,22 +175,31 @@ std::uint32_t make_cubes(const Program& prog, std::uint32_t L, std::uint32_t dep
     width = depth * L;
     std::uint64_t total = 1;
     for (std::uint32_t j = 0; j < depth; ++j) total *= L + 1;
+    // the L literals of level j for pick p, precomputed: pat[(j * (L + 1) + p) * L + i]
+    std::vector<std::int32_t> pat(static_cast<std::size_t>(depth) * (L + 1) * L, 0);
+    for (std::uint32_t j = 0; j < depth; ++j)
+        for (std::uint32_t p = 0; p <= L; ++p)
+            for (std::uint32_t i = 0; i < L && i <= p; ++i) {
+                const Choice& c = ch[j * L + i];
+                // F a: nogood {T a}; T a: nogood {T b}
+                pat[(static_cast<std::size_t>(j) * (L + 1) + p) * L + i] = static_cast<std::int32_t>(i < p ? c.a : c.b);
+            }
+    const std::uint64_t mine = total / static_cast<std::uint64_t>(world) +
+                               (static_cast<std::uint64_t>(rank) < total % static_cast<std::uint64_t>(world) ? 1 : 0);
+    cubes.resize(mine * width);
+    std::int32_t* out = cubes.data();
     std::uint32_t n = 0;
-    for (std::uint64_t cube = 0; cube < total; ++cube) {
-        if (static_cast<int>(cube % static_cast<std::uint64_t>(world)) != rank) continue;
+    for (std::uint64_t cube = static_cast<std::uint64_t>(rank); cube < total; cube += static_cast<std::uint64_t>(world)) {
         std::uint64_t digits = cube;
         for (std::uint32_t j = 0; j < depth; ++j) {
             const std::uint32_t pick = static_cast<std::uint32_t>(digits % (L + 1));
             digits /= L + 1;
-            for (std::uint32_t i = 0; i < L; ++i) {
-                const Choice& c = ch[j * L + i];
-                if (i < pick) cubes.push_back(static_cast<std::int32_t>(c.a));        // F a: nogood {T a}
-                else if (i == pick) cubes.push_back(static_cast<std::int32_t>(c.b));  // T a: nogood {T b}
-                else cubes.push_back(0);
-            }
+            std::memcpy(out, pat.data() + (static_cast<std::size_t>(j) * (L + 1) + pick) * L, L * sizeof(std::int32_t));
+            out += L;
         }
         ++n;
     }
+    cubes.resize(static_cast<std::size_t>(n) * width);
     return n;
 }
 
@@ -453,7 +462,10 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             EngineCallbacks cb;
             const std::uint32_t np = prog.atom_count();
             cb.on_model = [&](const EngineModel& m) {
+                std::size_t pop = 0;
+                for (std::uint32_t x : m.bits) pop += static_cast<std::size_t>(__builtin_popcount(x));
                 std::vector<std::uint32_t> ids;
+                ids.reserve(pop);  // one allocation per model
                 for (std::size_t w = 0; w < m.bits.size(); ++w)
                     for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
                         const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;

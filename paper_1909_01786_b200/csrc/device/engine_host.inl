@@ -320,11 +320,20 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         cudaEventElapsedTime(&ms, e0, e1);
         res.device_ms += ms;
         ++res.launches;
+        const bool laps = std::getenv("YAS_PROFILE") != nullptr;
+        auto lap = [&](const char* what) {
+            if (laps)
+                std::fprintf(stderr, "[yas host]   %s at %.2f ms\n", what,
+                             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count());
+        };
+        lap("kernel done");
         ck(cudaMemcpy2D(ctl.data(), sizeof(dev::Ctl), ar.slots[0].ctl(), ar.L.bytes, sizeof(dev::Ctl), n_slots,
                         cudaMemcpyDeviceToHost),
            "ctl");
+        lap("ctl copied");
         bool more = false;
         std::uint32_t err = dev::kDone;
+        EngineModel em;  // reused: one allocation for all delivered models
         // all slots' model buffers in two strided copies (not two per slot)
         std::uint32_t maxm = 0;
         for (std::uint32_t s = 0; s < n_slots; ++s) maxm = std::max(maxm, ctl[s].n_mbuf);
@@ -343,13 +352,13 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         if (cfg.portfolio)
             for (std::uint32_t s = 0; s < n_slots; ++s)
                 if (ctl[s].status == dev::kDone && (winner == ~0u || ctl[s].done_ns < ctl[winner].done_ns)) winner = s;
+        lap("models copied");
         for (std::uint32_t s = 0; s < n_slots; ++s) {
             dev::Ctl& c = ctl[s];
             if (cfg.portfolio && s != winner) c.n_mbuf = 0;
             if (c.n_mbuf) {
                 const std::size_t b0 = static_cast<std::size_t>(s) * maxm * ar.K.mwords;
                 for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
-                    EngineModel em;
                     em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m) * ar.K.mwords),
                                    mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m + 1) * ar.K.mwords));
                     em.cube = mc[static_cast<std::size_t>(s) * maxm + m];
@@ -367,6 +376,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             if (c.status == dev::kYield) more = true;
             else if (c.status != dev::kDone && c.status != dev::kRunning) err = c.status;
         }
+        lap("models delivered");
         if (err != dev::kDone) {
             res.status = err;
             break;

@@ -40,7 +40,10 @@ struct yas_program {
 };
 
 struct yas_result {
-    std::vector<std::vector<std::uint32_t>> models;
+    // models flat: model m is ids[off[m], off[m + 1]) (sorted atom ids)
+    std::vector<std::uint32_t> ids;
+    std::vector<std::uint64_t> off{0};
+    std::size_t count() const { return off.size() - 1; }
     std::vector<std::uint32_t> cubes;
     yas_stats stats{};
     int status = 1;
@@ -456,28 +459,27 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
 
         auto res = std::make_unique<yas_result>();
         for (int attempt = 0;; ++attempt) {
-            std::vector<std::vector<std::uint32_t>> models;
+            std::vector<std::uint32_t> ids_all;  // delivered models, flat
+            std::vector<std::uint64_t> offs{0};
             std::vector<std::uint32_t> mcubes;
             std::vector<yas_trace> traces;
             EngineCallbacks cb;
             const std::uint32_t np = prog.atom_count();
             cb.on_model = [&](const EngineModel& m) {
-                std::size_t pop = 0;
-                for (std::uint32_t x : m.bits) pop += static_cast<std::size_t>(__builtin_popcount(x));
-                std::vector<std::uint32_t> ids;
-                ids.reserve(pop);  // one allocation per model
+                const std::size_t at = ids_all.size();
                 for (std::size_t w = 0; w < m.bits.size(); ++w)
                     for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
                         const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
-                        if (a <= np) ids.push_back(a);
+                        if (a <= np) ids_all.push_back(a);
                     }
                 if (cfg.verify) {
                     // record_model's checks (solver.cpp:221-229)
+                    const std::vector<std::uint32_t> ids(ids_all.begin() + static_cast<std::ptrdiff_t>(at), ids_all.end());
                     if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
                     if (tp_step(prog, ids) != ids)
                         throw VerifyError("computed model is not a fixpoint of the consequence operator");
                 }
-                models.push_back(std::move(ids));
+                offs.push_back(ids_all.size());
                 mcubes.push_back(m.cube);
                 return true;
             };
@@ -502,16 +504,17 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             if (er.status == dev::kErrValidate) throw std::logic_error("fixpoint invariant broken");
             if (cfg.trace)
                 for (const yas_trace& t : traces) cfg.trace(&t, cfg.trace_user);
-            res->models = std::move(models);
+            res->ids = std::move(ids_all);
+            res->off = std::move(offs);
             res->cubes = std::move(mcubes);
             fill_stats(res->stats, er.stats);
-            res->stats.models = res->models.size();
+            res->stats.models = res->count();
             res->stats.wall_ms = er.wall_ms;
             res->stats.device_ms = er.device_ms;
             res->stats.launches = er.launches;
             res->stats.cubes = portfolio ? 0 : n_cubes;
             res->stats.portfolio_variant = er.variant;
-            res->status = res->models.empty() ? 1 : 0;
+            res->status = res->count() == 0 ? 1 : 0;
             lap("result");
             break;
         }
@@ -521,27 +524,22 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
 }
 
 int yas_result_status(const yas_result* r) { return r ? r->status : 1; }
-uint64_t yas_result_model_count(const yas_result* r) { return r ? r->models.size() : 0; }
+uint64_t yas_result_model_count(const yas_result* r) { return r ? r->count() : 0; }
 const uint32_t* yas_result_model(const yas_result* r, uint64_t m, uint32_t* n) {
-    if (!r || m >= r->models.size()) {
+    if (!r || m >= r->count()) {
         if (n) *n = 0;
         return nullptr;
     }
-    if (n) *n = static_cast<uint32_t>(r->models[m].size());
-    return r->models[m].data();
+    if (n) *n = static_cast<uint32_t>(r->off[m + 1] - r->off[m]);
+    return r->ids.data() + r->off[m];
 }
 size_t yas_result_models_flat(const yas_result* r, uint32_t* ids, size_t cap, uint64_t* offsets, uint32_t* cubes) {
     if (!r) return 0;
-    size_t total = 0;
-    for (std::size_t m = 0; m < r->models.size(); ++m) {
-        if (offsets) offsets[m] = total;
-        if (cubes) cubes[m] = m < r->cubes.size() ? r->cubes[m] : 0;
-        for (const uint32_t a : r->models[m]) {
-            if (ids && total < cap) ids[total] = a;
-            ++total;
-        }
-    }
-    if (offsets) offsets[r->models.size()] = total;
+    const std::size_t total = r->ids.size(), n = r->count();
+    if (ids) std::memcpy(ids, r->ids.data(), std::min(cap, total) * sizeof(uint32_t));
+    if (offsets) std::memcpy(offsets, r->off.data(), (n + 1) * sizeof(uint64_t));
+    if (cubes)
+        for (std::size_t m = 0; m < n; ++m) cubes[m] = m < r->cubes.size() ? r->cubes[m] : 0;
     return total;
 }
 uint32_t yas_result_model_cube(const yas_result* r, uint64_t m) {

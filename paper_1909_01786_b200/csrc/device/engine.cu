@@ -2541,12 +2541,18 @@ struct Search {
     __device__ __forceinline__ bool handle_conflicts() {
         if (g.leader_warp()) analyze_and_learn();
         g.sync();
+#ifdef YAS_TINY_PROF
+        mark(14);  // profiling build: conflict analysis + learning
+#endif
         if (c->status != kRunning) return false;
         if (c->b[0] == 0) return false;
         const bool restart = c->b[1] != 0;
         const std::uint32_t target = c->b[2];
         backjump(target);
         if (restart) initial_propagation(false);
+#ifdef YAS_TINY_PROF
+        mark(15);  // profiling build: backjump (+ restart)
+#endif
         if (g.leader_warp()) {
             const std::uint32_t n_sel = c->b[3];
             const std::int32_t* added = sl.scratch();

@@ -185,6 +185,33 @@ def test_reset_clears_whole_deps_rows(engine):
     assert run(Y.Propagator(store, 2, engine), True) == fresh
 
 
+@pytest.mark.parametrize("engine", ENGINES)
+def test_batched_calls_match_flushed_calls(engine):
+    """Recorded calls launched as one batch (bulk inputs uploaded early, staging buffers growing
+    mid-batch) give the same fixpoint as the same calls launched one by one."""
+    import numpy as np
+    store, seeded, dec = Y.NogoodStore.planted(20_000, 200_000, 50)
+    sd = np.asarray(seeded, dtype=np.int32)
+    out = []
+    for flush_each in (True, False):
+        p = Y.Propagator(store, 16, engine)
+        for rep in range(2):
+            p.reset()
+            p.push_decision(dec)
+            p.assign_propagated(sd[:64], 2)  # small, then a bulk input larger than the staging so far
+            if flush_each:
+                p.flush()
+            p.assign_propagated(sd[64:], 2)
+            if flush_each:
+                p.flush()
+            p.seed(np.concatenate([[dec], sd]).astype(np.int32))
+            if flush_each:
+                p.flush()
+            o = p.propagate_and_check(2)
+            out.append((o.violated, o.propagations, o.passes, fnv(p.trail())))
+    assert out[0] == out[1] == out[2] == out[3]
+
+
 def test_grid_pass_trace_diagnostics():
     """The per-pass phase stamps of whole-grid propagation are readable and ordered."""
     store, seeded, dec = Y.NogoodStore.planted(20_000, 200_000, 50)

@@ -1711,7 +1711,10 @@ struct Search {
 
     // Frontiers this small run in block 0 alone: a block barrier costs ~0.1 us,
     // a grid barrier ~1.5 us, and one block covers them in one or two batches.
-    static constexpr std::uint32_t kSoloT = 0;  // measured: no gain on the L2-flushed benchmark (0.294 vs 0.300 ms)
+#ifndef YAS_SOLO_T
+#define YAS_SOLO_T 0
+#endif
+    static constexpr std::uint32_t kSoloT = YAS_SOLO_T;  // measured (L2 flushed): 0 -> 0.288 ms, 512 -> 0.297, 2048 -> 0.311
 
     __device__ __forceinline__ bool propagate_grid(std::uint32_t level) {
         frontier_offsets();

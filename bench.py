@@ -180,7 +180,7 @@ def main():
 
     import torch
     import paper_1909_01786_b200 as Y
-    from paper_1909_01786_b200 import instances as I
+    from workloads import instances as I
 
     torch.cuda.set_device(local)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2

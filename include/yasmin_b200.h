@@ -71,7 +71,9 @@ int yas_program_rule_aux(const yas_program* p, uint32_t rule, uint32_t out[4]);
 uint32_t yas_program_total_atoms(const yas_program* p); /* AuxMap::total_atoms */
 /* nogood_census vs compiled counts: census[3], counts[3] = rule, atom, constraint. */
 int yas_program_census(const yas_program* p, uint64_t census[3], uint64_t counts[3]);
-/* tp_step (program.hpp:96): interp sorted; out gets up to cap ids; returns count. */
+/* tp_step (program.hpp:96): interp sorted; out gets up to cap ids; returns count,
+ * or SIZE_MAX when an id is 0 or above atom_count (the reference throws
+ * std::out_of_range from vector::at there). */
 size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap);
 /* Cube split used by yas_solve when cfg.cube_atoms > 0. Choice atoms are
  * atoms a whose only rule is "a :- not b." with "b :- not a." present. The
@@ -83,7 +85,8 @@ size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t 
  * rank's cube count; host-only. */
 size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
                          int32_t* out, size_t cap, uint32_t* width);
-/* verify_model (solver.hpp:116): 1 when the sorted atom set is an answer set. */
+/* verify_model (solver.hpp:116): 1 when the sorted atom set is an answer set, 0
+ * when not, -YAS_ERR_ARG when an id is 0 or above atom_count. */
 int yas_verify_model(const yas_program* p, const uint32_t* atom_ids, size_t n);
 
 /* ---- solve / enumerate: solve(GroundProgram, SolverConfig) (solver.hpp:113) */
@@ -207,7 +210,15 @@ int yas_propagator_push_decision(yas_propagator* p, int32_t lit);              /
 int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level,
                           const uint64_t* deps, uint32_t n_deps, int overflow, int32_t antecedent);
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n); /* Frontier::seed / last.push_back */
-int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n); /* NogoodStore::add_learned */
+/* NogoodStore::add_learned (nogood_store.cpp:81-107): the literals are
+ * canonicalised like Nogood::make; returns the new id, or -1 for an empty or
+ * vacuous set, a literal 0 or an atom above the store's total_atoms (message
+ * in yas_propagator_last_error). */
+int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n);
+/* Message of the last failed propagator call (CUDA error, invalid argument, a
+ * seed beyond A + 1 frontier literals — the latter is detected on the device
+ * and reported by the next result-returning call). Returns the full length. */
+size_t yas_propagator_last_error(const yas_propagator* p, char* buf, size_t cap);
 /* Exact literal counts of checked nogoods in yas_outcome.checked_lits (roofline
  * accounting; costs an extra load per decided long nogood, off by default). */
 int yas_propagator_count_literals(yas_propagator* p, int on);

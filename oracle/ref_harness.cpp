@@ -358,7 +358,7 @@ int cmd_planted(unsigned atoms, std::size_t count, unsigned pct, std::uint64_t s
     const double b1 = now_ms();
     std::vector<double> times;
     PropagationOutcome out;
-    std::uint64_t digest = 0;
+    std::uint64_t digest = 0, rdigest = 0, ddigest = 0;
     std::size_t trail = 0;
     for (int r = 0; r < reps; ++r) {
         WorkerPool pool(1);
@@ -376,8 +376,19 @@ int cmd_planted(unsigned atoms, std::size_t count, unsigned pct, std::uint64_t s
         out = prop.propagate_and_check(a, f, 2);
         times.push_back(now_ms() - t0);
         digest = 0xcbf29ce484222325ull;
-        for (const auto& e : a.trail())
+        rdigest = ddigest = 0xcbf29ce484222325ull;
+        for (const auto& e : a.trail()) {
             digest = (digest ^ static_cast<std::uint32_t>(e.lit.code())) * 0x100000001b3ull;
+            // antecedents (-1 for decision / seeded-without-reason) and Deps word 0 + overflow, trail order
+            const AtomId x = e.lit.atom();
+            const Reason rs = a.reason(x);
+            const std::int32_t rv = rs.kind == Reason::propagated ? rs.antecedent : -1;
+            rdigest = (rdigest ^ static_cast<std::uint32_t>(rv)) * 0x100000001b3ull;
+            const std::uint64_t d0 = a.deps().of(x)[0];
+            ddigest = (ddigest ^ static_cast<std::uint32_t>(d0)) * 0x100000001b3ull;
+            ddigest = (ddigest ^ static_cast<std::uint32_t>(d0 >> 32)) * 0x100000001b3ull;
+            ddigest = (ddigest ^ (a.deps().overflow(x) ? 1u : 0u)) * 0x100000001b3ull;
+        }
         trail = a.trail().size();
     }
     std::cout << "{\"atoms\":" << atoms << ",\"nogoods\":" << nogoods.size() << ",\"pct\":" << pct
@@ -385,6 +396,7 @@ int cmd_planted(unsigned atoms, std::size_t count, unsigned pct, std::uint64_t s
               << ",\"violated\":" << out.violated << ",\"conflicts\":" << out.conflicts.size()
               << ",\"propagations\":" << out.propagations << ",\"passes\":" << out.passes
               << ",\"trail\":" << trail << ",\"trail_digest\":" << digest
+              << ",\"reason_digest\":" << rdigest << ",\"deps_digest\":" << ddigest
               << ",\"prop_ms\":" << jarr(times) << "}\n";
     return 0;
 }

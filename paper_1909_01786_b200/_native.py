@@ -30,6 +30,7 @@ EXPORTS = [
     "yas_propagator_add_learned", "yas_propagator_count_literals", "yas_propagator_atoms", "yas_propagator_cells", "yas_propagator_reasons",
     "yas_propagator_deps", "yas_propagator_trail", "yas_propagator_conflicts", "yas_propagator_frontier",
     "yas_propagator_level", "yas_propagator_profile", "yas_propagator_flush", "yas_propagator_pass_trace",
+    "yas_propagator_last_error",
 ]
 
 
@@ -152,6 +153,7 @@ def lib() -> C.CDLL:
         "yas_propagator_profile": (C.c_int, [P, C.POINTER(C.c_uint64)]),
         "yas_propagator_flush": (C.c_int, [P]),
         "yas_propagator_pass_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(U32)]),
+        "yas_propagator_last_error": (SZ, [P, C.c_char_p, SZ]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -368,6 +368,8 @@ def tp_step(prog: GroundProgram, interp: Sequence[int]) -> List[int]:
     cap = prog.atom_count() + 1
     out = (C.c_uint32 * cap)()
     n = N.lib().yas_program_tp_step(prog._h, arr, len(interp), out, cap)
+    if n == C.c_size_t(-1).value:
+        raise ValueError("tp_step: atom id 0 or above atom_count")
     return list(out[:n])
 
 
@@ -383,7 +385,10 @@ def cubes(prog: GroundProgram, k: int, depth: int = 1, rank: int = 0, world: int
 
 def verify_model(prog: GroundProgram, model: Model) -> bool:
     ids = (C.c_uint32 * max(1, len(model.atom_ids)))(*model.atom_ids)
-    return N.lib().yas_verify_model(prog._h, ids, len(model.atom_ids)) == 1
+    r = N.lib().yas_verify_model(prog._h, ids, len(model.atom_ids))
+    if r < 0:
+        raise ValueError("verify_model: atom id 0 or above atom_count")
+    return r == 1
 
 
 def _config(cfg: SolverConfig) -> N.yas_config:
@@ -602,46 +607,54 @@ class Propagator:
             N.lib().yas_propagator_free(h)
             self._h = C.c_void_p(0)
 
+    def _check(self, rc: int):
+        """Every yas_propagator_* status is checked: a CUDA or argument failure raises."""
+        if rc != 0:
+            _raise(rc, _text(N.lib().yas_propagator_last_error, self._h).encode())
+
     def _outcome(self, o: N.yas_outcome) -> PropagationOutcome:
         confl = self.conflicts() if o.n_conflicts else []
         return PropagationOutcome(bool(o.violated), confl, o.propagations, o.passes, o.checks, o.device_ms,
                                   o.checked_lits)
 
     def reset(self):
-        N.lib().yas_propagator_reset(self._h)
+        self._check(N.lib().yas_propagator_reset(self._h))
 
     def flush(self):
         """Launch the recorded state-changing calls now (they otherwise run with the next result-returning call)."""
-        N.lib().yas_propagator_flush(self._h)
+        self._check(N.lib().yas_propagator_flush(self._h))
 
     def initial_propagation(self) -> PropagationOutcome:
         o = N.yas_outcome()
-        N.lib().yas_propagator_initial(self._h, C.byref(o))
+        self._check(N.lib().yas_propagator_initial(self._h, C.byref(o)))
         return self._outcome(o)
 
     def propagate_and_check(self, level: int) -> PropagationOutcome:
         o = N.yas_outcome()
-        N.lib().yas_propagator_propagate(self._h, level, C.byref(o))
+        self._check(N.lib().yas_propagator_propagate(self._h, level, C.byref(o)))
         return self._outcome(o)
 
     def push_decision(self, lit: int):
-        N.lib().yas_propagator_push_decision(self._h, lit)
+        self._check(N.lib().yas_propagator_push_decision(self._h, lit))
 
     def assign_propagated(self, lits: Sequence[int], level: int, deps: Sequence[int] = (), overflow: bool = False,
                           antecedent: int = 0):
         d = (C.c_uint64 * max(1, len(deps)))(*deps)
-        N.lib().yas_propagator_assign(self._h, _ints(lits), len(lits), level, d, len(deps), 1 if overflow else 0,
-                                      antecedent)
+        self._check(N.lib().yas_propagator_assign(self._h, _ints(lits), len(lits), level, d, len(deps),
+                                                  1 if overflow else 0, antecedent))
 
     def seed(self, lits: Sequence[int]):
-        N.lib().yas_propagator_seed(self._h, _ints(lits), len(lits))
+        self._check(N.lib().yas_propagator_seed(self._h, _ints(lits), len(lits)))
 
     def add_learned(self, lits: Sequence[int]) -> int:
-        return N.lib().yas_propagator_add_learned(self._h, _ints(lits), len(lits))
+        i = N.lib().yas_propagator_add_learned(self._h, _ints(lits), len(lits))
+        if i < 0:
+            raise ValueError(_text(N.lib().yas_propagator_last_error, self._h))
+        return i
 
     def count_literals(self, on: bool = True):
         """Exact checked-literal accounting (roofline bytes); off by default."""
-        N.lib().yas_propagator_count_literals(self._h, 1 if on else 0)
+        self._check(N.lib().yas_propagator_count_literals(self._h, 1 if on else 0))
 
     def level(self) -> int:
         return N.lib().yas_propagator_level(self._h)
@@ -661,29 +674,33 @@ class Propagator:
     def profile(self) -> List[int]:
         """Diagnostics: SM cycles per propagation phase (see yas_propagator_profile)."""
         out = (C.c_uint64 * 16)()
-        N.lib().yas_propagator_profile(self._h, out)
+        self._check(N.lib().yas_propagator_profile(self._h, out))
         return list(out)
 
     def cells(self) -> List[int]:
         out = (C.c_int32 * (self.atoms + 1))()
-        N.lib().yas_propagator_cells(self._h, out)
+        self._check(N.lib().yas_propagator_cells(self._h, out))
         return list(out)
 
     def reasons(self) -> List[int]:
         out = (C.c_int32 * (self.atoms + 1))()
-        N.lib().yas_propagator_reasons(self._h, out)
+        self._check(N.lib().yas_propagator_reasons(self._h, out))
         return list(out)
 
     def deps(self, word: int = 0):
         out = (C.c_uint64 * (self.atoms + 1))()
         ovf = (C.c_uint8 * (self.atoms + 1))()
-        N.lib().yas_propagator_deps(self._h, word, out, ovf)
+        self._check(N.lib().yas_propagator_deps(self._h, word, out, ovf))
         return list(out), list(ovf)
 
     def _array(self, fn, out: Optional[np.ndarray] = None) -> np.ndarray:
         if out is None:
             out = np.empty(self.atoms + 1, dtype=np.int32)  # trail, frontier, conflicts: one pass, <= A entries
         n = fn(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), out.size)
+        if n == 0:
+            msg = _text(N.lib().yas_propagator_last_error, self._h)
+            if msg:
+                raise DeviceError(msg)
         if n > out.size:  # (cannot happen for trail/frontier; conflicts may exceed A)
             out = np.empty(n, dtype=np.int32)
             n = fn(self._h, out.ctypes.data_as(C.POINTER(C.c_int32)), out.size)

@@ -9,7 +9,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdio>
+#include <climits>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -56,6 +58,7 @@ struct yas_store {
 struct yas_propagator {
     std::unique_ptr<Session> s;
     std::uint32_t atoms = 0;
+    char err[512] = {0};  // message of the last failed call (yas_propagator_last_error)
 };
 
 namespace {
@@ -95,6 +98,7 @@ void require_device(int device) {
 
 template <class F>
 int guarded(char* err, std::size_t cap, F&& f) {
+    if (err && cap) err[0] = '\0';  // a message always describes the call that returned it
     try {
         return f();
     } catch (const ParseFailure& e) {
@@ -107,6 +111,12 @@ int guarded(char* err, std::size_t cap, F&& f) {
         put_err(err, cap, e.what());
         return YAS_ERR_VERIFY;
     } catch (const std::invalid_argument& e) {
+        put_err(err, cap, e.what());
+        return YAS_ERR_ARG;
+    } catch (const std::length_error& e) {  // store beyond the device layout's limits
+        put_err(err, cap, e.what());
+        return YAS_ERR_CAPACITY;
+    } catch (const std::out_of_range& e) {
         put_err(err, cap, e.what());
         return YAS_ERR_ARG;
     } catch (const std::logic_error& e) {
@@ -306,32 +316,47 @@ size_t yas_program_print(const yas_program* p, char* buf, size_t cap) { return p
 size_t yas_program_dump_nogoods(const yas_program* p, char* buf, size_t cap) {
     if (!p) return 0;
     auto* q = const_cast<yas_program*>(p);
-    return put_text(dump_nogoods(q->completion(), q->prog), buf, cap);
+    std::size_t n = 0;
+    guarded(nullptr, 0, [&] { n = put_text(dump_nogoods(q->completion(), q->prog), buf, cap); return 0; });
+    return n;
 }
 size_t yas_program_store_csv(const yas_program* p, char* buf, size_t cap) {
     if (!p) return 0;
-    return put_text(const_cast<yas_program*>(p)->static_store().dump_csv(), buf, cap);
+    std::size_t n = 0;
+    guarded(nullptr, 0, [&] { n = put_text(const_cast<yas_program*>(p)->static_store().dump_csv(), buf, cap); return 0; });
+    return n;
 }
 size_t yas_program_diagnostics(const yas_program* p, char* buf, size_t cap) {
     if (!p) return 0;
-    std::string s;
-    for (const std::string& d : diagnostics(p->prog)) s += d + "\n";
-    return put_text(s, buf, cap);
+    std::size_t n = 0;
+    guarded(nullptr, 0, [&] {
+        std::string s;
+        for (const std::string& d : diagnostics(p->prog)) s += d + "\n";
+        n = put_text(s, buf, cap);
+        return 0;
+    });
+    return n;
 }
 int yas_program_rule_aux(const yas_program* p, uint32_t rule, uint32_t out[4]) {
-    if (!p || rule >= p->prog.rules().size()) return YAS_ERR_ARG;
-    const RuleAux& a = const_cast<yas_program*>(p)->completion().aux[rule];
-    out[0] = a.b;
-    out[1] = a.t;
-    out[2] = a.n;
-    out[3] = a.vacuous ? 1 : 0;
-    return YAS_OK;
+    if (!p || !out || rule >= p->prog.rules().size()) return YAS_ERR_ARG;
+    return guarded(nullptr, 0, [&] {
+        const RuleAux& a = const_cast<yas_program*>(p)->completion().aux[rule];
+        out[0] = a.b;
+        out[1] = a.t;
+        out[2] = a.n;
+        out[3] = a.vacuous ? 1 : 0;
+        return static_cast<int>(YAS_OK);
+    });
 }
 uint32_t yas_program_total_atoms(const yas_program* p) {
-    return p ? const_cast<yas_program*>(p)->completion().total_atoms : 0;
+    if (!p) return 0;
+    std::uint32_t n = 0;
+    guarded(nullptr, 0, [&] { n = const_cast<yas_program*>(p)->completion().total_atoms; return 0; });
+    return n;
 }
 int yas_program_census(const yas_program* p, uint64_t census_out[3], uint64_t counts[3]) {
-    if (!p) return YAS_ERR_ARG;
+    if (!p || !census_out || !counts) return YAS_ERR_ARG;
+    return guarded(nullptr, 0, [&] {
     const Census c = census(p->prog);
     const Census& k = const_cast<yas_program*>(p)->completion().counts;
     census_out[0] = c.rule_nogoods;
@@ -340,29 +365,48 @@ int yas_program_census(const yas_program* p, uint64_t census_out[3], uint64_t co
     counts[0] = k.rule_nogoods;
     counts[1] = k.atom_nogoods;
     counts[2] = k.constraint_nogoods;
-    return YAS_OK;
+    return static_cast<int>(YAS_OK);
+    });
 }
 size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap) {
-    if (!p) return 0;
-    std::vector<AtomId> in(interp, interp + n);
-    const std::vector<AtomId> r = tp_step(p->prog, in);
-    for (std::size_t i = 0; i < r.size() && i < cap; ++i) out[i] = r[i];
-    return r.size();
+    if (!p || (n && !interp)) return SIZE_MAX;
+    for (size_t i = 0; i < n; ++i)
+        if (interp[i] == 0 || interp[i] > p->prog.atom_count()) return SIZE_MAX;  // tp_step indexes with at()
+    std::size_t total = SIZE_MAX;
+    guarded(nullptr, 0, [&] {
+        std::vector<AtomId> in(interp, interp + n);
+        const std::vector<AtomId> r = tp_step(p->prog, in);
+        for (std::size_t i = 0; i < r.size() && i < cap; ++i) out[i] = r[i];
+        total = r.size();
+        return 0;
+    });
+    return total;
 }
 size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
                          int32_t* out, size_t cap, uint32_t* width) {
     if (!p) return 0;
-    std::vector<std::int32_t> cubes;
-    std::uint32_t w = 0;
-    const std::uint32_t n = make_cubes(p->prog, k, depth, want ? want : 2368, rank, world, cubes, w);
-    if (width) *width = w;
-    for (std::size_t i = 0; i < cubes.size() && i < cap; ++i) out[i] = cubes[i];
+    std::size_t n = 0;
+    guarded(nullptr, 0, [&] {
+        std::vector<std::int32_t> cubes;
+        std::uint32_t w = 0;
+        n = make_cubes(p->prog, k, depth, want ? want : 2368, rank, world, cubes, w);
+        if (width) *width = w;
+        for (std::size_t i = 0; i < cubes.size() && out && i < cap; ++i) out[i] = cubes[i];
+        return 0;
+    });
     return n;
 }
 
 int yas_verify_model(const yas_program* p, const uint32_t* ids, size_t n) {
-    if (!p) return 0;
-    return is_answer_set(p->prog, std::vector<AtomId>(ids, ids + n)) ? 1 : 0;
+    if (!p || (n && !ids)) return -YAS_ERR_ARG;
+    for (size_t i = 0; i < n; ++i)
+        if (ids[i] == 0 || ids[i] > p->prog.atom_count()) return -YAS_ERR_ARG;
+    int ok = -YAS_ERR_ARG;
+    guarded(nullptr, 0, [&] {
+        ok = is_answer_set(p->prog, std::vector<AtomId>(ids, ids + n)) ? 1 : 0;
+        return 0;
+    });
+    return ok;
 }
 
 void yas_config_default(yas_config* c) {
@@ -453,7 +497,8 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         eo.slots = portfolio ? n_cubes : slots_per_gpu;
         const bool many = width > 0;
         const std::uint64_t cap = cfg.learned_capacity;
-        eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, many ? (1u << 13) : (1u << 18)));
+        const std::uint64_t cap1 = cap == UINT64_MAX ? cap : cap + 1;  // saturating: UINT64_MAX = unbounded
+        eo.lcap = static_cast<std::uint32_t>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(cap1, many ? (1u << 13) : (1u << 18))));
         eo.lpool = many ? (1u << 16) : (1u << 22);
         eo.slice_ms = 500.0;
 
@@ -491,7 +536,7 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             if (n_cubes > 0) er = engine_solve(ep, dc, eo, cubes, n_cubes, width, cb);
             lap("engine");
             if (er.status == dev::kErrArena && attempt < 8) {
-                eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>(cap + 1, 2ull * eo.lcap));
+                eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>({cap1, 2ull * eo.lcap, 0x7FFFFFFFull}));
                 eo.lpool *= 2;
                 if (many && eo.slots > 64) eo.slots /= 2;
                 continue;
@@ -709,43 +754,54 @@ static void outcome_from(yas_propagator* p, bool violated, yas_outcome* o) {
 }
 
 int yas_propagator_flush(yas_propagator* p) {
-    return guarded(nullptr, 0, [&] { p->s->flush(); return static_cast<int>(YAS_OK); });
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] { p->s->flush(); return static_cast<int>(YAS_OK); });
 }
 int yas_propagator_reset(yas_propagator* p) {
-    return guarded(nullptr, 0, [&] { p->s->reset(); return static_cast<int>(YAS_OK); });
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] { p->s->reset(); return static_cast<int>(YAS_OK); });
 }
 int yas_propagator_initial(yas_propagator* p, yas_outcome* o) {
-    return guarded(nullptr, 0, [&] {
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] {
         const bool v = p->s->initial_propagation();
         outcome_from(p, v, o);
         return static_cast<int>(YAS_OK);
     });
 }
 int yas_propagator_propagate(yas_propagator* p, uint32_t level, yas_outcome* o) {
-    return guarded(nullptr, 0, [&] {
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] {
         const bool v = p->s->propagate(level);
         outcome_from(p, v, o);
         return static_cast<int>(YAS_OK);
     });
 }
 int yas_propagator_push_decision(yas_propagator* p, int32_t lit) {
-    return guarded(nullptr, 0, [&] { p->s->push_decision(lit); return static_cast<int>(YAS_OK); });
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] { p->s->push_decision(lit); return static_cast<int>(YAS_OK); });
 }
 int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level, const uint64_t* deps,
                           uint32_t n_deps, int overflow, int32_t antecedent) {
-    return guarded(nullptr, 0, [&] {
+    if (!p || (n && !lits)) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] {
         p->s->assign(lits, n, level, antecedent, reinterpret_cast<const unsigned long long*>(deps), deps ? n_deps : 0,
                      overflow != 0);
         return static_cast<int>(YAS_OK);
     });
 }
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n) {
-    return guarded(nullptr, 0, [&] { p->s->seed(lits, n); return static_cast<int>(YAS_OK); });
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] { p->s->seed(lits, n); return static_cast<int>(YAS_OK); });
 }
 int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n) {
+    if (!p || (n && !lits)) return -1;
     int32_t id = -1;
-    guarded(nullptr, 0, [&] { id = p->s->add_learned(std::vector<std::int32_t>(lits, lits + n)); return 0; });
+    guarded(p->err, sizeof p->err, [&] { id = p->s->add_learned(std::vector<std::int32_t>(lits, lits + n)); return 0; });
     return id;
+}
+size_t yas_propagator_last_error(const yas_propagator* p, char* buf, size_t cap) {
+    return p ? put_text(p->err, buf, cap) : 0;
 }
 int yas_propagator_count_literals(yas_propagator* p, int on) {
     if (!p) return YAS_ERR_ARG;
@@ -755,7 +811,7 @@ int yas_propagator_count_literals(yas_propagator* p, int on) {
 uint32_t yas_propagator_atoms(const yas_propagator* p) { return p ? p->atoms : 0; }
 int yas_propagator_pass_trace(yas_propagator* p, int on, uint64_t* out, size_t cap, uint32_t* blocks) {
     if (!p) return YAS_ERR_ARG;
-    return guarded(nullptr, 0, [&] {
+    return guarded(p->err, sizeof p->err, [&] {
         if (on >= 0) p->s->set_pass_trace(on != 0);
         if (out) {
             std::uint32_t b = 0;
@@ -768,45 +824,72 @@ int yas_propagator_pass_trace(yas_propagator* p, int on, uint64_t* out, size_t c
 }
 int yas_propagator_profile(const yas_propagator* p, uint64_t out[16]) {
     if (!p || !out) return YAS_ERR_ARG;
-    return guarded(nullptr, 0, [&] {
+    return guarded(const_cast<yas_propagator*>(p)->err, sizeof p->err, [&] {
         const dev::Ctl& c = p->s->ctl();
         for (int k = 0; k < 16; ++k) out[k] = c.prof[k];
         return static_cast<int>(YAS_OK);
     });
 }
-uint32_t yas_propagator_level(const yas_propagator* p) { return p ? p->s->ctl().cdl : 0; }
+// Read-backs: a CUDA failure leaves the message in yas_propagator_last_error;
+// the size_t variants then return 0.
+}  // extern "C"
+namespace {
+yas_propagator* mut(const yas_propagator* p) { return const_cast<yas_propagator*>(p); }
+template <class F>
+size_t guarded_size(const yas_propagator* p, F&& f) {
+    size_t n = 0;
+    if (guarded(mut(p)->err, sizeof p->err, [&] { n = f(); return static_cast<int>(YAS_OK); }) != YAS_OK) return 0;
+    return n;
+}
+}  // namespace
+extern "C" {
+uint32_t yas_propagator_level(const yas_propagator* p) {
+    return p ? static_cast<uint32_t>(guarded_size(p, [&] { return static_cast<size_t>(p->s->ctl().cdl); })) : 0;
+}
 int yas_propagator_cells(const yas_propagator* p, int32_t* out) {
-    const auto v = p->s->cells();
-    std::copy(v.begin(), v.end(), out);
-    return YAS_OK;
+    if (!p || !out) return YAS_ERR_ARG;
+    return guarded(mut(p)->err, sizeof p->err, [&] {
+        const auto v = p->s->cells();
+        std::copy(v.begin(), v.end(), out);
+        return static_cast<int>(YAS_OK);
+    });
 }
 int yas_propagator_reasons(const yas_propagator* p, int32_t* out) {
-    const auto v = p->s->reasons();
-    std::copy(v.begin(), v.end(), out);
-    return YAS_OK;
+    if (!p || !out) return YAS_ERR_ARG;
+    return guarded(mut(p)->err, sizeof p->err, [&] {
+        const auto v = p->s->reasons();
+        std::copy(v.begin(), v.end(), out);
+        return static_cast<int>(YAS_OK);
+    });
 }
 int yas_propagator_deps(const yas_propagator* p, uint32_t word, uint64_t* out, uint8_t* overflow) {
-    if (word >= p->s->deps_words()) return YAS_ERR_ARG;
-    const auto v = p->s->deps_word(word);
-    std::copy(v.begin(), v.end(), out);
-    if (overflow) {
-        const auto o = p->s->deps_overflow();
-        std::copy(o.begin(), o.end(), overflow);
-    }
-    return YAS_OK;
+    if (!p || !out || word >= p->s->deps_words()) return YAS_ERR_ARG;
+    return guarded(mut(p)->err, sizeof p->err, [&] {
+        const auto v = p->s->deps_word(word);
+        std::copy(v.begin(), v.end(), out);
+        if (overflow) {
+            const auto o = p->s->deps_overflow();
+            std::copy(o.begin(), o.end(), overflow);
+        }
+        return static_cast<int>(YAS_OK);
+    });
 }
 size_t yas_propagator_trail(const yas_propagator* p, int32_t* out, size_t cap) {
-    return p->s->trail_into(out, cap);
+    return p ? guarded_size(p, [&] { return p->s->trail_into(out, cap); }) : 0;
 }
 size_t yas_propagator_conflicts(const yas_propagator* p, int32_t* out, size_t cap) {
-    const auto v = p->s->conflicts();
-    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-    return v.size();
+    return p ? guarded_size(p, [&] {
+        const auto v = p->s->conflicts();
+        for (size_t i = 0; i < v.size() && out && i < cap; ++i) out[i] = v[i];
+        return v.size();
+    }) : 0;
 }
 size_t yas_propagator_frontier(const yas_propagator* p, int32_t* out, size_t cap) {
-    const auto v = p->s->frontier();
-    for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
-    return v.size();
+    return p ? guarded_size(p, [&] {
+        const auto v = p->s->frontier();
+        for (size_t i = 0; i < v.size() && out && i < cap; ++i) out[i] = v[i];
+        return v.size();
+    }) : 0;
 }
 
 }  // extern "C"

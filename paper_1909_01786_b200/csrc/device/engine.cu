@@ -3194,12 +3194,20 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             g.sync();
             break;
         }
-        case kOpSeed:  // frontier.last.push_back for a bulk of literals
-            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr(c->cur)[c->F + k] = op.lits[k];
+        case kOpSeed: {  // frontier.last.push_back for a bulk of literals (at most A + 1 in total)
+            const std::uint32_t F = c->F;
+            if (static_cast<unsigned long long>(F) + op.n > S.A + 1ull) {
+                g.sync();
+                if (g.leader()) c->op_err = 1;
+                g.sync();
+                break;
+            }
+            for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) sl.fr(c->cur)[F + k] = op.lits[k];
             g.sync();
-            if (g.leader()) c->F += op.n;
+            if (g.leader()) c->F = F + op.n;
             g.sync();
             break;
+        }
         case kOpLearn:  // NogoodStore::add_learned (kNoTruth guard)
             if (g.leader_warp()) {
                 std::int32_t* buf = sl.scratch() + 128;

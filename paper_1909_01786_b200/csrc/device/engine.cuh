@@ -94,6 +94,9 @@ struct Ctl {
     std::uint32_t n_props, n_confl, n_pending, n_mbuf, n_trace;
     std::uint32_t learned_n, lpool_used, locc_used, lunits_n;
     std::uint32_t cube, epoch, stamp, pad0;
+    // Propagator API: an op rejected on the device (seed past the frontier
+    // capacity); the host raises it at the next result-returning call
+    std::uint32_t op_err, pad1;
     // Deps rows may hold words beyond their atom's level (Propagator API only:
     // Deps given to assign, propagation below the decision level); the next
     // reset then clears whole rows

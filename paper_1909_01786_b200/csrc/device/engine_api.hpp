@@ -98,6 +98,7 @@ public:
     struct Impl;
 
 private:
+    void check_op_error() const;  // raises (and clears) an op the device rejected
     std::unique_ptr<Impl> impl_;
     std::uint32_t W_;
     float last_ms_ = 0.f;

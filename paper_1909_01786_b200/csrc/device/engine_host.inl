@@ -1,6 +1,7 @@
 // Host side of the engine: uploads, per-slot arenas, the launch/drain loop.
 // Included at the end of engine.cu (needs the kernel templates).
 #include <chrono>
+#include <cstddef>
 #include <cstdlib>
 
 namespace yas {
@@ -596,7 +597,7 @@ void record_op(Session::Impl& im, const dev::OpArgs& op, const std::int32_t* lit
 }
 }  // namespace
 
-void Session::flush() { flush_ops(*impl_, nullptr); }
+void Session::flush() { flush_ops(*impl_, nullptr); }  // asynchronous: a rejected op raises at the next result
 
 void Session::reset() {
     dev::OpArgs op{};
@@ -609,7 +610,9 @@ bool Session::initial_propagation() {
     op.op = dev::kOpInitial;
     record_op(*impl_, op);
     flush_ops(*impl_, &last_ms_);
-    return ctl().b[10] != 0;
+    const bool v = ctl().b[10] != 0;
+    check_op_error();
+    return v;
 }
 
 bool Session::propagate(std::uint32_t level) {
@@ -618,7 +621,9 @@ bool Session::propagate(std::uint32_t level) {
     op.level = level;
     record_op(*impl_, op);
     flush_ops(*impl_, &last_ms_);
-    return ctl().b[10] != 0;
+    const bool v = ctl().b[10] != 0;
+    check_op_error();
+    return v;
 }
 
 void Session::push_decision(std::int32_t lit) {
@@ -644,19 +649,45 @@ void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_
 }
 
 void Session::seed(const std::int32_t* lits, std::size_t n) {
+    const std::uint32_t A = impl_->ar.A;
+    if (n > static_cast<std::size_t>(A) + 1) throw std::invalid_argument("seed: more literals than atoms");
+    for (std::size_t k = 0; k < n; ++k)
+        if (lits[k] == 0 || lit_atom(lits[k]) > A) throw std::invalid_argument("seed: literal out of range");
     dev::OpArgs op{};
     op.op = dev::kOpSeed;
     op.n = static_cast<std::uint32_t>(n);
     record_op(*impl_, op, lits, n);
 }
 
-std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits) {
+std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits_in) {
+    // NogoodStore::add_learned takes a canonical Nogood (nogood.hpp:80-87):
+    // atoms in [1, A], sorted, no repeats, never both signs of one atom
+    for (std::int32_t l : lits_in)
+        if (l == 0 || lit_atom(l) > impl_->ar.A) throw std::invalid_argument("add_learned: literal out of range");
+    auto ng = Nogood::make(lits_in, kLearned, kNoTruth);
+    if (!ng) throw std::invalid_argument("add_learned: vacuous nogood (both signs of one atom)");
+    if (ng->lits.empty()) throw std::invalid_argument("add_learned: empty nogood");
+    const std::vector<std::int32_t>& lits = ng->lits;
     dev::OpArgs op{};
     op.op = dev::kOpLearn;
     op.n = static_cast<std::uint32_t>(lits.size());
     record_op(*impl_, op, lits.data(), lits.size());
     flush_ops(*impl_, nullptr);
-    return static_cast<std::int32_t>(ctl().b[12]);
+    const std::int32_t id = static_cast<std::int32_t>(ctl().b[12]);
+    check_op_error();
+    return id;
+}
+
+void Session::check_op_error() const {
+    dev::Ctl& c = *impl_->h_ctl;
+    if (!c.op_err) return;
+    c.op_err = 0;  // cleared on both sides: the session stays usable
+    const std::uint32_t zero = 0;
+    ck(cudaMemcpyAsync(reinterpret_cast<char*>(impl_->ar.slots[0].ctl()) + offsetof(dev::Ctl, op_err), &zero,
+                       sizeof zero, cudaMemcpyHostToDevice, impl_->stream),
+       "clear op error");
+    ck(cudaStreamSynchronize(impl_->stream), "clear op error");
+    throw std::invalid_argument("seed: frontier capacity exceeded (more than A + 1 frontier literals)");
 }
 
 void Session::set_count_lits(bool on) { impl_->cfg.count_lits = on ? 1u : 0u; }

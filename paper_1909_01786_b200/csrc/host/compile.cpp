@@ -1,6 +1,7 @@
 #include "compile.hpp"
 
 #include <algorithm>
+#include <stdexcept>
 
 namespace yas {
 
@@ -171,6 +172,12 @@ StaticStore build_store(const std::vector<Nogood>& nogoods, AtomId total_atoms) 
         if (n.lits.size() == 1 && n.may_assert(-n.lits[0])) st.units.push_back(n.lits[0]);
         else rest.push_back(&n);
     }
+    // ids carry their length class in the top two bits of the device's
+    // occurrence entries, and offsets are 32-bit (compile.hpp)
+    std::size_t lits = 0;
+    for (const Nogood* n : rest) lits += n->lits.size();
+    if (rest.size() >= (std::size_t{1} << 30) || lits > 0xFFFFFFFFull)
+        throw std::length_error("store too large: at most 2^30 - 1 nogoods and 2^32 - 1 literals");
     std::stable_sort(rest.begin(), rest.end(),
                      [](const Nogood* a, const Nogood* b) { return a->lits.size() < b->lits.size(); });
     st.off.reserve(rest.size() + 1);

@@ -10,7 +10,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_1909_01786_b200 as Y  # noqa: E402
-from paper_1909_01786_b200 import instances as I  # noqa: E402
+from workloads import instances as I  # noqa: E402
 
 G = os.path.join(ROOT, "tests", "golden")
 STAT_KEYS = ["decisions", "propagations", "conflicts", "learned_count", "learned_length_sum", "restarts", "models",

@@ -2,7 +2,7 @@
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1909_01786_b200 as Y
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 12
 text = I.queens(n)
 for rep in range(3):

@@ -1,7 +1,7 @@
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1909_01786_b200 as Y
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 prog = Y.parse_program(I.queens(int(sys.argv[1]) if len(sys.argv) > 1 else 12))
 for spec in sys.argv[2:]:
     k, d = map(int, spec.split(":"))

@@ -3,7 +3,7 @@
 import sys, os, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1909_01786_b200 as Y
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 name = sys.argv[1]
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 engine = sys.argv[3] if len(sys.argv) > 3 else "auto"

@@ -18,7 +18,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 REF = os.path.join(ROOT, "oracle", "_ref", "aspine_ref")
 sys.path.insert(0, ROOT)
 
-from paper_1909_01786_b200 import instances as I  # noqa: E402
+from workloads import instances as I  # noqa: E402
 
 MODES = [("fwd", "occ"), ("res", "occ"), ("fwd", "jw"), ("res", "jw"), ("fwd", "act"), ("res", "act")]
 

@@ -3,7 +3,7 @@ single-search enumeration (trajectories differ by design)."""
 import pytest
 
 import paper_1909_01786_b200 as Y
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 
 from _util import golden
 

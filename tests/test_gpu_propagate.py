@@ -226,3 +226,43 @@ def test_grid_pass_trace_diagnostics():
     first = tr[0, 0]
     assert first[0] > 0 and all(first[k] <= first[k + 1] for k in range(0, 8))
     assert (int(first[9]) & 0xFFFFFFFF) == 1 + len(seeded)  # F of pass 0
+
+
+# ---- argument checking on the low-level API ------------------------
+@pytest.mark.parametrize("engine", ENGINES)
+def test_add_learned_canonicalises_and_rejects_bad_sets(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2]], 4), 1, engine)
+    # repeats are dropped and the order does not matter (Nogood::make)
+    assert p.add_learned([3, 4, 3]) == 1
+    assert p.add_learned([4, 3]) == 2  # an equal set is appended again (duplicate census only)
+    for bad in ([], [0], [5], [-9, 1], [2, -2]):
+        with pytest.raises(ValueError):
+            p.add_learned(bad)
+    p.push_decision(-4)
+    p.seed([-4])
+    o = p.propagate_and_check(2)  # the session stays usable after rejected calls
+    assert not o.violated
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_seed_out_of_range_and_over_capacity(engine):
+    p = Y.Propagator(Y.NogoodStore.build([[1, 2]], 2), 1, engine)
+    with pytest.raises(ValueError):
+        p.seed([3])
+    with pytest.raises(ValueError):
+        p.seed([0])
+    p.seed([1, 2, 1])          # A + 1 = 3 frontier literals: accepted
+    p.seed([2])                # the fourth exceeds the frontier capacity: reported by the next result
+    with pytest.raises(ValueError):
+        p.propagate_and_check(1)
+    p.reset()
+    p.push_decision(1)
+    p.seed([1])
+    o = p.propagate_and_check(2)
+    assert not o.violated and p.cells()[2] == -2
+
+
+def test_unbounded_learned_capacity_solves():
+    prog = Y.parse_program("a :- not b.\nb :- not a.\n:- a.\n")
+    r = Y.solve(prog, Y.SolverConfig(max_models=0, learned_capacity=2**64 - 1))
+    assert [m.atom_ids for m in r.models] == [[2]]

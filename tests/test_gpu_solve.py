@@ -4,7 +4,7 @@ verdicts, identical model sequences and identical trajectory counters
 import pytest
 
 import paper_1909_01786_b200 as Y
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 
 from _util import HEUR, config_from_opts, golden, stats_diff
 
@@ -116,7 +116,7 @@ def test_determinism_and_stats_text():
 def test_model_list_views_match_per_model_accessors():
     """SolveResult.models is a lazy sequence over yas_result_models_flat: length,
     indexing, slicing and names agree with the model-by-model C-ABI."""
-    from paper_1909_01786_b200 import instances as I
+    from workloads import instances as I
     prog = Y.parse_program(I.queens(6))
     r = Y.solve(prog, Y.SolverConfig(max_models=0))
     ms = r.models

@@ -5,7 +5,7 @@ import pytest
 
 import paper_1909_01786_b200 as Y
 from paper_1909_01786_b200 import aspine as A
-from paper_1909_01786_b200 import instances as I
+from workloads import instances as I
 
 from _util import golden
 
@@ -148,3 +148,16 @@ def test_ladder_cubes_partition_and_encoding():
     parts = [A.cubes(p, 6, 2, r, 3) for r in range(3)]
     assert sorted(tuple(c) for part in parts for c in part) == sorted(tuple(c) for c in two)
     assert len(A.cubes(p, 6, 0, want=300)) == 343
+
+
+# ---- invalid ids raise instead of aborting the host process --------
+def test_tp_step_and_verify_reject_out_of_range_ids():
+    p = Y.parse_program("a :- not b.\nb :- not a.\n")
+    with pytest.raises(ValueError):
+        Y.tp_step(p, [7])
+    with pytest.raises(ValueError):
+        Y.tp_step(p, [0])
+    with pytest.raises(ValueError):
+        Y.verify_model(p, Y.Model([1, 9], []))
+    assert Y.tp_step(p, []) == [1, 2]
+    assert Y.verify_model(p, Y.Model([1], ["a"]))

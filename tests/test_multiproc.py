@@ -26,7 +26,7 @@ def _worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import paper_1909_01786_b200 as Y
     from paper_1909_01786_b200 import aspine as A
-    from paper_1909_01786_b200 import instances as I
+    from workloads import instances as I
     p = Y.parse_program(I.queens(6))
     mine = A.cubes(p, 6, 2, rank, world)
     n = torch.tensor([len(mine)], dtype=torch.int64)

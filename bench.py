@@ -33,6 +33,41 @@ WORKLOAD = "planted store: 1M nogoods, 100k atoms, len U[2,6], 50% of H seeded a
 REF_BIN = os.path.join(ROOT, "oracle", "_ref", "aspine_ref")
 
 
+def pins():
+    """Reference outputs at full size (tests/golden/pins.json, make_golden.py pins)."""
+    with open(os.path.join(ROOT, "tests", "golden", "pins.json")) as f:
+        return json.load(f)
+
+
+def fnv(words, h=0xcbf29ce484222325):
+    for c in words:
+        h = ((h ^ (int(c) & 0xFFFFFFFF)) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def planted_parity(prop, o, exp):
+    """Untimed: the fixpoint equals the reference's (counts + trail / reason / Deps digests)."""
+    tr = prop.trail()
+    reasons = prop.reasons()
+    d0, ovf = prop.deps(0)
+    rs, ds = [], []
+    for lit in tr:
+        x = abs(lit)
+        rs.append(reasons[x] if reasons[x] >= 0 else -1)
+        ds += [d0[x] & 0xFFFFFFFF, d0[x] >> 32, 1 if ovf[x] else 0]
+    got = (o.propagations, o.passes, len(tr), fnv(tr), fnv(rs), fnv(ds))
+    want = (exp["propagations"], exp["passes"], exp["trail"], exp["trail_digest"], exp["reason_digest"],
+            exp["deps_digest"])
+    return got == want
+
+
+def model_set_digest(models):
+    words = []
+    for m in sorted(tuple(sorted(x)) for x in models):
+        words += list(m) + [0]
+    return fnv(words)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -252,6 +287,8 @@ def main():
         tr = prop.trail_array(trail_buf)  # D2H: the fixpoint trail, into pinned host memory
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     e2e_max = allreduce([statistics.mean(e2e_ms)], "max", world)[0]
+    exp1m = next(e for e in pins()["planted_1m"] if e["pct"] == PLANTED["pct"])
+    parity = {"planted_1m": planted_parity(prop, o, exp1m) and checks == 1_077_320 * args.steps}
     h2d = 4 * (1 + len(seeded)) + 4 * (1 + len(seeded)) + 8 * 16
     d2h = 4 * len(tr)
 
@@ -271,6 +308,7 @@ def main():
         "e2e": {"value": (all_checks / args.steps) / (e2e_max / 1e3), "unit": "checks/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_max},
         "clocks": clk.summary(), "gpu_launches": launches, "bracket_wall_s": wall,
+        "parity": parity,
     }
 
     log("cpu baseline")
@@ -298,12 +336,16 @@ def main():
         del prop
         log("planted 8M")
         line["planted_8m"] = planted_large(Y, torch, flush, local)
+        parity["planted_8m"] = line["planted_8m"].pop("parity")
         log("enumeration")
         line["enumeration"] = enumeration(Y, I, rank, world, local)
         line["enumeration_q8"] = enumeration(Y, I, rank, world, local, n=8)
+        parity["queens12"] = line["enumeration"].pop("parity")
+        parity["queens8"] = line["enumeration_q8"].pop("parity")
         if rank == 0:
             log("random program 4a")
             line["random_program_4a"] = random_program(Y, I, local)
+            parity["rand4a"] = line["random_program_4a"].pop("parity")
             log("first model")
             line["first_model"] = first_model(Y, I, local)
         log("done")
@@ -339,6 +381,7 @@ def planted_large(Y, torch, flush, local, steps=5):
     lits = run().checked_lits
     prop.count_literals(False)
     outs = [run() for _ in range(steps)]
+    parity = planted_parity(prop, outs[-1], pins()["planted_8m"][0])
     ms = statistics.mean(o.device_ms for o in outs)
     checks = outs[-1].checks
     peak, _ = peaks()
@@ -346,7 +389,7 @@ def planted_large(Y, torch, flush, local, steps=5):
     out = {"workload": "planted 8M nogoods / 800k atoms, 50% seeded (exceeds L2)", "checks_per_step": checks,
            "passes": outs[-1].passes, "ms_per_step": ms, "checks_per_s": checks / (ms / 1e3),
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak},
-           "l2": "flushed before every step"}
+           "l2": "flushed before every step", "parity": parity}
     if os.path.exists(REF_BIN):  # one reference call on the same store (bounded: ~1 s)
         r = subprocess.run([REF_BIN, "planted", str(cfg["atoms"]), str(cfg["nogoods"]), str(cfg["pct"]),
                             hex(cfg["seed"]), "1"], capture_output=True, text=True, check=True)
@@ -368,10 +411,23 @@ def random_program(Y, I, local):
     t = time.perf_counter()
     r = Y.solve(prog, Y.SolverConfig(device=local))
     solve_cached_ms = (time.perf_counter() - t) * 1e3  # the program keeps its compiled store
-    out = {"status": r.status.name, "device_ms": r.stats.device_ms, "passes": r.stats.passes,
-           "checks": r.stats.checks, "checks_per_s": r.stats.checks / (r.stats.device_ms / 1e3),
+    lits = Y.solve(prog, Y.SolverConfig(device=local, count_lits=True)).stats.checked_lits  # untimed
+    dev = [Y.solve(prog, Y.SolverConfig(device=local)).stats.device_ms for _ in range(3)]
+    dev_ms = statistics.mean(dev)
+    algo = 12 * r.stats.checks + 4 * lits
+    peak, _ = peaks()
+    exp = pins()["rand4a"]
+    keys = [k for k in exp["stats"] if k not in ("wall_ms", "watch_replacements")]
+    parity = (r.status.name.upper() == exp["status"] and all(getattr(r.stats, k) == exp["stats"][k] for k in keys)
+              and len(r.models) == 1 and model_set_digest([r.models[0].atom_ids]) == exp["model_digest"])
+    out = {"status": r.status.name, "device_ms": dev_ms, "passes": r.stats.passes,
+           "checks": r.stats.checks, "checks_per_s": r.stats.checks / (dev_ms / 1e3),
            "parse_ms": load_ms, "solve_wall_ms": solve_ms, "solve_wall_ms_compiled": solve_cached_ms,
-           "decisions": r.stats.decisions}
+           "decisions": r.stats.decisions, "parity": parity,
+           "roofline": {"bound": "hbm", "achieved": algo / (dev_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": algo / (dev_ms / 1e3) / 1e9 / peak, "algorithmic_bytes_per_launch": algo,
+                        "checked_lits": lits, "timed": "whole solve kernel (initial propagation + 54 passes + "
+                                                       "model), CUDA events, mean of 3, L2 warm"}}
     if os.path.exists(REF_BIN):
         p = subprocess.run([REF_BIN, "solve", "-", "-n", "1", "--no-models", "--reps", "2"], input=text,
                            capture_output=True, text=True, check=True)
@@ -384,9 +440,44 @@ def random_program(Y, I, local):
     return out
 
 
+def cpu_cube_split(Y, text, cubes):
+    """Config 5 CPU side: the same cube set, one reference solve per cube,
+    on every host core (one process each); wall time of the whole set and the model set."""
+    import tempfile
+    prog = Y.parse_program(text)
+    nproc = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as d:
+        lp, cf = os.path.join(d, "p.lp"), os.path.join(d, "cubes.txt")
+        with open(lp, "w") as f:
+            f.write(text)
+        with open(cf, "w") as f:
+            for c in cubes:
+                f.write(" ".join(prog.name(abs(l)) for l in c if l) + "\n")
+        t = time.perf_counter()
+        procs = [subprocess.Popen([REF_BIN, "cubes", lp, cf, str(k), str(nproc)], stdout=subprocess.PIPE, text=True)
+                 for k in range(nproc)]
+        outs = [json.loads(p.communicate()[0]) for p in procs]
+        wall = (time.perf_counter() - t) * 1e3
+    models = [m for o in outs for m in o["models"]]
+    return {"cores": nproc, "processes": nproc, "cubes": len(cubes), "wall_ms": wall,
+            "models": len(models), "model_set_digest": model_set_digest(models)}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def enumeration(Y, I, rank, world, local, n=12):
     """n-queens, all answer sets: ladder cubes over the choice atoms, partitioned
     over the ranks; model count all-reduced (SUM), time max over ranks."""
+    from paper_1909_01786_b200 import aspine as A
     text = I.queens(n)
     cfg = Y.SolverConfig(max_models=0, cube_atoms=n, rank=rank, world=world, device=local)
     Y.solve(Y.parse_program(text), cfg)  # warm-up (module load, allocations)
@@ -401,22 +492,35 @@ def enumeration(Y, I, rank, world, local, n=12):
            "expected_models": {8: 92, 10: 724, 12: 14200}.get(n),
            "wall_ms": wall_max, "device_ms": dev_max, "cubes": int(cubes), "n_gpus": world,
            "passes_rank0": r.stats.passes}
+    # parity: the model set against the reference's (rank 0's share when world > 1 is checked by the tests)
+    ids = [m.atom_ids for m in r.models]
+    if n == 12:
+        exp = pins()["queens12"]
+        out["parity"] = world > 1 or (len(ids) == exp["models"] and model_set_digest(ids) == exp["model_set_digest"])
+    else:
+        with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
+            exp8 = json.load(f)["queens8/fwd/occ"]["models"]
+        out["parity"] = world > 1 or sorted(ids) == sorted(exp8)
     if rank == 0 and os.path.exists(REF_BIN):
-        # bounded CPU sample: the reference's first 1000 models of the same enumeration
-        if n <= 8:  # the whole enumeration is a bounded sample
+        if n <= 8:  # the whole single-thread enumeration is a bounded sample
             p = subprocess.run([REF_BIN, "solve", "-", "-n", "0", "--no-models", "--reps", "3"], input=text,
                                capture_output=True, text=True, check=True)
             ref = json.loads(p.stdout)
             out["cpu_reference"] = {"sample": f"queens{n}, all models, workers=1, mean of 3",
-                                    "run_ms": statistics.mean(ref["run_ms"])}
-        else:  # bounded sample: the reference's first 1000 models of the same enumeration
-            p = subprocess.run([REF_BIN, "solve", "-", "-n", "1000", "--no-models"], input=text,
-                               capture_output=True, text=True, check=True)
-            ref = json.loads(p.stdout)
-            rate = ref["stats"]["models"] / (ref["run_ms"][0] / 1e3)
-            out["cpu_reference"] = {"sample": f"queens{n}, first 1000 models, workers=1", "models_per_s": rate,
-                                    "extrapolated_all_models_s": out["expected_models"] / rate,
-                                    "measured_all_models_s_survey": 168.0 if n == 12 else None}
+                                    "run_ms": statistics.mean(ref["run_ms"]), "cores": 1}
+        else:
+            # the same cube set on every host core (one reference process per core); the
+            # full single-thread run (~3 min) is measured once by scripts/cpu_q12_reference.py
+            cubes_all = A.cubes(prog, n, 0, want=4 * 148 * 8 * world)
+            cs = cpu_cube_split(Y, text, cubes_all)
+            cs["parity"] = cs["models"] == out["expected_models"] and (
+                n != 12 or cs["model_set_digest"] == pins()["queens12"]["model_set_digest"])
+            cs["cpu_model"] = cpu_model()
+            out["cpu_reference_cube_split"] = cs
+            full = os.path.join(ROOT, "profiles", "r02_q12_reference_full.json")
+            if n == 12 and os.path.exists(full):
+                with open(full) as f:
+                    out["cpu_reference_full"] = json.load(f)
         out["models_per_s"] = n_models / (wall_max / 1e3)
     return out
 

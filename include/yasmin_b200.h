@@ -127,6 +127,8 @@ typedef struct yas_config {
                             concurrent searches with diverse (mode, heuristic), variant (v0 + rank * portfolio
                             + k) % 6 with v0 = mode | heuristic << 1 first; the first search to finish reports
                             its model or UNSAT (0 or 1 = off) */
+    uint32_t count_lits; /* 1: exact literal counts of the checked nogoods in yas_stats.checked_lits
+                            (roofline accounting; one extra load per decided long nogood, off by default) */
 } yas_config;
 
 void yas_config_default(yas_config* cfg);

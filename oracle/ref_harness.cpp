@@ -14,6 +14,11 @@
 //                              as program text + brute-force oracle families
 //   aspine_ref propstores SEED COUNT ATOMS MAXLEN
 //        -> random stores (P/tests/support/gen.hpp:73-87) + reference Propagator fixpoint
+//   aspine_ref cubes FILE CUBES PART NPARTS
+//        -> enumerate all answer sets of FILE + cube c (for c % NPARTS == PART), one
+//           reference solve per cube; CUBES has one cube per line, each a list of atom
+//           names n standing for the integrity constraint ":- n." (the cube split of
+//           SURVEY.md 8(e), run on CPU processes for the config-5 baseline)
 //   aspine_ref planted ATOMS NOGOODS PCT SEED [REPS]
 //        -> the planted 1M-nogood store of SURVEY.md App. C, reference propagate_and_check
 #include <chrono>
@@ -401,6 +406,38 @@ int cmd_planted(unsigned atoms, std::size_t count, unsigned pct, std::uint64_t s
     return 0;
 }
 
+// Config 5 on CPU processes: the same cube set the device enumerates, one
+// reference solve (-n 0) of program + cube constraints per cube.
+int cmd_cubes(const std::string& file, const std::string& cube_file, unsigned part, unsigned nparts) {
+    std::ifstream in(file);
+    if (!in) throw std::runtime_error("cannot open " + file);
+    std::stringstream ss;
+    ss << in.rdbuf();
+    const std::string text = ss.str();
+    std::ifstream cf(cube_file);
+    if (!cf) throw std::runtime_error("cannot open " + cube_file);
+    SolverConfig cfg;
+    cfg.max_models = 0;
+    const double t0 = now_ms();
+    std::string line;
+    std::size_t index = 0, solved = 0;
+    std::ostringstream models;
+    std::size_t count = 0;
+    while (std::getline(cf, line)) {
+        if (index++ % nparts != part) continue;
+        std::string cube_text = text;
+        std::istringstream names(line);
+        for (std::string n; names >> n;) cube_text += "\n:- " + n + ".";
+        const GroundProgram prog = parse_program(std::string_view(cube_text));
+        const SolveResult r = solve(prog, cfg);
+        for (const Model& m : r.models) models << (count++ ? "," : "") << jarr(m.atom_ids);
+        ++solved;
+    }
+    std::cout << "{\"cubes\":" << solved << ",\"ms\":" << (now_ms() - t0) << ",\"models\":[" << models.str()
+              << "]}\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -414,6 +451,9 @@ int main(int argc, char** argv) {
             return cmd_propstores(std::stoull(argv[2], nullptr, 0), std::stoi(argv[3]),
                                   static_cast<unsigned>(std::stoul(argv[4])),
                                   static_cast<unsigned>(std::stoul(argv[5])));
+        if (cmd == "cubes" && argc >= 6)
+            return cmd_cubes(argv[2], argv[3], static_cast<unsigned>(std::stoul(argv[4])),
+                             static_cast<unsigned>(std::stoul(argv[5])));
         if (cmd == "planted" && argc >= 6)
             return cmd_planted(static_cast<unsigned>(std::stoul(argv[2])), std::stoull(argv[3]),
                                static_cast<unsigned>(std::stoul(argv[4])),

@@ -51,7 +51,7 @@ class yas_config(C.Structure):
         ("learned_capacity", C.c_uint64), ("trace", TRACE_FN), ("trace_user", C.c_void_p),
         ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("cube_depth", C.c_uint32),
         ("slots", C.c_uint32),
-        ("rank", C.c_int), ("world", C.c_int), ("portfolio", C.c_uint32),
+        ("rank", C.c_int), ("world", C.c_int), ("portfolio", C.c_uint32), ("count_lits", C.c_uint32),
     ]
 
 

@@ -136,6 +136,7 @@ class SolverConfig:
     rank: int = 0
     world: int = 1
     portfolio: int = 0  # first-model portfolio: concurrent searches with diverse (mode, heuristic)
+    count_lits: bool = False  # exact literals of checked nogoods in stats.checked_lits (roofline accounting)
 
 
 _STAT_FIELDS = ["decisions", "propagations", "conflicts", "learned_count", "learned_length_sum", "restarts",
@@ -416,6 +417,7 @@ def _config(cfg: SolverConfig) -> N.yas_config:
     c.rank = cfg.rank
     c.world = cfg.world
     c.portfolio = cfg.portfolio
+    c.count_lits = 1 if cfg.count_lits else 0
     return c
 
 

@@ -469,6 +469,7 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         dc.debug_validate = cfg.debug_validate ? 1u : 0u;
         dc.learned_capacity = cfg.learned_capacity;
         dc.trace = cfg.trace ? 1u : 0u;
+        dc.count_lits = cfg.count_lits ? 1u : 0u;
 
         std::vector<std::int32_t> cubes;
         std::uint32_t width = 0, n_cubes = 1;

@@ -50,3 +50,33 @@ def config_from_opts(opts, **kw):
 
 def stats_diff(stats, expected):
     return {k: (getattr(stats, k), expected[k]) for k in STAT_KEYS if getattr(stats, k) != expected[k]}
+
+
+def fnv(seq, h=0xcbf29ce484222325):
+    """FNV-1a over 32-bit words (oracle/ref_harness.cpp cmd_planted digests)."""
+    for c in seq:
+        h = ((h ^ (int(c) & 0xFFFFFFFF)) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def trail_digests(p):
+    """(trail, reason, Deps) digests of a Propagator's assignment in trail order,
+    as the reference harness prints them: the literal sequence; the antecedent of
+    each trail atom (-1 unless propagated); Deps word 0 (low, high) + overflow."""
+    tr = p.trail()
+    reasons = p.reasons()
+    d0, ovf = p.deps(0)
+    rs, ds = [], []
+    for lit in tr:
+        x = abs(lit)
+        rs.append(reasons[x] if reasons[x] >= 0 else -1)
+        ds += [d0[x] & 0xFFFFFFFF, d0[x] >> 32, 1 if ovf[x] else 0]
+    return len(tr), fnv(tr), fnv(rs), fnv(ds)
+
+
+def model_set_digest(models):
+    """Order-independent digest of a set of answer sets (tests/golden/make_golden.py)."""
+    words = []
+    for m in sorted(tuple(sorted(x)) for x in models):
+        words += list(m) + [0]
+    return fnv(words)

@@ -108,8 +108,35 @@ def planted():
     return [ref(["planted", "20000", "200000", str(p), "0x1b00b5"]) for p in (1, 10, 50, 90)]
 
 
+def model_set_digest(models):
+    """Order-independent digest of a set of answer sets: FNV-1a over the sorted
+    models, each a sorted atom-id list closed by a 0 (tests/_util.py mirrors it)."""
+    h = 0xcbf29ce484222325
+    for m in sorted(tuple(sorted(x)) for x in models):
+        for a in list(m) + [0]:
+            h = ((h ^ (a & 0xFFFFFFFF)) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+def pins():
+    """Parity pins for every configuration bench.py reports (VERDICT r1 "next" #1):
+    full-size planted fixpoints (1M at 1/10/50/90 %, 8M at 50 %) with trail, reason
+    and Deps digests; config 4a's first model and SolveStats; all 14,200 answer sets
+    of queens(12) as count + model-set digest (the reference needs minutes here)."""
+    out = {"planted_1m": [ref(["planted", "100000", "1000000", str(p), "0x1b00b5"]) for p in (1, 10, 50, 90)],
+           "planted_8m": [ref(["planted", "800000", "8000000", "50", "0x1b00b5"])]}
+    r = solve_text(I.random_program(), ["-n", "1"])
+    out["rand4a"] = {"status": r["status"], "stats": r["stats"], "model_len": len(r["models"][0]),
+                     "model_digest": model_set_digest(r["models"])}
+    for n in (12,):
+        r = solve_text(I.queens(n), ["-n", "0"])
+        out[f"queens{n}"] = {"status": r["status"], "models": len(r["models"]),
+                             "model_set_digest": model_set_digest(r["models"]), "stats": r["stats"]}
+    return out
+
+
 def main():
-    targets = sys.argv[1:] or ["corpus", "extras", "configs", "propstores", "planted", "dumps"]
+    targets = sys.argv[1:] or ["corpus", "extras", "configs", "propstores", "planted", "dumps", "pins"]
     for t in targets:
         data = globals()[t]()
         with open(os.path.join(HERE, f"{t}.json"), "w") as f:

@@ -4,7 +4,7 @@ import pytest
 
 import paper_1909_01786_b200 as Y
 
-from _util import golden
+from _util import golden, trail_digests
 
 pytestmark = pytest.mark.gpu
 ENGINES = ["block", "grid"]
@@ -107,7 +107,8 @@ def test_random_stores_match_reference(engine, key):
 @pytest.mark.parametrize("engine", ENGINES)
 def test_planted_fixpoint_matches_reference(engine):
     """200k-nogood planted stores (App. C recipe) at 1/10/50/90 % seeds: identical
-    propagation count, pass count and trail (FNV digest of the literal sequence)."""
+    propagation count, pass count, trail (FNV digest of the literal sequence) and the
+    reasons and Deps of the trail atoms (digests in trail order)."""
     for exp in golden("planted"):
         s, seeded, dec = Y.NogoodStore.planted(exp["atoms"], exp["nogoods"], exp["pct"])
         p = Y.Propagator(s, 16, engine)
@@ -119,6 +120,7 @@ def test_planted_fixpoint_matches_reference(engine):
         assert not o.violated
         assert (o.propagations, o.passes, len(tr)) == (exp["propagations"], exp["passes"], exp["trail"])
         assert fnv(tr) == exp["trail_digest"]
+        assert trail_digests(p) == (exp["trail"], exp["trail_digest"], exp["reason_digest"], exp["deps_digest"])
 
 
 def test_planted_1m_properties():

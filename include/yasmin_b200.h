@@ -98,6 +98,31 @@ typedef struct yas_trace {
 } yas_trace; /* ConflictTrace, solver.hpp:37-42 */
 typedef void (*yas_trace_fn)(const yas_trace* t, void* user);
 
+/* ---- fleets: one enumeration / portfolio over the GPUs of several processes --
+ * (no reference counterpart: the reference is single-process).
+ * Rank 0's GPU holds the shared cube queue and the portfolio claim; every other
+ * rank maps it through CUDA IPC (NVLink peer access) and takes cubes from it
+ * with system-scope atomics, so work is balanced across GPUs while it runs.
+ * The only collective of a solve is the final all-reduce of model counts,
+ * error and termination flags: NCCL (yas_fleet_create_nccl), or the caller's
+ * own transport (yas_fleet_create with two callbacks, e.g. torch.distributed).
+ * If a rank cannot map rank 0's block, cubes are dealt statically (c % world). */
+typedef struct yas_fleet yas_fleet;
+/* In place over all ranks; op 0 sum, 1 max, 2 min. Return 0 on success. */
+typedef int (*yas_allreduce_fn)(uint64_t* vals, size_t n, int op, void* user);
+/* In place: root's bytes to every rank. Return 0 on success. */
+typedef int (*yas_broadcast_fn)(void* buf, size_t bytes, int root, void* user);
+/* ncclGetUniqueId; rank 0 creates it and the caller hands the 128 bytes to every rank. */
+int yas_fleet_unique_id(uint8_t out[128], char* err, size_t err_cap);
+int yas_fleet_create_nccl(const uint8_t unique_id[128], int rank, int world, int device, yas_fleet** out, char* err,
+                          size_t err_cap);
+int yas_fleet_create(int rank, int world, int device, yas_allreduce_fn allreduce, yas_broadcast_fn broadcast,
+                     void* user, yas_fleet** out, char* err, size_t err_cap);
+void yas_fleet_free(yas_fleet* f);
+/* dynamic = 1 when every rank takes cubes from rank 0's shared queue. */
+int yas_fleet_info(const yas_fleet* f, int* rank, int* world, int* device, int* dynamic);
+int yas_fleet_allreduce(yas_fleet* f, uint64_t* vals, size_t n, int op, char* err, size_t err_cap);
+
 typedef struct yas_config {
     /* SolverConfig (solver.hpp:44-57) */
     int mode;              /* 0 fwd (default), 1 res */
@@ -129,6 +154,12 @@ typedef struct yas_config {
                             its model or UNSAT (0 or 1 = off) */
     uint32_t count_lits; /* 1: exact literal counts of the checked nogoods in yas_stats.checked_lits
                             (roofline accounting; one extra load per decided long nogood, off by default) */
+    uint32_t n_devices;  /* cube enumeration / portfolio over this many GPUs of this process (0 or 1: `device`
+                            only); cubes come from one queue in the first GPU's memory (NVLink peer access) */
+    const int* devices;  /* n_devices CUDA ordinals (NULL: device, device + 1, ...); an ordinal may repeat */
+    yas_fleet* fleet;    /* several processes share the enumeration / portfolio; overrides rank, world and
+                            device (one GPU per process). Every rank calls yas_solve with the same program
+                            and options; each returns the models its GPU found. */
 } yas_config;
 
 void yas_config_default(yas_config* cfg);
@@ -147,6 +178,11 @@ typedef struct yas_stats {
     uint64_t cubes;    /* cubes assigned to this rank */
     uint64_t checked_lits; /* literals of the checked nogoods (algorithmic traffic) */
     int64_t portfolio_variant; /* winning (mode | heuristic << 1) of a portfolio run, -1 otherwise */
+    uint64_t fleet_models;     /* models found by every GPU / rank of the solve (all-reduced) */
+    uint32_t devices;          /* GPUs of this process that ran */
+    uint32_t fleet_ranks;      /* processes of the fleet (1 without) */
+    int32_t fleet_winner;      /* portfolio: rank whose search finished first (-1: none / not a portfolio) */
+    uint32_t pad;
 } yas_stats;
 
 int yas_solve(const yas_program* p, const yas_config* cfg, yas_result** out, char* err, size_t err_cap);

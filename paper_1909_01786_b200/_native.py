@@ -40,6 +40,8 @@ class yas_trace(C.Structure):
 
 
 TRACE_FN = C.CFUNCTYPE(None, C.POINTER(yas_trace), C.c_void_p)
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.c_int, C.c_void_p)
+BROADCAST_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
 
 
 class yas_config(C.Structure):
@@ -52,6 +54,7 @@ class yas_config(C.Structure):
         ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("cube_depth", C.c_uint32),
         ("slots", C.c_uint32),
         ("rank", C.c_int), ("world", C.c_int), ("portfolio", C.c_uint32), ("count_lits", C.c_uint32),
+        ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int)), ("fleet", C.c_void_p),
     ]
 
 
@@ -62,7 +65,9 @@ class yas_stats(C.Structure):
         "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods", "res_learned", "fwd_learned",
         "fwd_fallbacks", "uip_check_failures", "fwd_decision_only_failures", "asserting_failures", "checks",
         "searches", "launches")] + [("device_ms", C.c_double), ("cubes", C.c_uint64), ("checked_lits", C.c_uint64),
-                                              ("portfolio_variant", C.c_int64)]
+                                              ("portfolio_variant", C.c_int64), ("fleet_models", C.c_uint64),
+                                              ("devices", C.c_uint32), ("fleet_ranks", C.c_uint32),
+                                              ("fleet_winner", C.c_int32), ("pad", C.c_uint32)]
 
 
 class yas_outcome(C.Structure):
@@ -154,6 +159,15 @@ def lib() -> C.CDLL:
         "yas_propagator_flush": (C.c_int, [P]),
         "yas_propagator_pass_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(U32)]),
         "yas_propagator_last_error": (SZ, [P, C.c_char_p, SZ]),
+        "yas_fleet_unique_id": (C.c_int, [C.POINTER(C.c_uint8), C.c_char_p, SZ]),
+        "yas_fleet_create_nccl": (C.c_int, [C.POINTER(C.c_uint8), C.c_int, C.c_int, C.c_int, C.POINTER(P),
+                                            C.c_char_p, SZ]),
+        "yas_fleet_create": (C.c_int, [C.c_int, C.c_int, C.c_int, ALLREDUCE_FN, BROADCAST_FN, P, C.POINTER(P),
+                                       C.c_char_p, SZ]),
+        "yas_fleet_free": (None, [P]),
+        "yas_fleet_info": (C.c_int, [P, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]),
+        "yas_fleet_allreduce": (C.c_int, [P, pU64, SZ, C.c_int, C.c_char_p, SZ]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

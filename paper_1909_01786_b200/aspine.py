@@ -137,13 +137,16 @@ class SolverConfig:
     world: int = 1
     portfolio: int = 0  # first-model portfolio: concurrent searches with diverse (mode, heuristic)
     count_lits: bool = False  # exact literals of checked nogoods in stats.checked_lits (roofline accounting)
+    devices: Optional[Sequence[int]] = None  # cube enumeration / portfolio over these GPUs of this process
+    fleet: Optional["Fleet"] = None  # several processes share the enumeration / portfolio (one GPU each)
 
 
 _STAT_FIELDS = ["decisions", "propagations", "conflicts", "learned_count", "learned_length_sum", "restarts",
                 "models", "wall_ms", "passes", "watch_replacements", "duplicate_learned", "blocking_nogoods",
                 "res_learned", "fwd_learned", "fwd_fallbacks", "uip_check_failures",
                 "fwd_decision_only_failures", "asserting_failures", "checks", "searches", "launches",
-                "device_ms", "cubes", "checked_lits", "portfolio_variant"]
+                "device_ms", "cubes", "checked_lits", "portfolio_variant", "fleet_models", "devices",
+                "fleet_ranks", "fleet_winner"]
 
 
 @dataclass
@@ -173,6 +176,10 @@ class SolveStats:
     cubes: int = 0
     checked_lits: int = 0
     portfolio_variant: int = -1
+    fleet_models: int = 0  # models of every GPU / rank of the solve (all-reduced)
+    devices: int = 1       # GPUs of this process that ran
+    fleet_ranks: int = 1   # processes of the fleet
+    fleet_winner: int = -1  # portfolio: rank whose search finished first
 
     def avg_learned_len(self) -> float:
         return 0.0 if self.learned_count == 0 else self.learned_length_sum / self.learned_count
@@ -418,6 +425,12 @@ def _config(cfg: SolverConfig) -> N.yas_config:
     c.world = cfg.world
     c.portfolio = cfg.portfolio
     c.count_lits = 1 if cfg.count_lits else 0
+    if cfg.devices:
+        c.n_devices = len(cfg.devices)
+        c._devs = (C.c_int * len(cfg.devices))(*cfg.devices)  # kept alive with the struct
+        c.devices = C.cast(c._devs, C.POINTER(C.c_int))
+    if cfg.fleet is not None:
+        c.fleet = cfg.fleet._h
     return c
 
 
@@ -459,6 +472,113 @@ def solve(prog: GroundProgram, cfg: Optional[SolverConfig] = None) -> SolveResul
     finally:
         L.yas_result_free(h)
     return SolveResult(models, stats, status, cubes)
+
+
+class Fleet:
+    """Processes (one GPU each) sharing one cube enumeration or first-model portfolio.
+
+    Rank 0's GPU holds the shared cube queue; the other ranks map it through CUDA
+    IPC and take cubes with system-scope atomics, and the final model counts and
+    flags are all-reduced. Transport: NCCL (``Fleet.nccl``) or any process group
+    given as two collectives (``Fleet.from_process_group`` for torch.distributed).
+    """
+
+    def __init__(self, handle, keep=()):
+        self._h = handle
+        self._keep = keep  # ctypes callbacks must outlive the fleet
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        err = C.create_string_buffer(512)
+        rc = N.lib().yas_fleet_unique_id(buf, err, 512)
+        if rc != 0:
+            _raise(rc, err.value)
+        return bytes(buf)
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, rank: int, world: int, device: int) -> "Fleet":
+        uid = (C.c_uint8 * 128)(*unique_id)
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = N.lib().yas_fleet_create_nccl(uid, rank, world, device, C.byref(h), err, 512)
+        if rc != 0:
+            _raise(rc, err.value)
+        return cls(h.value)
+
+    @classmethod
+    def from_collectives(cls, rank: int, world: int, device: int, allreduce, broadcast) -> "Fleet":
+        """allreduce(list[int], op) -> list[int] with op 'sum'|'max'|'min'; broadcast(bytes, root) -> bytes."""
+        ops = {0: "sum", 1: "max", 2: "min"}
+
+        def _ar(vals, n, op, _user):
+            try:
+                out = allreduce([vals[i] for i in range(n)], ops[op])
+                for i in range(n):
+                    vals[i] = int(out[i])
+                return 0
+            except Exception:  # reported as a failed collective by the C side
+                return 1
+
+        def _bc(buf, nbytes, root, _user):
+            try:
+                data = broadcast(C.string_at(buf, nbytes), root)
+                C.memmove(buf, data, nbytes)
+                return 0
+            except Exception:
+                return 1
+
+        ar, bc = N.ALLREDUCE_FN(_ar), N.BROADCAST_FN(_bc)
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        rc = N.lib().yas_fleet_create(rank, world, device, ar, bc, None, C.byref(h), err, 512)
+        if rc != 0:
+            _raise(rc, err.value)
+        return cls(h.value, (ar, bc))
+
+    @classmethod
+    def from_process_group(cls, device: int, group=None) -> "Fleet":
+        """A fleet over an initialised torch.distributed process group (gloo or nccl)."""
+        import torch
+        import torch.distributed as dist
+        dev = "cpu" if dist.get_backend(group) == "gloo" else f"cuda:{device}"
+        red = {"sum": dist.ReduceOp.SUM, "max": dist.ReduceOp.MAX, "min": dist.ReduceOp.MIN}
+
+        def allreduce(vals, op):
+            t = torch.tensor(vals, dtype=torch.int64, device=dev)  # counts and flags stay below 2^63
+            dist.all_reduce(t, op=red[op], group=group)
+            return [int(x) & 0xFFFFFFFFFFFFFFFF for x in t.tolist()]
+
+        def broadcast(data, root):
+            t = torch.tensor(list(data), dtype=torch.uint8, device=dev)
+            dist.broadcast(t, src=root, group=group)
+            return bytes(t.cpu().tolist())
+
+        return cls.from_collectives(dist.get_rank(group), dist.get_world_size(group), device, allreduce, broadcast)
+
+    def info(self):
+        r, w, d, dyn = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        N.lib().yas_fleet_info(self._h, C.byref(r), C.byref(w), C.byref(d), C.byref(dyn))
+        return {"rank": r.value, "world": w.value, "device": d.value, "dynamic": bool(dyn.value)}
+
+    def allreduce(self, vals, op: str = "sum"):
+        arr = (C.c_uint64 * len(vals))(*vals)
+        err = C.create_string_buffer(512)
+        rc = N.lib().yas_fleet_allreduce(self._h, arr, len(vals), {"sum": 0, "max": 1, "min": 2}[op], err, 512)
+        if rc != 0:
+            _raise(rc, err.value)
+        return list(arr)
+
+    def close(self):
+        if self._h:
+            N.lib().yas_fleet_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def stats_csv_header() -> str:

@@ -17,9 +17,11 @@
 #include <memory>
 #include <sstream>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "device/engine_api.hpp"
+#include "fleet.hpp"
 #include "host/compile.hpp"
 #include "host/program.hpp"
 
@@ -88,6 +90,10 @@ struct CapacityError : std::runtime_error {
 struct VerifyError : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+
+void ck_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
 
 void require_device(int device) {
     int n = 0;
@@ -424,6 +430,98 @@ void yas_config_default(yas_config* c) {
     c->world = 1;
 }
 
+namespace {
+
+// One engine run per GPU of this process, in parallel host threads; the
+// models each GPU delivers are kept per GPU (merged by the caller).
+struct DevRun {
+    int device = 0;
+    dev::Config dc{};
+    EngineOptions eo;
+    std::vector<std::int32_t> cubes;
+    std::uint32_t n_cubes = 0;
+    EngineResult er;
+    std::vector<std::uint32_t> ids;
+    std::vector<std::uint64_t> offs{0};
+    std::vector<std::uint32_t> mcubes;
+    std::vector<yas_trace> traces;
+    std::exception_ptr error;
+};
+
+void run_device(DevRun& d, const EngineProgram& ep, const Program& prog, const yas_config& cfg, std::uint32_t width) {
+    try {
+        d.ids.clear();
+        d.offs.assign(1, 0);
+        d.mcubes.clear();
+        d.traces.clear();
+        EngineCallbacks cb;
+        const std::uint32_t np = prog.atom_count();
+        cb.on_model = [&](const EngineModel& m) {
+            const std::size_t at = d.ids.size();
+            for (std::size_t w = 0; w < m.bits.size(); ++w)
+                for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
+                    const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
+                    if (a <= np) d.ids.push_back(a);
+                }
+            if (cfg.verify) {
+                // record_model's checks (solver.cpp:221-229)
+                const std::vector<std::uint32_t> ids(d.ids.begin() + static_cast<std::ptrdiff_t>(at), d.ids.end());
+                if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
+                if (tp_step(prog, ids) != ids) throw VerifyError("computed model is not a fixpoint of the consequence operator");
+            }
+            d.offs.push_back(d.ids.size());
+            d.mcubes.push_back(m.cube);
+            return true;
+        };
+        if (cfg.trace)
+            cb.on_trace = [&](std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj) {
+                d.traces.push_back({static_cast<int>(mode), conflict, len, bj});
+            };
+        d.er = EngineResult{};
+        if (d.n_cubes > 0) d.er = engine_solve(ep, d.dc, d.eo, d.cubes, d.n_cubes, width, cb);
+    } catch (...) {
+        d.error = std::current_exception();
+    }
+}
+
+// Shared queue / claim block for the GPUs of this process (no fleet): in the
+// first GPU's memory, mapped into the others over NVLink. Returns null when a
+// GPU cannot reach it (then the cubes are dealt statically).
+struct LocalFleet {
+    dev::Fleet* ctl = nullptr;
+    int home = 0;
+    ~LocalFleet() {
+        if (ctl) {
+            cudaSetDevice(home);
+            cudaFree(ctl);
+        }
+    }
+};
+
+bool local_fleet(LocalFleet& lf, const std::vector<int>& devs) {
+    lf.home = devs[0];
+    for (int d : devs) {
+        if (d == lf.home) continue;
+        int ok = 0;
+        if (cudaDeviceCanAccessPeer(&ok, d, lf.home) != cudaSuccess || !ok) return false;
+        ck_cuda(cudaSetDevice(d), "cudaSetDevice");
+        const cudaError_t e = cudaDeviceEnablePeerAccess(lf.home, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else ck_cuda(e, "cudaDeviceEnablePeerAccess");
+    }
+    ck_cuda(cudaSetDevice(lf.home), "cudaSetDevice");
+    ck_cuda(cudaMalloc(&lf.ctl, sizeof(dev::Fleet)), "cudaMalloc fleet");
+    return true;
+}
+
+void reset_fleet_ctl(dev::Fleet* ctl, int device) {
+    ck_cuda(cudaSetDevice(device), "cudaSetDevice");
+    const dev::Fleet init{0u, 0u, 0xffffffffu, 0u};
+    ck_cuda(cudaMemcpy(ctl, &init, sizeof init, cudaMemcpyHostToDevice), "fleet reset");
+}
+
+}  // namespace
+
 int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, char* err, size_t err_cap) {
     if (!p || !out) return YAS_ERR_ARG;
     *out = nullptr;
@@ -432,6 +530,13 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
     else yas_config_default(&cfg);
     return guarded(err, err_cap, [&] {
         if (cfg.deps_words < 1 || cfg.deps_words > 1024) throw std::invalid_argument("deps_words must be in [1, 1024]");
+        yas_fleet* fl = cfg.fleet;
+        if (fl) {
+            if (cfg.n_devices > 1) throw std::invalid_argument("a fleet runs one GPU per process (n_devices must be <= 1)");
+            cfg.rank = fl->rank;
+            cfg.world = fl->world;
+            cfg.device = fl->device;
+        }
         if (cfg.world < 1) cfg.world = 1;
         const auto tp0 = std::chrono::steady_clock::now();
         const bool prof = std::getenv("YAS_PROFILE") != nullptr;
@@ -440,7 +545,12 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                 std::fprintf(stderr, "[yas host] %s at %.2f ms\n", what,
                              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
         };
-        require_device(cfg.device);
+        std::vector<int> devs;
+        if (cfg.n_devices > 1)
+            for (std::uint32_t i = 0; i < cfg.n_devices; ++i) devs.push_back(cfg.devices ? cfg.devices[i] : cfg.device + static_cast<int>(i));
+        else
+            devs.push_back(cfg.device);
+        for (int d : devs) require_device(d);
         lap("device");
         auto* q = const_cast<yas_program*>(p);
         const Program& prog = q->prog;
@@ -471,100 +581,343 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         dc.trace = cfg.trace ? 1u : 0u;
         dc.count_lits = cfg.count_lits ? 1u : 0u;
 
-        std::vector<std::int32_t> cubes;
-        std::uint32_t width = 0, n_cubes = 1;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cfg.device);
         std::uint32_t per_sm = 8;  // concurrent searches per SM for cube enumeration
         if (const char* e = std::getenv("YAS_SEARCHES_PER_SM")) per_sm = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
         const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * per_sm;
+        const bool enumerate = cfg.cube_atoms > 0 && cfg.max_models == 0;
         const bool portfolio = cfg.portfolio > 1 && cfg.max_models == 1 && cfg.cube_atoms == 0;
-        if (cfg.cube_atoms > 0 && cfg.max_models == 0) {
-            n_cubes = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * static_cast<std::uint32_t>(cfg.world),
-                                 cfg.rank, cfg.world, cubes, width);
-        } else if (portfolio) {  // one search per variant, every rank
-            n_cubes = std::min<std::uint32_t>(cfg.portfolio, static_cast<std::uint32_t>(sms));
-            dc.portfolio = 1;
-            dc.pf_base = (dc.mode | dc.heur << 1) + static_cast<std::uint32_t>(cfg.rank) * cfg.portfolio;
-        } else if (cfg.rank != 0) {
-            n_cubes = 0;  // a single search runs on rank 0 only
+        if (!enumerate && !portfolio) devs.resize(1);  // one search: the first GPU
+        const std::uint32_t ndev = static_cast<std::uint32_t>(devs.size());
+        const std::uint32_t gpus = ndev * static_cast<std::uint32_t>(cfg.world);  // every GPU of the fleet
+
+        // the shared queue: this process's GPUs (peer mappings) or the fleet (IPC)
+        LocalFleet lf;
+        dev::Fleet* shared = nullptr;
+        int shared_dev = cfg.device;
+        if (fl) {
+            shared = fl->ctl;
+            shared_dev = fl->device;
+        } else if (ndev > 1 && local_fleet(lf, devs)) {
+            shared = lf.ctl;
+            shared_dev = lf.home;
+        }
+        const bool dynamic = fl ? fl->dynamic : shared != nullptr;
+
+        std::vector<DevRun> runs(ndev);
+        std::uint32_t width = 0;
+        if (enumerate) {
+            std::vector<std::int32_t> cubes;
+            // one shared queue: every GPU gets the whole cube list; otherwise cube c
+            // runs on GPU (rank * ndev + i) == c % gpus
+            const int qrank = dynamic ? 0 : cfg.rank * static_cast<int>(ndev);
+            const std::uint32_t total = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * gpus, 0, 1, cubes, width);
+            for (std::uint32_t i = 0; i < ndev; ++i) {
+                DevRun& d = runs[i];
+                if (dynamic) {
+                    d.cubes = cubes;
+                    d.n_cubes = total;
+                } else {
+                    const std::uint32_t g = static_cast<std::uint32_t>(qrank) + i;
+                    for (std::uint32_t c = g; c < total; c += gpus) {
+                        d.cubes.insert(d.cubes.end(), cubes.begin() + static_cast<std::ptrdiff_t>(c) * width,
+                                       cubes.begin() + static_cast<std::ptrdiff_t>(c + 1) * width);
+                        ++d.n_cubes;
+                    }
+                }
+            }
+            if (total == 1 && width == 0) {  // no choice atoms: one search, on the first GPU of rank 0
+                for (std::uint32_t i = 0; i < ndev; ++i) runs[i].n_cubes = (i == 0 && cfg.rank == 0) ? 1u : 0u;
+            }
+        } else if (portfolio) {  // one search per variant on every GPU
+            for (std::uint32_t i = 0; i < ndev; ++i) runs[i].n_cubes = std::min<std::uint32_t>(cfg.portfolio, static_cast<std::uint32_t>(sms));
+        } else {
+            runs[0].n_cubes = cfg.rank == 0 ? 1u : 0u;  // a single search runs on rank 0 only
         }
         lap("compiled + cubes");
 
-        EngineOptions eo;
-        eo.device = cfg.device;
-        const bool wide = !portfolio && (cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0));
-        eo.grid = wide;
-        eo.slots = portfolio ? n_cubes : slots_per_gpu;
         const bool many = width > 0;
         const std::uint64_t cap = cfg.learned_capacity;
         const std::uint64_t cap1 = cap == UINT64_MAX ? cap : cap + 1;  // saturating: UINT64_MAX = unbounded
-        eo.lcap = static_cast<std::uint32_t>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(cap1, many ? (1u << 13) : (1u << 18))));
-        eo.lpool = many ? (1u << 16) : (1u << 22);
-        eo.slice_ms = 500.0;
+        for (std::uint32_t i = 0; i < ndev; ++i) {
+            DevRun& d = runs[i];
+            const std::uint32_t gi = static_cast<std::uint32_t>(cfg.rank) * ndev + i;  // GPU index in the fleet
+            d.device = devs[i];
+            d.dc = dc;
+            if (portfolio) {
+                d.dc.portfolio = 1;
+                d.dc.pf_base = (dc.mode | dc.heur << 1) + gi * cfg.portfolio;
+            }
+            EngineOptions& eo = d.eo;
+            eo.device = devs[i];
+            eo.grid = !portfolio && (cfg.engine == 2 || (cfg.engine == 0 && st.size() >= (1u << 18) && width == 0));
+            eo.slots = portfolio ? d.n_cubes : slots_per_gpu;
+            eo.lcap = static_cast<std::uint32_t>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(cap1, many ? (1u << 13) : (1u << 18))));
+            eo.lpool = many ? (1u << 16) : (1u << 22);
+            eo.slice_ms = 500.0;
+            // the shared block is mapped on this GPU: the home GPU, a peer of it, or this rank's IPC view
+            eo.fleet = (shared && (dynamic || portfolio)) ? shared : nullptr;
+            eo.fleet_tag = gi << 16;
+        }
 
         auto res = std::make_unique<yas_result>();
+        std::uint64_t fleet_vals[4] = {0, 0, 0, 0};
         for (int attempt = 0;; ++attempt) {
-            std::vector<std::uint32_t> ids_all;  // delivered models, flat
-            std::vector<std::uint64_t> offs{0};
-            std::vector<std::uint32_t> mcubes;
-            std::vector<yas_trace> traces;
-            EngineCallbacks cb;
-            const std::uint32_t np = prog.atom_count();
-            cb.on_model = [&](const EngineModel& m) {
-                const std::size_t at = ids_all.size();
-                for (std::size_t w = 0; w < m.bits.size(); ++w)
-                    for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
-                        const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
-                        if (a <= np) ids_all.push_back(a);
-                    }
-                if (cfg.verify) {
-                    // record_model's checks (solver.cpp:221-229)
-                    const std::vector<std::uint32_t> ids(ids_all.begin() + static_cast<std::ptrdiff_t>(at), ids_all.end());
-                    if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
-                    if (tp_step(prog, ids) != ids)
-                        throw VerifyError("computed model is not a fixpoint of the consequence operator");
+            if (shared) {
+                if (!fl || fl->owner) reset_fleet_ctl(shared, shared_dev);
+                if (fl && fl->comm) {  // nobody starts before rank 0 has reset the queue
+                    std::uint64_t b = 0;
+                    fl->comm->allreduce(&b, 1, FleetComm::kMax);
                 }
-                offs.push_back(ids_all.size());
-                mcubes.push_back(m.cube);
-                return true;
-            };
-            if (cfg.trace)
-                cb.on_trace = [&](std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj) {
-                    traces.push_back({static_cast<int>(mode), conflict, len, bj});
-                };
-            EngineResult er;
-            if (n_cubes > 0) er = engine_solve(ep, dc, eo, cubes, n_cubes, width, cb);
+            }
+            if (ndev == 1) {
+                run_device(runs[0], ep, prog, cfg, width);
+            } else {
+                std::vector<std::thread> th;
+                for (DevRun& d : runs) th.emplace_back([&, dp = &d] { run_device(*dp, ep, prog, cfg, width); });
+                for (std::thread& t : th) t.join();
+            }
             lap("engine");
-            if (er.status == dev::kErrArena && attempt < 8) {
-                eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>({cap1, 2ull * eo.lcap, 0x7FFFFFFFull}));
-                eo.lpool *= 2;
-                if (many && eo.slots > 64) eo.slots /= 2;
+            std::uint32_t status = dev::kDone;
+            std::exception_ptr first_error;
+            for (DevRun& d : runs) {
+                if (d.error && !first_error) first_error = d.error;
+                if (d.er.status != dev::kDone && status == dev::kDone) status = d.er.status;
+            }
+            bool retry = status == dev::kErrArena && attempt < 8;
+            if (fl && fl->comm) {  // every rank retries, or none (the shared queue restarts from 0)
+                std::uint64_t v = retry ? 1 : 0;
+                fl->comm->allreduce(&v, 1, FleetComm::kMax);
+                retry = v != 0 && attempt < 8;
+            }
+            if (retry) {
+                for (DevRun& d : runs) {
+                    d.eo.lcap = static_cast<std::uint32_t>(std::min<std::uint64_t>({cap1, 2ull * d.eo.lcap, 0x7FFFFFFFull}));
+                    d.eo.lpool *= 2;
+                    if (many && d.eo.slots > 64) d.eo.slots /= 2;
+                    d.error = nullptr;
+                }
                 continue;
             }
-            if (er.status == dev::kErrArena) throw std::runtime_error("device learned-nogood arena exhausted");
-            if (er.status == dev::kErrCapacity)
+            // merge: GPUs in order; a portfolio reports the GPU whose search won the claim
+            std::vector<std::uint32_t> order;
+            int won = -1;
+            for (std::uint32_t i = 0; i < ndev; ++i)
+                if (runs[i].er.won) won = static_cast<int>(i);
+            if (portfolio) {
+                if (won >= 0) order.push_back(static_cast<std::uint32_t>(won));
+            } else {
+                for (std::uint32_t i = 0; i < ndev; ++i) order.push_back(i);
+            }
+            std::vector<yas_trace> traces;
+            for (std::uint32_t i : order) {
+                const DevRun& d = runs[i];
+                const std::uint64_t base = res->ids.size();
+                res->ids.insert(res->ids.end(), d.ids.begin(), d.ids.end());
+                for (std::size_t m = 1; m < d.offs.size(); ++m) res->off.push_back(base + d.offs[m]);
+                res->cubes.insert(res->cubes.end(), d.mcubes.begin(), d.mcubes.end());
+                traces.insert(traces.end(), d.traces.begin(), d.traces.end());
+            }
+            if (fl && fl->comm) {  // the final all-reduce: models, fleet-wide errors, the portfolio winner
+                std::uint64_t sum[1] = {res->count()};
+                fl->comm->allreduce(sum, 1, FleetComm::kSum);
+                std::uint64_t mx[3] = {status != dev::kDone || first_error ? 1u : 0u,
+                                       won >= 0 ? static_cast<std::uint64_t>(cfg.rank) + 1 : 0,
+                                       won >= 0 && res->count() > 0 ? 1u : 0u};
+                fl->comm->allreduce(mx, 3, FleetComm::kMax);
+                fleet_vals[0] = sum[0];
+                fleet_vals[1] = mx[0];
+                fleet_vals[2] = mx[1];
+                fleet_vals[3] = mx[2];
+            }
+            if (first_error) std::rethrow_exception(first_error);
+            if (status == dev::kErrArena) throw std::runtime_error("device learned-nogood arena exhausted");
+            if (status == dev::kErrCapacity)
                 throw CapacityError("learned nogood store capacity exceeded (" + std::to_string(cap) + " nogoods)");
-            if (er.status == dev::kErrLogic)
-                throw std::logic_error("res_learning: literal at conflict level has no antecedent");
-            if (er.status == dev::kErrValidate) throw std::logic_error("fixpoint invariant broken");
+            if (status == dev::kErrLogic) throw std::logic_error("res_learning: literal at conflict level has no antecedent");
+            if (status == dev::kErrValidate) throw std::logic_error("fixpoint invariant broken");
             if (cfg.trace)
                 for (const yas_trace& t : traces) cfg.trace(&t, cfg.trace_user);
-            res->ids = std::move(ids_all);
-            res->off = std::move(offs);
-            res->cubes = std::move(mcubes);
-            fill_stats(res->stats, er.stats);
+            dev::Stats tot{};
+            double dev_ms = 0.0, wall_ms = 0.0;
+            std::uint64_t launches = 0, searches = 0;
+            for (std::uint32_t i = 0; i < ndev; ++i) {
+                const EngineResult& er = runs[i].er;
+                const unsigned long long* pb = &er.stats.decisions;
+                unsigned long long* pa = &tot.decisions;
+                if (!portfolio)
+                    for (std::size_t k = 0; k < sizeof(dev::Stats) / 8; ++k) pa[k] += pb[k];
+                searches += er.stats.searches;
+                dev_ms = std::max(dev_ms, er.device_ms);
+                wall_ms = std::max(wall_ms, er.wall_ms);
+                launches += er.launches;
+            }
+            if (portfolio && won >= 0) tot = runs[static_cast<std::size_t>(won)].er.stats;  // the winner's trajectory
+            fill_stats(res->stats, tot);
+            res->stats.searches = searches;
             res->stats.models = res->count();
-            res->stats.wall_ms = er.wall_ms;
-            res->stats.device_ms = er.device_ms;
-            res->stats.launches = er.launches;
-            res->stats.cubes = portfolio ? 0 : n_cubes;
-            res->stats.portfolio_variant = er.variant;
-            res->status = res->count() == 0 ? 1 : 0;
+            res->stats.wall_ms = wall_ms;
+            res->stats.device_ms = dev_ms;
+            res->stats.launches = launches;
+            res->stats.cubes = portfolio ? 0 : searches;  // cubes this process searched
+            res->stats.portfolio_variant = won >= 0 ? runs[static_cast<std::size_t>(won)].er.variant : -1;
+            res->stats.devices = ndev;
+            res->stats.fleet_ranks = static_cast<std::uint32_t>(cfg.world);
+            if (fl && fl->comm) {
+                res->stats.fleet_models = fleet_vals[0];
+                res->stats.fleet_winner = portfolio ? static_cast<std::int32_t>(fleet_vals[2]) - 1 : -1;
+                res->status = portfolio ? (fleet_vals[3] ? 0 : 1) : (fleet_vals[0] ? 0 : 1);
+            } else {
+                res->stats.fleet_models = res->count();
+                res->stats.fleet_winner = portfolio && won >= 0 ? 0 : -1;
+                res->status = res->count() == 0 ? 1 : 0;
+            }
             lap("result");
             break;
         }
         *out = res.release();
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+namespace {
+
+// Collectives through caller-supplied functions (e.g. torch.distributed or MPI).
+class CallbackComm final : public FleetComm {
+public:
+    CallbackComm(yas_allreduce_fn ar, yas_broadcast_fn bc, void* user) : ar_(ar), bc_(bc), user_(user) {}
+    void allreduce(std::uint64_t* vals, std::size_t n, Op op) override {
+        if (ar_(vals, n, static_cast<int>(op), user_) != 0) throw std::runtime_error("fleet all-reduce callback failed");
+    }
+    void broadcast(void* buf, std::size_t bytes, int root) override {
+        if (bc_(buf, bytes, root, user_) != 0) throw std::runtime_error("fleet broadcast callback failed");
+    }
+
+private:
+    yas_allreduce_fn ar_;
+    yas_broadcast_fn bc_;
+    void* user_;
+};
+
+// Rank 0 allocates the shared block; its CUDA IPC handle goes to every rank,
+// which maps it (NVLink peer access across processes). If any rank cannot,
+// every rank keeps a private block and the cubes are dealt statically.
+void fleet_attach(yas_fleet& f) {
+    ck_cuda(cudaSetDevice(f.device), "cudaSetDevice");
+    cudaIpcMemHandle_t h{};
+    if (f.rank == 0) {
+        ck_cuda(cudaMalloc(&f.ctl, sizeof(dev::Fleet)), "cudaMalloc fleet");
+        f.owner = true;
+        if (f.world > 1) ck_cuda(cudaIpcGetMemHandle(&h, f.ctl), "cudaIpcGetMemHandle");
+    }
+    if (f.world == 1) {
+        f.dynamic = true;
+        return;
+    }
+    f.comm->broadcast(&h, sizeof h, 0);
+    std::uint64_t ok = 1;
+    if (f.rank != 0) {
+        void* ptr = nullptr;
+        if (cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+            f.ctl = static_cast<dev::Fleet*>(ptr);
+            f.ipc = true;
+        } else {
+            cudaGetLastError();
+            ok = 0;
+        }
+    }
+    f.comm->allreduce(&ok, 1, FleetComm::kMin);
+    f.dynamic = ok == 1;
+    if (!f.dynamic && f.rank != 0) {  // private block: portfolio stop within this rank only
+        if (f.ipc) cudaIpcCloseMemHandle(f.ctl);
+        f.ipc = false;
+        ck_cuda(cudaMalloc(&f.ctl, sizeof(dev::Fleet)), "cudaMalloc fleet");
+        f.owner = true;
+    }
+}
+
+int fleet_make(int rank, int world, int device, std::unique_ptr<FleetComm> (*make)(void*), void* arg, yas_fleet** out,
+               char* err, size_t cap) {
+    if (!out) return YAS_ERR_ARG;
+    *out = nullptr;
+    return guarded(err, cap, [&] {
+        if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("fleet: rank must be in [0, world)");
+        require_device(device);
+        auto f = std::make_unique<yas_fleet>();
+        f->rank = rank;
+        f->world = world;
+        f->device = device;
+        f->comm = make(arg);
+        fleet_attach(*f);
+        *out = f.release();
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+}  // namespace
+
+int yas_fleet_unique_id(uint8_t out[128], char* err, size_t err_cap) {
+    if (!out) return YAS_ERR_ARG;
+    return guarded(err, err_cap, [&] {
+        require_device(0);
+        nccl_unique_id(out);
+        return static_cast<int>(YAS_OK);
+    });
+}
+
+int yas_fleet_create_nccl(const uint8_t unique_id[128], int rank, int world, int device, yas_fleet** out, char* err,
+                          size_t err_cap) {
+    if (!unique_id) return YAS_ERR_ARG;
+    struct A {
+        const uint8_t* id;
+        int rank, world, device;
+    } a{unique_id, rank, world, device};
+    return fleet_make(rank, world, device,
+                      [](void* p) {
+                          const A& x = *static_cast<const A*>(p);
+                          return nccl_comm(x.id, x.rank, x.world, x.device);
+                      },
+                      &a, out, err, err_cap);
+}
+
+int yas_fleet_create(int rank, int world, int device, yas_allreduce_fn allreduce, yas_broadcast_fn broadcast, void* user,
+                     yas_fleet** out, char* err, size_t err_cap) {
+    if (!allreduce || !broadcast) return YAS_ERR_ARG;
+    struct A {
+        yas_allreduce_fn ar;
+        yas_broadcast_fn bc;
+        void* user;
+    } a{allreduce, broadcast, user};
+    return fleet_make(rank, world, device,
+                      [](void* p) -> std::unique_ptr<FleetComm> {
+                          const A& x = *static_cast<const A*>(p);
+                          return std::make_unique<CallbackComm>(x.ar, x.bc, x.user);
+                      },
+                      &a, out, err, err_cap);
+}
+
+void yas_fleet_free(yas_fleet* f) {
+    if (!f) return;
+    cudaSetDevice(f->device);
+    if (f->ipc) cudaIpcCloseMemHandle(f->ctl);
+    else if (f->owner && f->ctl) cudaFree(f->ctl);
+    delete f;
+}
+
+int yas_fleet_info(const yas_fleet* f, int* rank, int* world, int* device, int* dynamic) {
+    if (!f) return YAS_ERR_ARG;
+    if (rank) *rank = f->rank;
+    if (world) *world = f->world;
+    if (device) *device = f->device;
+    if (dynamic) *dynamic = f->dynamic ? 1 : 0;
+    return YAS_OK;
+}
+
+int yas_fleet_allreduce(yas_fleet* f, uint64_t* vals, size_t n, int op, char* err, size_t err_cap) {
+    if (!f || (n && !vals) || op < 0 || op > 2) return YAS_ERR_ARG;
+    return guarded(err, err_cap, [&] {
+        f->comm->allreduce(vals, n, static_cast<FleetComm::Op>(op));
         return static_cast<int>(YAS_OK);
     });
 }

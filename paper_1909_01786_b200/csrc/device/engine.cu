@@ -2918,6 +2918,12 @@ struct Search {
             if (ph != kLoop) return;
             // yield check at the loop top (clean state)
             if (g.leader()) {
+                // a portfolio search another GPU / process has beaten ends here
+                if constexpr (!G::kGrid)
+                    if (C.portfolio && C.fleet && *reinterpret_cast<volatile std::uint32_t*>(&C.fleet->stop)) {
+                        c->status = kDone;
+                        c->phase = kFinished;
+                    }
                 bool y = sh->stop != 0;
                 if (c->n_mbuf >= K.mcap || (C.trace && c->n_trace + 64 > K.tcap)) {
                     y = true;
@@ -2928,6 +2934,8 @@ struct Search {
             }
             g.sync();
             mark(11);
+            if constexpr (!G::kGrid)
+                if (c->status != kRunning) return;
             if (c->b[15]) {
                 if (g.leader()) c->status = kYield;
                 g.sync();
@@ -3003,7 +3011,12 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
         if (!G::kGrid && C.portfolio && g.c->phase == kFinished) {  // first to finish: stop the others
             if (g.leader()) {
                 g.c->done_ns = gtimer();
+                const std::uint32_t tag = C.fleet_tag + blockIdx.x;
+                const std::uint32_t prev = C.fleet ? atomicCAS_system(&C.fleet->winner, 0xffffffffu, tag)
+                                                   : atomicCAS(&sh->winner, 0xffffffffu, tag);
+                g.c->won = prev == 0xffffffffu ? 1u : 0u;
                 sh->stop = 1;
+                if (C.fleet) atomicExch_system(&C.fleet->stop, 1u);
                 g.c->status = kDone;
             }
             g.sync();
@@ -3013,7 +3026,9 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
             g.sync();
             if (g.leader()) {
                 g.c->phase = kIdle;
-                g.c->b[9] = sh->stop ? 0xffffffffu : atomicAdd(&sh->cube_next, 1u);
+                g.c->b[9] = sh->stop ? 0xffffffffu
+                            : C.fleet ? atomicAdd_system(&C.fleet->cube_next, 1u)
+                                      : atomicAdd(&sh->cube_next, 1u);
             }
             g.sync();
             const std::uint32_t cube = g.c->b[9];

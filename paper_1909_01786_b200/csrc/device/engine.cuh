@@ -33,6 +33,17 @@ enum Status : std::uint32_t {
 
 enum Phase : std::uint32_t { kIdle = 0, kInit = 1, kLoop = 2, kAfterModel = 3, kFinished = 4 };
 
+// Coordination shared by every GPU (and process) of one enumeration or
+// portfolio: the cube queue, the portfolio stop flag and the first finisher's
+// claim. It lives in the home GPU's memory; the other GPUs reach it through
+// NVLink peer mappings (CUDA IPC across processes) with system-scope atomics.
+struct Fleet {
+    std::uint32_t cube_next;  // next cube of the shared queue
+    std::uint32_t stop;       // portfolio: a search finished, every other search ends
+    std::uint32_t winner;     // portfolio: tag of the first finisher (~0 = none yet)
+    std::uint32_t pad;
+};
+
 struct Config {
     std::uint32_t mode;  // 0 fwd, 1 res
     std::uint32_t heur;  // 0 occ, 1 jw, 2 act
@@ -56,6 +67,8 @@ struct Config {
     // (mode, heuristic) = (v & 1, v >> 1); the first to finish stops the others
     std::uint32_t portfolio, pf_base;
     std::uint32_t warp_pass_t;  // single-CTA searches: passes with at most this many entries run in one warp
+    Fleet* fleet;               // cube queue / portfolio claim shared across GPUs (null: this GPU's Shared)
+    std::uint32_t fleet_tag;    // this GPU's portfolio claim tag base (slot index added)
 };
 
 // Read-only static store + program rules (host-built, uploaded once).
@@ -96,7 +109,8 @@ struct Ctl {
     std::uint32_t cube, epoch, stamp, pad0;
     // Propagator API: an op rejected on the device (seed past the frontier
     // capacity); the host raises it at the next result-returning call
-    std::uint32_t op_err, pad1;
+    std::uint32_t op_err;
+    std::uint32_t won;  // portfolio: this search claimed the first finish
     // Deps rows may hold words beyond their atom's level (Propagator API only:
     // Deps given to assign, propagation below the decision level); the next
     // reset then clears whole rows
@@ -190,7 +204,8 @@ struct Shared {  // global (all-slot) coordination
     std::uint32_t stop;
     std::uint32_t bar_count, bar_gen;
     unsigned long long t_start;
-    std::uint32_t partial_pad[27];
+    std::uint32_t winner;  // portfolio on one GPU without a fleet: first finisher's tag (~0 = none)
+    std::uint32_t partial_pad[26];
     // grid barrier: block b publishes the epoch of the barrier it reached
     std::uint32_t arrive[1024];
 };

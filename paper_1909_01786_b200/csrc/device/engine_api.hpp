@@ -31,6 +31,8 @@ struct EngineOptions {
     std::uint32_t mcap = 4096;       // models buffered per slot between drains
     std::uint32_t tcap = 8192;       // trace records per slot between drains
     double slice_ms = 200.0;         // kernel time slice before a yield
+    dev::Fleet* fleet = nullptr;     // shared cube queue / portfolio claim (device pointer valid on `device`)
+    std::uint32_t fleet_tag = 0;     // portfolio claim tag base of this GPU
 };
 
 struct EngineModel {
@@ -45,6 +47,7 @@ struct EngineResult {
     double device_ms = 0.0;  // sum of kernel time (CUDA events)
     double wall_ms = 0.0;    // host wall time of the launch loop
     std::int32_t variant = -1;  // portfolio: (mode | heuristic << 1) of the search that finished first
+    bool won = false;           // portfolio: a search of this run claimed the first finish
 };
 
 struct EngineCallbacks {

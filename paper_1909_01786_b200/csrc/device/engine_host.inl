@@ -199,6 +199,7 @@ struct Arena {
         for (std::uint32_t s = 0; s < n_slots; ++s) slots[s] = dev::Slot{L.base + static_cast<unsigned long long>(s) * o, &L};
         sh = dalloc<dev::Shared>(1, owned);
         ck(cudaMemset(sh, 0, sizeof(dev::Shared)), "memset");
+        ck(cudaMemset(&sh->winner, 0xff, sizeof(std::uint32_t)), "memset");
         const std::uint32_t gb = grid_blocks ? grid_blocks : 1;
         partial = dalloc<unsigned long long>(4 * gb, owned);
         pd = dalloc<double>(gb, owned);
@@ -258,6 +259,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     cfg.phase_prof = std::getenv("YAS_PROFILE") ? 1u : 0u;
     cfg.cube_width = cube_width;
     cfg.slice_ns = static_cast<std::uint64_t>(opt.slice_ms * 1e6);
+    cfg.fleet = opt.fleet;
+    cfg.fleet_tag = opt.fleet_tag;
 
     cudaEvent_t e0, e1;
     ck(cudaEventCreate(&e0), "event");
@@ -348,11 +351,12 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                             cudaMemcpyDeviceToHost),
                "models");
         }
-        // portfolio: only the search that finished first reports (its model, or UNSAT)
+        // portfolio: only the search that claimed the first finish reports (its
+        // model, or UNSAT); with a fleet it may be on another GPU / process
         winner = ~0u;
         if (cfg.portfolio)
             for (std::uint32_t s = 0; s < n_slots; ++s)
-                if (ctl[s].status == dev::kDone && (winner == ~0u || ctl[s].done_ns < ctl[winner].done_ns)) winner = s;
+                if (ctl[s].status == dev::kDone && ctl[s].won) winner = s;
         lap("models copied");
         for (std::uint32_t s = 0; s < n_slots; ++s) {
             dev::Ctl& c = ctl[s];
@@ -400,6 +404,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         tot = ctl[winner].st;
         tot.searches = searches;
         res.variant = ctl[winner].variant;
+        res.won = true;
     }
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {

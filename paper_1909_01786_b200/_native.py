@@ -31,6 +31,8 @@ EXPORTS = [
     "yas_propagator_deps", "yas_propagator_trail", "yas_propagator_conflicts", "yas_propagator_frontier",
     "yas_propagator_level", "yas_propagator_profile", "yas_propagator_flush", "yas_propagator_pass_trace",
     "yas_propagator_last_error",
+    "yas_fleet_unique_id", "yas_fleet_create_nccl", "yas_fleet_create", "yas_fleet_free", "yas_fleet_info",
+    "yas_fleet_allreduce",
 ]
 
 

@@ -488,7 +488,17 @@ class Fleet:
         self._keep = keep  # ctypes callbacks must outlive the fleet
 
     @staticmethod
+    def _share_nccl():
+        # libnccl.so.2 is opened once per process: load torch's copy first when torch
+        # is installed, so both use the same (newer) NCCL
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
+
+    @staticmethod
     def unique_id() -> bytes:
+        Fleet._share_nccl()
         buf = (C.c_uint8 * 128)()
         err = C.create_string_buffer(512)
         rc = N.lib().yas_fleet_unique_id(buf, err, 512)
@@ -498,6 +508,7 @@ class Fleet:
 
     @classmethod
     def nccl(cls, unique_id: bytes, rank: int, world: int, device: int) -> "Fleet":
+        cls._share_nccl()
         uid = (C.c_uint8 * 128)(*unique_id)
         h = C.c_void_p()
         err = C.create_string_buffer(512)

@@ -35,8 +35,11 @@ struct NcclApi {
 private:
     static NcclApi load() {
         NcclApi a;
-        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
-        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        // an NCCL the process already holds (e.g. torch's) is reused: a second
+        // copy under the same soname would shadow the newer one for later loads
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_LOCAL);
         if (!h) return a;
         auto sym = [&](auto& fn, const char* name) { fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(dlsym(h, name)); };
         sym(a.get_unique_id, "ncclGetUniqueId");

@@ -474,33 +474,62 @@ def cpu_model():
     return None
 
 
+_FLEET = None
+
+
+def fleet(Y, rank, world, local):
+    """The product's multi-GPU path: one fleet of all ranks (rank 0's GPU holds the
+    shared cube queue, NCCL for the final all-reduce; gloo process group on a
+    shared-GPU check)."""
+    global _FLEET
+    if world == 1:
+        return None
+    if _FLEET is None:
+        import torch.distributed as dist
+        if dist.get_backend() == "gloo":
+            _FLEET = Y.Fleet.from_process_group(local)
+        else:
+            uid = [Y.Fleet.unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            _FLEET = Y.Fleet.nccl(uid[0], rank, world, local)
+    return _FLEET
+
+
 def enumeration(Y, I, rank, world, local, n=12):
-    """n-queens, all answer sets: ladder cubes over the choice atoms, partitioned
-    over the ranks; model count all-reduced (SUM), time max over ranks."""
+    """n-queens, all answer sets: ladder cubes over the choice atoms from one queue
+    shared by every GPU (SolverConfig.fleet); the model count comes from the
+    product's own all-reduce, time is the max over ranks."""
     from paper_1909_01786_b200 import aspine as A
     text = I.queens(n)
-    cfg = Y.SolverConfig(max_models=0, cube_atoms=n, rank=rank, world=world, device=local)
+    fl = fleet(Y, rank, world, local)
+    cfg = Y.SolverConfig(max_models=0, cube_atoms=n, device=local, fleet=fl)
     Y.solve(Y.parse_program(text), cfg)  # warm-up (module load, allocations)
     barrier(world)
     t = time.perf_counter()
     prog = Y.parse_program(text)
     r = Y.solve(prog, cfg)
     wall = (time.perf_counter() - t) * 1e3
-    n_models, cubes = allreduce([float(len(r.models)), float(r.stats.cubes)], "sum", world)
+    n_models = r.stats.fleet_models
+    cubes = allreduce([float(r.stats.cubes)], "sum", world)[0]
     wall_max, dev_max = allreduce([wall, r.stats.device_ms], "max", world)
     out = {"instance": f"queens{n} (all answer sets)", "models": int(n_models),
            "expected_models": {8: 92, 10: 724, 12: 14200}.get(n),
            "wall_ms": wall_max, "device_ms": dev_max, "cubes": int(cubes), "n_gpus": world,
-           "passes_rank0": r.stats.passes}
-    # parity: the model set against the reference's (rank 0's share when world > 1 is checked by the tests)
-    ids = [m.atom_ids for m in r.models]
+           "passes_rank0": r.stats.passes, "cube_queue": "shared (fleet)" if fl is not None else "one GPU"}
+    # parity: the union of every rank's models against the reference's model set
+    ids = [list(m.atom_ids) for m in r.models]
+    if world > 1:
+        import torch.distributed as dist
+        parts = [None] * world
+        dist.all_gather_object(parts, ids)
+        ids = [m for part in parts for m in part]
     if n == 12:
         exp = pins()["queens12"]
-        out["parity"] = world > 1 or (len(ids) == exp["models"] and model_set_digest(ids) == exp["model_set_digest"])
+        out["parity"] = len(ids) == exp["models"] and model_set_digest(ids) == exp["model_set_digest"]
     else:
         with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
             exp8 = json.load(f)["queens8/fwd/occ"]["models"]
-        out["parity"] = world > 1 or sorted(ids) == sorted(exp8)
+        out["parity"] = sorted(ids) == sorted(exp8)
     if rank == 0 and os.path.exists(REF_BIN):
         if n <= 8:  # the whole single-thread enumeration is a bounded sample
             p = subprocess.run([REF_BIN, "solve", "-", "-n", "0", "--no-models", "--reps", "3"], input=text,

@@ -76,12 +76,14 @@ int yas_program_census(const yas_program* p, uint64_t census[3], uint64_t counts
  * std::out_of_range from vector::at there). */
 size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t n, uint32_t* out, size_t cap);
 /* Cube split used by yas_solve when cfg.cube_atoms > 0. Choice atoms are
- * atoms a whose only rule is "a :- not b." with "b :- not a." present. The
+ * atoms a whose only rule is "a :- not b." with "b :- not a." present,
+ * followed by every other atom that heads a rule (T a is then the passive unit
+ * nogood {F a}, -a below). The
  * first depth*k of them form `depth` nested ladders of width k: per level a
  * cube fixes (F a_0..F a_{i-1}, T a_i) or all F, so the (k+1)^depth cubes
  * partition the answer sets. depth 0 = smallest depth with >= want cubes.
  * Cube c runs on rank c % world. Each cube is width = depth*k unit-nogood
- * literals (0 = none): +a (":- a.") or +b (":- b.", i.e. T a). Returns this
+ * literals (0 = none): +a (":- a."), +b (":- b.", i.e. T a) or -a (":- not a."). Returns this
  * rank's cube count; host-only. */
 size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
                          int32_t* out, size_t cap, uint32_t* width);

@@ -145,6 +145,12 @@ int guarded(char* err, std::size_t cap, F&& f) {
 //   T a  <=>  F b   and the constraint ":- not a." is equivalent to ":- b.",
 // so both cube polarities can be stated as *forcing* unit nogoods: F a as
 // {T a}, T a as {T b}. Partners are skipped (b is determined by a).
+//
+// Any other atom a that heads a rule can split too: ":- a." is the unit nogood
+// {T a} (asserts F a), ":- not a." the unit nogood {F a}; the latter may not
+// assert T a (truth guard kNoTruth, nogood.hpp:62-73) and stays a passive
+// check that fails when a becomes false. Such atoms (b = 0) follow the choice
+// pairs, in atom order, so programs without even loops shard as well.
 struct Choice {
     AtomId a, b;
 };
@@ -166,6 +172,8 @@ std::vector<Choice> choice_atoms(const Program& prog) {
         out.push_back({a, b});
         taken[a] = taken[b] = 1;
     }
+    for (AtomId a = 1; a <= prog.atom_count(); ++a)
+        if (!taken[a] && !prog.rules_of(a).empty()) out.push_back({a, 0});
     return out;
 }
 
@@ -200,8 +208,9 @@ std::uint32_t make_cubes(const Program& prog, std::uint32_t L, std::uint32_t dep
         for (std::uint32_t p = 0; p <= L; ++p)
             for (std::uint32_t i = 0; i < L && i <= p; ++i) {
                 const Choice& c = ch[j * L + i];
-                // F a: nogood {T a}; T a: nogood {T b}
-                pat[(static_cast<std::size_t>(j) * (L + 1) + p) * L + i] = static_cast<std::int32_t>(i < p ? c.a : c.b);
+                // F a: nogood {T a}; T a: nogood {T b} (choice pair) or {F a}
+                const std::int32_t t = c.b ? static_cast<std::int32_t>(c.b) : -static_cast<std::int32_t>(c.a);
+                pat[(static_cast<std::size_t>(j) * (L + 1) + p) * L + i] = i < p ? static_cast<std::int32_t>(c.a) : t;
             }
     const std::uint64_t mine = total / static_cast<std::uint64_t>(world) +
                                (static_cast<std::uint64_t>(rank) < total % static_cast<std::uint64_t>(world) ? 1 : 0);

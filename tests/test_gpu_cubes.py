@@ -41,3 +41,17 @@ def test_queens10_count():
     assert len(r.models) == 724 and len({tuple(m.atom_ids) for m in r.models}) == 724
     for m in r.models[:50]:
         assert Y.verify_model(Y.parse_program(I.queens(10)), m)
+
+
+def test_corpus_generic_cubes_match_families():
+    """Every corpus program split over rule heads as well as choice pairs (the
+    passive ":- not a." cubes included): the union of the cubes' answer sets is
+    the brute-force family (acceptance_main.cpp:85-123)."""
+    bad = []
+    for prog in golden("corpus"):
+        p = Y.parse_program(prog["text"])
+        r = Y.solve(p, Y.SolverConfig(max_models=0, cube_atoms=2, cube_depth=3))
+        got = sorted(m.atom_ids for m in r.models)
+        if got != sorted(prog["family"]) or len({tuple(m) for m in got}) != len(got):
+            bad.append(prog["name"])
+    assert not bad, bad[:10]

@@ -150,6 +150,18 @@ def test_ladder_cubes_partition_and_encoding():
     assert len(A.cubes(p, 6, 0, want=300)) == 343
 
 
+def test_cubes_without_choice_pairs_use_rule_heads():
+    """Programs without even-loop pairs still shard: atoms that head a rule split as
+    ":- a." (+a, asserts F a) and ":- not a." (-a, a passive unit nogood {F a})."""
+    p = Y.parse_program("p :- q.\nq :- not r.\nr :- s.\n")
+    assert [p.name(a) for a in (1, 2, 3, 4)] == ["p", "q", "r", "s"]
+    assert A.cubes(p, 2, 1) == [[-1, 0], [1, -2], [1, 2]]
+    assert len(A.cubes(p, 1, 0, want=8)) == 8  # p, q, r: three levels of width 1
+    # pairs come first, then the remaining rule heads
+    q = Y.parse_program("a :- not b.\nb :- not a.\nc :- a.\n")
+    assert A.cubes(q, 2, 1) == [[2, 0], [1, -3], [1, 3]]
+
+
 # ---- invalid ids raise instead of aborting the host process (ADVICE r1) --------
 def test_tp_step_and_verify_reject_out_of_range_ids():
     p = Y.parse_program("a :- not b.\nb :- not a.\n")

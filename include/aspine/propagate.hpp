@@ -1,0 +1,4 @@
+// Reference include path /root/reference/proj/include/aspine/propagate.hpp: the
+// yasmin-b200 C++ facade provides it (include/yasmin/aspine.hpp).
+#pragma once
+#include "../yasmin/aspine.hpp"

@@ -52,6 +52,13 @@ int yas_device_name(int device, char* buf, size_t cap);
 int yas_program_parse(const char* text, size_t len, yas_program** out, int* err_line, char* err, size_t err_cap);
 int yas_program_parse_file(const char* path, yas_program** out, int* err_line, char* err, size_t err_cap);
 void yas_program_free(yas_program* p);
+/* Programmatic construction (GroundProgram(), intern, add_rule; program.hpp:51-62):
+ * an empty program, then atoms and rules in the caller's order. add_rule sorts and
+ * dedups the bodies; head 0 is a constraint; ids must be interned already. */
+yas_program* yas_program_create(void);
+uint32_t yas_program_intern(yas_program* p, const char* name); /* 0 on failure */
+int yas_program_add_rule(yas_program* p, uint32_t head, const uint32_t* pos, size_t n_pos, const uint32_t* neg,
+                         size_t n_neg);
 uint32_t yas_program_atom_count(const yas_program* p);       /* GroundProgram::atom_count */
 uint32_t yas_program_rule_count(const yas_program* p);       /* rules().size() */
 uint32_t yas_program_constraint_count(const yas_program* p); /* constraints().size() */
@@ -214,6 +221,10 @@ void yas_store_free(yas_store* s);
 uint32_t yas_store_size(const yas_store* s);
 uint32_t yas_store_total_atoms(const yas_store* s);
 size_t yas_store_dump_csv(const yas_store* s, char* buf, size_t cap);
+/* CSR nogood `id` (NogoodStore::literals / truth_guard / origin): copies at most cap
+ * literal codes, returns the length (0 for an id out of range); origin 0
+ * completion, 1 constraint, 2 learned. */
+size_t yas_store_nogood(const yas_store* s, uint32_t id, int32_t* lits, size_t cap, uint32_t* guard, uint8_t* origin);
 /* static_units (literals), unit_ids, static_class_bounds */
 size_t yas_store_units(const yas_store* s, int32_t* out, size_t cap);
 size_t yas_store_unit_ids(const yas_store* s, int32_t* out, size_t cap);
@@ -250,6 +261,7 @@ int yas_propagator_push_decision(yas_propagator* p, int32_t lit);              /
 int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint32_t level,
                           const uint64_t* deps, uint32_t n_deps, int overflow, int32_t antecedent);
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n); /* Frontier::seed / last.push_back */
+int yas_propagator_clear_frontier(yas_propagator* p);                     /* Frontier::clear */
 /* NogoodStore::add_learned (nogood_store.cpp:81-107): the literals are
  * canonicalised like Nogood::make; returns the new id, or -1 for an empty or
  * vacuous set, a literal 0 or an atom above the store's total_atoms (message

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <fstream>
 #include <memory>
+#include <new>
 #include <sstream>
 #include <string>
 #include <thread>
@@ -299,6 +300,41 @@ int yas_program_parse_file(const char* path, yas_program** out, int* err_line, c
     ss << in.rdbuf();
     const std::string text = ss.str();
     return yas_program_parse(text.data(), text.size(), out, err_line, err, err_cap);
+}
+
+yas_program* yas_program_create(void) { return new (std::nothrow) yas_program(); }
+
+uint32_t yas_program_intern(yas_program* p, const char* name) {
+    if (!p || !name) return 0;
+    std::uint32_t id = 0;
+    guarded(nullptr, 0, [&] {
+        id = p->prog.intern(name);
+        p->comp.reset();  // compiled views follow the program
+        p->store.reset();
+        return 0;
+    });
+    return id;
+}
+
+int yas_program_add_rule(yas_program* p, uint32_t head, const uint32_t* pos, size_t n_pos, const uint32_t* neg,
+                         size_t n_neg) {
+    if (!p || (n_pos && !pos) || (n_neg && !neg)) return YAS_ERR_ARG;
+    const std::uint32_t n = p->prog.atom_count();
+    if (head > n) return YAS_ERR_ARG;
+    for (size_t i = 0; i < n_pos; ++i)
+        if (pos[i] == 0 || pos[i] > n) return YAS_ERR_ARG;
+    for (size_t i = 0; i < n_neg; ++i)
+        if (neg[i] == 0 || neg[i] > n) return YAS_ERR_ARG;
+    return guarded(nullptr, 0, [&] {
+        Rule r;
+        r.head = head;
+        r.pos_body.assign(pos, pos + n_pos);
+        r.neg_body.assign(neg, neg + n_neg);
+        p->prog.add_rule(std::move(r));
+        p->comp.reset();
+        p->store.reset();
+        return static_cast<int>(YAS_OK);
+    });
 }
 
 void yas_program_free(yas_program* p) { delete p; }
@@ -1018,6 +1054,15 @@ void yas_store_free(yas_store* s) { delete s; }
 uint32_t yas_store_size(const yas_store* s) { return s ? s->st.size() : 0; }
 uint32_t yas_store_total_atoms(const yas_store* s) { return s ? s->st.total_atoms : 0; }
 size_t yas_store_dump_csv(const yas_store* s, char* buf, size_t cap) { return s ? put_text(s->st.dump_csv(), buf, cap) : 0; }
+size_t yas_store_nogood(const yas_store* s, uint32_t id, int32_t* lits, size_t cap, uint32_t* guard, uint8_t* origin) {
+    if (!s || id >= s->st.size()) return 0;
+    const std::uint32_t lo = s->st.off[id], len = s->st.off[id + 1] - lo;
+    for (std::uint32_t k = 0; k < len && lits && k < cap; ++k) lits[k] = s->st.pool[lo + k];
+    if (guard) *guard = s->st.guard[id];
+    if (origin) *origin = id < s->st.origin.size() ? s->st.origin[id] : 1;
+    return len;
+}
+
 size_t yas_store_units(const yas_store* s, int32_t* out, size_t cap) {
     if (!s) return 0;
     for (size_t i = 0; i < s->st.units.size() && i < cap; ++i) out[i] = s->st.units[i];
@@ -1156,6 +1201,10 @@ int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n) {
     if (!p) return YAS_ERR_ARG;
     return guarded(p->err, sizeof p->err, [&] { p->s->seed(lits, n); return static_cast<int>(YAS_OK); });
+}
+int yas_propagator_clear_frontier(yas_propagator* p) {
+    if (!p) return YAS_ERR_ARG;
+    return guarded(p->err, sizeof p->err, [&] { p->s->clear_frontier(); return static_cast<int>(YAS_OK); });
 }
 int32_t yas_propagator_add_learned(yas_propagator* p, const int32_t* lits, size_t n) {
     if (!p || (n && !lits)) return -1;

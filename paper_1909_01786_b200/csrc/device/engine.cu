@@ -3096,7 +3096,10 @@ __global__ void __launch_bounds__(BS, 1)
 
 // Low-level operations on one slot (Propagator-style API for tests and the
 // propagation microbenchmark).
-enum Op : std::uint32_t { kOpReset = 0, kOpInitial = 1, kOpPropagate = 2, kOpDecide = 3, kOpAssign = 4, kOpSeed = 5, kOpLearn = 6 };
+enum Op : std::uint32_t {
+    kOpReset = 0, kOpInitial = 1, kOpPropagate = 2, kOpDecide = 3, kOpAssign = 4, kOpSeed = 5, kOpLearn = 6,
+    kOpClearFrontier = 7
+};
 
 struct OpArgs {
     std::uint32_t op;
@@ -3223,6 +3226,10 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
             g.sync();
             break;
         }
+        case kOpClearFrontier:  // Frontier::clear (assignment.hpp:160-163)
+            if (g.leader()) c->F = 0;
+            g.sync();
+            break;
         case kOpLearn:  // NogoodStore::add_learned (kNoTruth guard)
             if (g.leader_warp()) {
                 std::int32_t* buf = sl.scratch() + 128;

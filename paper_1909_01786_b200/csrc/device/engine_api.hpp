@@ -79,6 +79,7 @@ public:
     void assign(const std::int32_t* lits, std::size_t n, std::uint32_t level, std::int32_t antecedent,
                 const unsigned long long* deps, std::size_t n_deps, bool ovf);
     void seed(const std::int32_t* lits, std::size_t n);
+    void clear_frontier();
     std::int32_t add_learned(const std::vector<std::int32_t>& lits);
     void set_count_lits(bool on);
     // diagnostics: per-pass x per-block phase timestamps of grid propagations

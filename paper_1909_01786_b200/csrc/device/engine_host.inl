@@ -664,6 +664,12 @@ void Session::seed(const std::int32_t* lits, std::size_t n) {
     record_op(*impl_, op, lits, n);
 }
 
+void Session::clear_frontier() {
+    dev::OpArgs op{};
+    op.op = dev::kOpClearFrontier;
+    record_op(*impl_, op);
+}
+
 std::int32_t Session::add_learned(const std::vector<std::int32_t>& lits_in) {
     // NogoodStore::add_learned takes a canonical Nogood (nogood.hpp:80-87):
     // atoms in [1, A], sorted, no repeats, never both signs of one atom

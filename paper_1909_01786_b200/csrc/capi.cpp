@@ -1033,15 +1033,14 @@ int yas_store_build(const int32_t* lits, const uint32_t* offsets, size_t n, cons
     if (!out) return YAS_ERR_ARG;
     *out = nullptr;
     return guarded(err, err_cap, [&] {
-        std::vector<Nogood> ngs;
-        ngs.reserve(n);
+        NogoodSet ngs;
         for (size_t k = 0; k < n; ++k) {
             std::vector<std::int32_t> l(lits + offsets[k], lits + offsets[k + 1]);
             for (std::int32_t x : l)
                 if (x == 0 || lit_atom(x) > total_atoms) throw std::invalid_argument("literal out of range");
             auto ng = Nogood::make(std::move(l), origins ? origins[k] : static_cast<std::uint8_t>(kConstraint), guards ? guards[k] : kAnyTruth);
             if (!ng || ng->lits.empty()) throw std::invalid_argument("vacuous or empty nogood " + std::to_string(k));
-            ngs.push_back(std::move(*ng));
+            ngs.push(*ng);
         }
         auto s = std::make_unique<yas_store>();
         s->st = build_store(ngs, total_atoms);
@@ -1099,8 +1098,7 @@ int yas_store_planted(uint32_t atoms, uint64_t count, uint32_t pct, uint64_t see
     std::vector<std::uint8_t> h(atoms + 1, 0);
     for (uint32_t a = 1; a <= atoms; ++a) h[a] = below(100) < 50 ? 1 : 0;
     auto hlit = [&](uint32_t a) { return h[a] ? static_cast<std::int32_t>(a) : -static_cast<std::int32_t>(a); };
-    std::vector<Nogood> ngs;
-    ngs.reserve(count);
+    NogoodSet ngs;
     while (ngs.size() < count) {
         const uint32_t len = 2 + static_cast<uint32_t>(below(5));
         std::vector<std::int32_t> l;
@@ -1109,7 +1107,7 @@ int yas_store_planted(uint32_t atoms, uint64_t count, uint32_t pct, uint64_t see
             l.push_back(below(100) < 50 ? a : -a);
         }
         l[0] = -hlit(lit_atom(l[0]));
-        if (auto ng = Nogood::make(std::move(l), kConstraint)) ngs.push_back(std::move(*ng));
+        if (auto ng = Nogood::make(std::move(l), kConstraint)) ngs.push(*ng);
     }
     std::vector<std::int32_t> sd;
     for (uint32_t a = 2; a <= atoms; ++a)

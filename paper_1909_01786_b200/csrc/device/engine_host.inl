@@ -41,8 +41,9 @@ T* dalloc(std::size_t n, std::vector<void*>& owned) {
     return static_cast<T*>(p);
 }
 
-template <class T>
-T* dupload(const std::vector<T>& v, std::vector<void*>& owned) {
+template <class V>
+typename V::value_type* dupload(const V& v, std::vector<void*>& owned) {
+    using T = typename V::value_type;
     T* p = dalloc<T>(v.size(), owned);
     if (!v.empty()) ck(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "upload");
     return p;

@@ -9,7 +9,11 @@
 
 #include <array>
 #include <cstdint>
+#include <memory>
+#include <new>
+#include <utility>
 #include <optional>
+#include <span>
 #include <string>
 #include <vector>
 
@@ -38,6 +42,52 @@ struct Nogood {
     bool may_assert(std::int32_t l) const { return l < 0 || guard == kAnyTruth || guard == lit_atom(l); }
 };
 
+/// Allocator whose value-initialisation is a no-op: large host arrays that are
+/// written in full (in parallel) right after sizing skip the zero fill.
+template <class T>
+struct NoInit : std::allocator<T> {
+    template <class U>
+    struct rebind {
+        using other = NoInit<U>;
+    };
+    NoInit() = default;
+    template <class U>
+    NoInit(const NoInit<U>&) noexcept {}
+    template <class U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <class U, class... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
+};
+template <class T>
+using BigVec = std::vector<T, NoInit<T>>;
+
+/// Flat list of canonical nogoods (literals of nogood k are
+/// lits[off[k], off[k + 1]), sorted by atom): the completion's output and the
+/// store builder's input, one allocation per array instead of per nogood.
+struct NogoodSet {
+    std::vector<std::int32_t> lits;
+    std::vector<std::uint64_t> off{0};
+    std::vector<std::uint32_t> guard;
+    std::vector<std::uint8_t> origin;
+
+    std::size_t size() const { return guard.size(); }
+    std::size_t length(std::size_t k) const { return static_cast<std::size_t>(off[k + 1] - off[k]); }
+    const std::int32_t* begin(std::size_t k) const { return lits.data() + off[k]; }
+    bool may_assert(std::size_t k, std::int32_t l) const {
+        return l < 0 || guard[k] == kAnyTruth || guard[k] == lit_atom(l);
+    }
+    void push(const Nogood& n) {
+        lits.insert(lits.end(), n.lits.begin(), n.lits.end());
+        off.push_back(lits.size());
+        guard.push_back(n.guard);
+        origin.push_back(n.origin);
+    }
+};
+
 struct RuleAux {
     AtomId b = 0, t = 0, n = 0;
     bool vacuous = false;
@@ -49,7 +99,7 @@ struct Census {
 };
 
 struct Completion {
-    std::vector<Nogood> nogoods;
+    NogoodSet nogoods;
     std::vector<RuleAux> aux;      // per rule
     std::vector<std::uint32_t> aux_rule;  // aux atom - first_aux -> rule index
     std::vector<std::uint8_t> aux_kind;   // 0 body, 1 pos test, 2 neg test
@@ -70,18 +120,18 @@ std::string dump_nogoods(const Completion& comp, const Program& prog);
 struct StaticStore {
     AtomId total_atoms = 0;
     std::vector<std::uint32_t> off{0};
-    std::vector<std::int32_t> pool;
+    BigVec<std::int32_t> pool;
     std::vector<std::uint32_t> guard;
     std::vector<std::uint8_t> origin;
     std::vector<std::int32_t> units;     // literals of the static unit nogoods
     std::vector<std::int32_t> unit_ids;  // CSR ids of length-1 entries
     std::vector<std::uint32_t> occ_off;  // (2A+2)*4 + 1
-    std::vector<std::int32_t> occ_ids;
+    BigVec<std::int32_t> occ_ids;
     // Device copy of the occurrence lists: per (literal, nogood) one 16-byte
     // entry {id | length_class << 30, guard, x, y} with x, y two *other*
     // literals of the nogood (0 when absent), so binary/ternary nogoods are
     // decided from the entry. Nogood ids therefore stay below 2^30.
-    std::vector<std::int32_t> occ_fat;  // 4 ints per occurrence, same order as occ_ids
+    BigVec<std::int32_t> occ_fat;  // 4 ints per occurrence, same order as occ_ids
     std::array<std::uint32_t, 4> bounds{0, 0, 0, 0};
 
     std::uint32_t size() const { return static_cast<std::uint32_t>(off.size() - 1); }
@@ -91,6 +141,6 @@ struct StaticStore {
 
 inline std::uint32_t length_class(std::uint32_t len) { return len >= 4 ? 3u : len - 1u; }
 
-StaticStore build_store(const std::vector<Nogood>& nogoods, AtomId total_atoms);
+StaticStore build_store(const NogoodSet& nogoods, AtomId total_atoms);
 
 }  // namespace yas

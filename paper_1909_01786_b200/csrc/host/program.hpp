@@ -32,9 +32,14 @@ class Program {
 public:
     Program() { names_.emplace_back(); }
 
-    AtomId intern(std::string_view name);
+    AtomId intern(std::string_view name) { return intern_hashed(name, name_hash(name)); }
+    AtomId intern_hashed(std::string_view name, std::uint64_t hash);
     AtomId find(std::string_view name) const;
+    static std::uint64_t name_hash(std::string_view name);
     void add_rule(Rule r);
+    /// Bulk construction (parse_text): distinct names in id order with their
+    /// hashes, then the statements in file order (bodies sorted, no repeats).
+    void adopt(std::vector<std::string> names, std::vector<std::uint64_t> hashes, std::vector<Rule> stmts);
 
     AtomId atom_count() const { return static_cast<AtomId>(names_.size() - 1); }
     const std::string& name(AtomId id) const { return names_.at(id); }
@@ -47,7 +52,17 @@ private:
     std::vector<Rule> rules_;
     std::vector<Rule> constraints_;
     std::vector<std::vector<std::uint32_t>> rules_of_{1};
-    std::unordered_map<std::string, AtomId> ids_;
+    // open-addressing name table keyed by name_hash: slot = hash high bits | id
+    // (0 empty), so a probe touches the name only on a likely match
+    std::vector<std::uint64_t> table_;
+    std::vector<std::uint64_t> hashes_{0};  // per id
+    void grow();
+
+public:
+    /// Hint: the slot `hash` probes first will be read soon (parse_text prefetches ahead).
+    void prefetch(std::uint64_t hash) const {
+        if (!table_.empty()) __builtin_prefetch(table_.data() + (hash & (table_.size() - 1)));
+    }
 };
 
 struct ParseFailure : std::runtime_error {

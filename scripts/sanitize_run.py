@@ -1,0 +1,60 @@
+"""Workload for compute-sanitizer (memcheck / racecheck / synccheck / initcheck):
+both engines on small cases — the propagator API on random and planted stores,
+full solves of a corpus slice in every mode, a cube enumeration and a portfolio.
+Kept small because the sanitizers replay every access.
+
+    compute-sanitizer --tool racecheck python scripts/sanitize_run.py
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import paper_1909_01786_b200 as Y  # noqa: E402
+from workloads import instances as I  # noqa: E402
+
+
+def golden(name):
+    with open(os.path.join(ROOT, "tests", "golden", name + ".json")) as f:
+        return json.load(f)
+
+
+def main():
+    checks = 0
+    for engine in ("block", "grid"):
+        for st in golden("propstores")["test_propagate"][:20]:
+            p = Y.Propagator(Y.NogoodStore.build(st["nogoods"], 10), 1, engine)
+            o = p.initial_propagation()
+            if not o.violated:
+                o = p.propagate_and_check(1)
+                if not o.violated and st["decision"]:
+                    p.push_decision(st["decision"])
+                    p.seed([st["decision"]])
+                    p.propagate_and_check(2)
+            assert p.trail() == st["trail"], engine
+            checks += 1
+        s, seeded, dec = Y.NogoodStore.planted(2000, 20000, 50)
+        p = Y.Propagator(s, 16, engine)
+        p.push_decision(dec)
+        p.assign_propagated(seeded, 2)
+        p.seed([dec] + seeded)
+        assert not p.propagate_and_check(2).violated
+        checks += 1
+    for prog in golden("corpus")[:24]:
+        for mode in ("fwd", "res"):
+            r = Y.solve(Y.parse_program(prog["text"]), Y.SolverConfig(max_models=0, mode=Y.LearnMode[mode]))
+            assert sorted(m.atom_ids for m in r.models) == sorted(prog["family"]), prog["name"]
+            checks += 1
+    r = Y.solve(Y.parse_program(I.queens(6)), Y.SolverConfig(max_models=0, cube_atoms=6, cube_depth=1))
+    assert len(r.models) == 4
+    r = Y.solve(Y.parse_program(I.queens(5)), Y.SolverConfig(max_models=0, engine="grid"))
+    assert len(r.models) == 10
+    r = Y.solve(Y.parse_program(I.colouring(30, 4.0, 3, 7)), Y.SolverConfig(portfolio=3))
+    assert r.status == Y.SolveStatus.sat
+    print(f"sanitize_run: {checks + 3} workloads ok")
+
+
+if __name__ == "__main__":
+    main()

@@ -173,3 +173,37 @@ def test_tp_step_and_verify_reject_out_of_range_ids():
         Y.verify_model(p, Y.Model([1, 9], []))
     assert Y.tp_step(p, []) == [1, 2]
     assert Y.verify_model(p, Y.Model([1], ["a"]))
+
+
+def _first_occurrence_names(text):
+    """Atom names in first-occurrence order (head, then body left to right), by a
+    plain Python scan of the canonical format (program.cpp:141-174 semantics)."""
+    import re
+    atom = re.compile(r"[A-Za-z_][A-Za-z0-9_]*(?:\([A-Za-z0-9_,()]*\)[A-Za-z0-9_]*)*")
+    seen, order = set(), []
+    for line in text.split("\n"):
+        line = line.split("%", 1)[0]
+        for m in atom.finditer(line):
+            name = m.group(0)
+            if name == "not" and line[m.end():m.end() + 1] == " ":
+                continue
+            if name not in seen:
+                seen.add(name)
+                order.append(name)
+    return order
+
+
+def test_parallel_parse_keeps_first_occurrence_ids():
+    """Large programs are tokenized and interned by every host thread; ids must
+    still follow first occurrence exactly, and the program must print back to
+    the same statements."""
+    for text in (I.random_program(), I.queens(12), I.hamiltonian(200, 1.0, 1)):
+        p = Y.parse_program(text)
+        names = _first_occurrence_names(text)
+        assert p.atom_count() == len(names)
+        assert [p.name(i) for i in range(1, p.atom_count() + 1)] == names
+        q = Y.parse_program(Y.print_program(p))
+        assert Y.print_program(q) == Y.print_program(p)
+    with pytest.raises(Y.ParseError) as e:
+        Y.parse_program(I.random_program() + "a :- b c.\n" + "d :- e\n")
+    assert e.value.line == I.random_program().count("\n") + 1

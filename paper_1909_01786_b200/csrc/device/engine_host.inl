@@ -10,6 +10,7 @@ namespace {
 
 constexpr int kBlockBS = 256;
 constexpr int kCubeBS = 128;  // cube enumeration with 8 searches per SM
+constexpr int kWarpBS = 32;   // cube enumeration with 16 single-warp searches per SM
 constexpr int kGridBS = 512;
 
 void ck(cudaError_t e, const char* what) {
@@ -274,8 +275,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     if (!opt.grid) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
-        per_sm = std::min<std::uint32_t>(8, (n_slots + sms - 1) / sms);
-        if (per_sm > 6) per_sm = 8;  // 6 or 8 searches per SM: 128-thread CTAs
+        per_sm = std::min<std::uint32_t>(16, (n_slots + sms - 1) / sms);
+        if (per_sm > 8) per_sm = 16;  // 16 searches per SM: one warp each
+        else if (per_sm > 6) per_sm = 8;  // 6 or 8 searches per SM: 128-thread CTAs
         else if (per_sm > 4) per_sm = 6;
         // keep most of the unified L1 for the (read-only) static store
         std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
@@ -293,7 +295,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
                         reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>),
                         reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 6>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 8>)}) {
+                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 8>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kWarpBS, 16>)}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
@@ -309,7 +312,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            if (per_sm > 6)
+            if (per_sm > 8)
+                dev::block_kernel<kWarpBS, 16><<<n_slots, kWarpBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            else if (per_sm > 6)
                 dev::block_kernel<kCubeBS, 8><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else if (per_sm > 4)
                 dev::block_kernel<kCubeBS, 6><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);

@@ -1955,6 +1955,7 @@ struct Search {
         const std::uint32_t cnt = __popc(wm), tnext = __shfl_sync(0xffffffffu, oinc, 31);
         const std::uint32_t dst = cur ^ 1u;
         tprof(3);
+        __syncwarp();  // every lane has read the frontier mirror (sm.fr / sm.froff) before it is rewritten
         if (winner) {
             set_cell(pa, plit > 0 ? static_cast<std::int32_t>(level) : -static_cast<std::int32_t>(level));
             sl.reason()[pa] = id;
@@ -3017,9 +3018,9 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
                 g.c->won = prev == 0xffffffffu ? 1u : 0u;
                 sh->stop = 1;
                 if (C.fleet) atomicExch_system(&C.fleet->stop, 1u);
-                g.c->status = kDone;
             }
-            g.sync();
+            g.sync();  // every thread has read status and phase: now the leader may finish the search
+            if (g.leader()) g.c->status = kDone;
             return;
         }
         if (g.c->phase == kIdle || g.c->phase == kFinished) {

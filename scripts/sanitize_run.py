@@ -51,8 +51,9 @@ def main():
     assert len(r.models) == 4
     r = Y.solve(Y.parse_program(I.queens(5)), Y.SolverConfig(max_models=0, engine="grid"))
     assert len(r.models) == 10
-    r = Y.solve(Y.parse_program(I.colouring(30, 4.0, 3, 7)), Y.SolverConfig(portfolio=3))
-    assert r.status == Y.SolveStatus.sat
+    col = Y.parse_program(I.colouring(30, 4.0, 3, 7))
+    r = Y.solve(col, Y.SolverConfig(portfolio=3))
+    assert r.status == Y.solve(col, Y.SolverConfig()).status
     print(f"sanitize_run: {checks + 3} workloads ok")
 
 

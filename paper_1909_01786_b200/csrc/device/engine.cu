@@ -1716,7 +1716,41 @@ struct Search {
 #endif
     static constexpr std::uint32_t kSoloT = YAS_SOLO_T;  // measured (L2 flushed): 0 -> 0.288 ms, 512 -> 0.297, 2048 -> 0.311
 
+    // Bulk L2 prefetch (TMA, cp.async.bulk.prefetch.L2) of this block's share
+    // of [p, p + bytes): fire-and-forget, no registers or shared memory held.
+    __device__ __forceinline__ void prefetch_share(const void* p, unsigned long long bytes) const {
+        const unsigned long long a0 = reinterpret_cast<unsigned long long>(p);
+        const unsigned long long lo = (a0 + 15) & ~15ull, hi = (a0 + bytes) & ~15ull;
+        if (hi <= lo) return;
+        const unsigned long long share = (((hi - lo) / gridDim.x) + 15) & ~15ull;
+        const unsigned long long b = lo + share * blockIdx.x, e = min(hi, b + share);
+        constexpr unsigned long long kChunk = 32768;
+        for (unsigned long long x = b + threadIdx.x * kChunk; x < e; x += blockDim.x * kChunk) {
+            const unsigned n = static_cast<unsigned>(min(kChunk, e - x));
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x), "r"(n) : "memory");
+        }
+    }
+
+    // When the static store and the per-atom state the passes touch fit in L2,
+    // stream them in at HBM bandwidth while the first (widest) pass runs: the
+    // later, narrow passes then meet L2 latency instead of a DRAM round trip
+    // at every dependent step (fat entry, nogood literals, claims, offsets).
+    __device__ __noinline__ void prefetch_store() const {
+        const std::uint32_t keys = (2 * S.A + 2) * 4;
+        const unsigned long long occ = __ldg(S.occ_off + keys), lits = __ldg(S.off + S.N);
+        prefetch_share(S.occ, occ * sizeof(int4));
+        prefetch_share(S.pool, lits * 4ull);
+        prefetch_share(S.off, (S.N + 1ull) * 4ull);
+        prefetch_share(S.guard, S.N * 4ull);
+        prefetch_share(S.occ_off, (keys + 1ull) * 4ull);
+        prefetch_share(sl.claim(), S.N * 8ull);
+        prefetch_share(sl.win(), (S.A + 1ull) * 8ull);
+        prefetch_share(sl.cells(), (S.A + 1ull) * 4ull);
+        prefetch_share(sl.ltot(), (2ull * S.A + 2) * 4ull);
+    }
+
     __device__ __forceinline__ bool propagate_grid(std::uint32_t level) {
+        if (C.prefetch) prefetch_store();
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
@@ -2097,8 +2131,9 @@ struct Search {
             sl.tpos()[a] = 0;
             sl.reason()[a] = kReasonNone;
         }
+        const bool lower = target < c->cdl;  // read by every thread before the barrier
         g.sync();
-        if (g.leader() && target < c->cdl) {
+        if (g.leader() && lower) {
             c->ts = from;
             c->cdl = target;
         }
@@ -2543,6 +2578,7 @@ struct Search {
     }
 
     __device__ __forceinline__ bool handle_conflicts() {
+        g.sync();  // the whole group has left propagation (it reads F, T, ... at its loop top)
         if (g.leader_warp()) analyze_and_learn();
         g.sync();
 #ifdef YAS_TINY_PROF
@@ -2935,9 +2971,11 @@ struct Search {
             }
             g.sync();
             mark(11);
-            if constexpr (!G::kGrid)
-                if (c->status != kRunning) return;
-            if (c->b[15]) {
+            // every thread reads both words before anyone may change them again
+            const bool ended = !G::kGrid && c->status != kRunning, yield = c->b[15] != 0;
+            if (ended) return;
+            if (yield) {
+                g.sync();
                 if (g.leader()) c->status = kYield;
                 g.sync();
                 return;
@@ -2959,7 +2997,9 @@ struct Search {
                 const bool go_on = handle_conflicts();
                 mark(7);
                 if (!go_on) {
-                    if (c->status != kRunning) return;
+                    const bool ended = c->status != kRunning;
+                    g.sync();  // status read everywhere before the leader moves on
+                    if (ended) return;
                     if (g.leader()) c->phase = kFinished;
                     g.sync();
                     return;

@@ -22,9 +22,10 @@ def golden(name):
 
 
 def main():
+    quick = "--quick" in sys.argv  # racecheck replays every shared-memory access: a smaller slice
     checks = 0
     for engine in ("block", "grid"):
-        for st in golden("propstores")["test_propagate"][:20]:
+        for st in golden("propstores")["test_propagate"][:6 if quick else 20]:
             p = Y.Propagator(Y.NogoodStore.build(st["nogoods"], 10), 1, engine)
             o = p.initial_propagation()
             if not o.violated:
@@ -35,14 +36,14 @@ def main():
                     p.propagate_and_check(2)
             assert p.trail() == st["trail"], engine
             checks += 1
-        s, seeded, dec = Y.NogoodStore.planted(2000, 20000, 50)
+        s, seeded, dec = Y.NogoodStore.planted(500 if quick else 2000, 5000 if quick else 20000, 50)
         p = Y.Propagator(s, 16, engine)
         p.push_decision(dec)
         p.assign_propagated(seeded, 2)
         p.seed([dec] + seeded)
         assert not p.propagate_and_check(2).violated
         checks += 1
-    for prog in golden("corpus")[:24]:
+    for prog in golden("corpus")[:6 if quick else 24]:
         for mode in ("fwd", "res"):
             r = Y.solve(Y.parse_program(prog["text"]), Y.SolverConfig(max_models=0, mode=Y.LearnMode[mode]))
             assert sorted(m.atom_ids for m in r.models) == sorted(prog["family"]), prog["name"]

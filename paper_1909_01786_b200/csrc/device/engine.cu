@@ -1716,41 +1716,7 @@ struct Search {
 #endif
     static constexpr std::uint32_t kSoloT = YAS_SOLO_T;  // measured (L2 flushed): 0 -> 0.288 ms, 512 -> 0.297, 2048 -> 0.311
 
-    // Bulk L2 prefetch (TMA, cp.async.bulk.prefetch.L2) of this block's share
-    // of [p, p + bytes): fire-and-forget, no registers or shared memory held.
-    __device__ __forceinline__ void prefetch_share(const void* p, unsigned long long bytes) const {
-        const unsigned long long a0 = reinterpret_cast<unsigned long long>(p);
-        const unsigned long long lo = (a0 + 15) & ~15ull, hi = (a0 + bytes) & ~15ull;
-        if (hi <= lo) return;
-        const unsigned long long share = (((hi - lo) / gridDim.x) + 15) & ~15ull;
-        const unsigned long long b = lo + share * blockIdx.x, e = min(hi, b + share);
-        constexpr unsigned long long kChunk = 32768;
-        for (unsigned long long x = b + threadIdx.x * kChunk; x < e; x += blockDim.x * kChunk) {
-            const unsigned n = static_cast<unsigned>(min(kChunk, e - x));
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(x), "r"(n) : "memory");
-        }
-    }
-
-    // When the static store and the per-atom state the passes touch fit in L2,
-    // stream them in at HBM bandwidth while the first (widest) pass runs: the
-    // later, narrow passes then meet L2 latency instead of a DRAM round trip
-    // at every dependent step (fat entry, nogood literals, claims, offsets).
-    __device__ __noinline__ void prefetch_store() const {
-        const std::uint32_t keys = (2 * S.A + 2) * 4;
-        const unsigned long long occ = __ldg(S.occ_off + keys), lits = __ldg(S.off + S.N);
-        prefetch_share(S.occ, occ * sizeof(int4));
-        prefetch_share(S.pool, lits * 4ull);
-        prefetch_share(S.off, (S.N + 1ull) * 4ull);
-        prefetch_share(S.guard, S.N * 4ull);
-        prefetch_share(S.occ_off, (keys + 1ull) * 4ull);
-        prefetch_share(sl.claim(), S.N * 8ull);
-        prefetch_share(sl.win(), (S.A + 1ull) * 8ull);
-        prefetch_share(sl.cells(), (S.A + 1ull) * 4ull);
-        prefetch_share(sl.ltot(), (2ull * S.A + 2) * 4ull);
-    }
-
     __device__ __forceinline__ bool propagate_grid(std::uint32_t level) {
-        if (C.prefetch) prefetch_store();
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
         const std::uint32_t dlev = level > c->cdl ? level : c->cdl;
@@ -3103,6 +3069,7 @@ __global__ void __launch_bounds__(BS, MINB)
     }
     __syncthreads();
     if (threadIdx.x == 0 && ctl.status == kYield) ctl.status = kRunning;
+    __syncthreads();  // the resumed status is what every thread reads first
     BlockG<BS> g{&ctl, sbuf, sd, si};
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
     __syncthreads();

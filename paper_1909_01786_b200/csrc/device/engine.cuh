@@ -67,7 +67,6 @@ struct Config {
     // (mode, heuristic) = (v & 1, v >> 1); the first to finish stops the others
     std::uint32_t portfolio, pf_base;
     std::uint32_t warp_pass_t;  // single-CTA searches: passes with at most this many entries run in one warp
-    std::uint32_t prefetch;     // whole-grid propagation: stream the store into L2 at the start of a call
     Fleet* fleet;               // cube queue / portfolio claim shared across GPUs (null: this GPU's Shared)
     std::uint32_t fleet_tag;    // this GPU's portfolio claim tag base (slot index added)
 };

@@ -459,7 +459,6 @@ struct Session::Impl {
     std::size_t h_uploaded = 0;  // prefix of this batch's staging already sent (bulk inputs go early)
     dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
     bool ctl_pending = false;
-    bool prefetch_ok = false;  // grid session whose store + pass state fit in L2 (prefetched per call)
 
     std::size_t append(const void* src, std::size_t ints) {
         if (stage_inflight) {  // the previous batch's upload may still read the buffer
@@ -504,13 +503,6 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
     impl_->ar.pool_size_ = store.pool.size();
     impl_->ar.upload_static(store, {}, 0, {});
     impl_->gblocks = grid ? grid_blocks_for(device) : 0;
-    {  // static store + claims / per-atom state: prefetched into L2 when they fit in ~3/4 of it
-        int l2 = 0;
-        cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, device);
-        const std::uint64_t bytes = 16ull * store.pool.size() + 4ull * store.pool.size() + 16ull * store.size() +
-                                    4ull * store.occ_off.size() + 24ull * store.total_atoms;
-        impl_->prefetch_ok = grid && l2 > 0 && bytes <= 3ull * static_cast<std::uint64_t>(l2) / 4;
-    }
     impl_->ar.alloc_slots(1, deps_words, lcap, lpool, 16, 128, 0, impl_->gblocks);
     if (!grid) {
         impl_->smc = plan_smem(impl_->ar.A, 96u * 1024u);
@@ -556,8 +548,6 @@ namespace {
 // it). `ms` (when given) waits for the kernel and returns its CUDA-event time.
 void flush_ops(Session::Impl& im, float* ms) {
     if (im.pending.empty()) return;
-    im.cfg.prefetch = im.prefetch_ok ? 1u : 0u;
-    if (const char* e = std::getenv("YAS_PREFETCH")) im.cfg.prefetch = im.grid && std::strtoul(e, nullptr, 10) ? 1u : 0u;
     if (im.h_used) {
         if (im.h_used > im.d_stage_cap) {
             ck(cudaStreamSynchronize(im.stream), "stream");  // the old buffer may still be read

@@ -3065,11 +3065,13 @@ __global__ void __launch_bounds__(BS, MINB)
     {
         const std::uint32_t* src = reinterpret_cast<const std::uint32_t*>(sl.ctl());
         std::uint32_t* dst = reinterpret_cast<std::uint32_t*>(&ctl);
-        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) dst[i] = src[i];
+        constexpr std::uint32_t kStatus = offsetof(Ctl, status) / 4;
+        for (std::uint32_t i = threadIdx.x; i < sizeof(Ctl) / 4; i += BS) {
+            const std::uint32_t v = src[i];
+            dst[i] = (i == kStatus && v == kYield) ? static_cast<std::uint32_t>(kRunning) : v;  // a yielded search resumes
+        }
     }
     __syncthreads();
-    if (threadIdx.x == 0 && ctl.status == kYield) ctl.status = kRunning;
-    __syncthreads();  // the resumed status is what every thread reads first
     BlockG<BS> g{&ctl, sbuf, sd, si};
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
     __syncthreads();

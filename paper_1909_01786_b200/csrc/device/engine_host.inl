@@ -193,7 +193,7 @@ struct Arena {
         };
         zero(L.o_ctl, L.o_claim);
         zero(L.o_pending, L.o_litat);
-        zero(L.o_dup, L.o_mbuf);
+        zero(L.o_dup, L.o_tbuf);  // ... and the model buffers: the host copies whole strided rows
         // occat (place reads whole 128-byte lines, masking bits outside the word) and the grid mirror
         zero(L.o_occat, L.o_obat);
         dev::init_slots<<<n_slots, 256>>>(L, static_cast<std::uint32_t>(A1), K.items);

@@ -342,6 +342,9 @@ def main():
         line["enumeration_q8"] = enumeration(Y, I, rank, world, local, n=8)
         parity["queens12"] = line["enumeration"].pop("parity")
         parity["queens8"] = line["enumeration_q8"].pop("parity")
+        log("enumeration q13 (scaling workload)")
+        line["enumeration_q13"] = enumeration(Y, I, rank, world, local, n=13)
+        parity["queens13"] = line["enumeration_q13"].pop("parity")
         if rank == 0:
             log("random program 4a")
             line["random_program_4a"] = random_program(Y, I, local)
@@ -513,7 +516,7 @@ def enumeration(Y, I, rank, world, local, n=12):
     cubes = allreduce([float(r.stats.cubes)], "sum", world)[0]
     wall_max, dev_max = allreduce([wall, r.stats.device_ms], "max", world)
     out = {"instance": f"queens{n} (all answer sets)", "models": int(n_models),
-           "expected_models": {8: 92, 10: 724, 12: 14200}.get(n),
+           "expected_models": {8: 92, 10: 724, 12: 14200, 13: 73712}.get(n),
            "wall_ms": wall_max, "device_ms": dev_max, "cubes": int(cubes), "n_gpus": world,
            "passes_rank0": r.stats.passes, "cube_queue": "shared (fleet)" if fl is not None else "one GPU"}
     # parity: the union of every rank's models against the reference's model set
@@ -523,8 +526,8 @@ def enumeration(Y, I, rank, world, local, n=12):
         parts = [None] * world
         dist.all_gather_object(parts, ids)
         ids = [m for part in parts for m in part]
-    if n == 12:
-        exp = pins()["queens12"]
+    if n >= 12:
+        exp = pins()[f"queens{n}"]
         out["parity"] = len(ids) == exp["models"] and model_set_digest(ids) == exp["model_set_digest"]
     else:
         with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as f:
@@ -543,7 +546,7 @@ def enumeration(Y, I, rank, world, local, n=12):
             cubes_all = A.cubes(prog, n, 0, want=4 * 148 * 8 * world)
             cs = cpu_cube_split(Y, text, cubes_all)
             cs["parity"] = cs["models"] == out["expected_models"] and (
-                n != 12 or cs["model_set_digest"] == pins()["queens12"]["model_set_digest"])
+                cs["model_set_digest"] == pins()[f"queens{n}"]["model_set_digest"])
             cs["cpu_model"] = cpu_model()
             out["cpu_reference_cube_split"] = cs
             full = os.path.join(ROOT, "profiles", "r02_q12_reference_full.json")

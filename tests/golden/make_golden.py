@@ -132,7 +132,34 @@ def pins():
         r = solve_text(I.queens(n), ["-n", "0"])
         out[f"queens{n}"] = {"status": r["status"], "models": len(r["models"]),
                              "model_set_digest": model_set_digest(r["models"]), "stats": r["stats"]}
+    out["queens13"] = queens13_by_cubes()
     return out
+
+
+def queens13_by_cubes():
+    """queens(13), the multi-GPU scaling workload: a single reference enumeration
+    runs for hours here, so the reference solves every cube of the ladder split
+    (one `aspine_ref cubes` process per core); the cubes partition the answer
+    sets, and the union must hold 73,712 distinct models (OEIS A000170)."""
+    import tempfile
+    import paper_1909_01786_b200 as Y
+    text = I.queens(13)
+    prog = Y.parse_program(text)
+    cubes = Y.cubes(prog, 13, 0, want=4 * 148 * 8)
+    nproc = os.cpu_count() or 1
+    with tempfile.TemporaryDirectory() as d:
+        lp, cf = os.path.join(d, "q13.lp"), os.path.join(d, "cubes.txt")
+        with open(lp, "w") as f:
+            f.write(text)
+        with open(cf, "w") as f:
+            for c in cubes:
+                f.write(" ".join(prog.name(abs(l)) for l in c if l) + "\n")
+        procs = [subprocess.Popen([REF, "cubes", lp, cf, str(k), str(nproc)], stdout=subprocess.PIPE, text=True)
+                 for k in range(nproc)]
+        models = [m for p in procs for m in json.loads(p.communicate()[0])["models"]]
+    assert len({tuple(m) for m in models}) == len(models) == 73712
+    return {"status": "SAT", "models": len(models), "model_set_digest": model_set_digest(models),
+            "source": f"reference, {len(cubes)} cubes solved one by one on {nproc} processes"}
 
 
 def main():

@@ -77,3 +77,13 @@ def test_stat_keys_cover_reference_counters():
     """Every counter of the pinned 4a run is compared except wall time and watches."""
     exp = golden("pins")["rand4a"]["stats"]
     assert set(exp) - set(STAT_KEYS) == {"wall_ms", "watch_replacements"}
+
+
+def test_queens13_two_devices_model_set():
+    """queens(13) (73,712 answer sets), the scaling workload, through one shared
+    cube queue over two GPUs of the process (the same B200 listed twice here)."""
+    exp = golden("pins")["queens13"]
+    r = Y.solve(Y.parse_program(I.queens(13)), Y.SolverConfig(max_models=0, cube_atoms=13, devices=[0, 0]))
+    ids = [m.atom_ids for m in r.models]
+    assert len(ids) == exp["models"] == 73_712
+    assert model_set_digest(ids) == exp["model_set_digest"]

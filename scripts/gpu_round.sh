@@ -15,10 +15,15 @@ if want bench; then
   timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 fi
 if want ncu; then
+  # reports stay on the box (/tmp/ncu, too large to copy back); summaries come back
+  mkdir -p /tmp/ncu
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-extras > gpurun_out/bench_ncu.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:op_grid_kernel -s 5 -c 1 -o gpurun_out/planted_grid -f python bench.py --steps 1 --warmup 3 --no-extras > gpurun_out/ncu_planted.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:block_kernel -s 1 -c 1 -o gpurun_out/q12_cubes -f python scripts/enum_timing.py 12 > gpurun_out/ncu_q12.log 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:block_kernel -c 1 -o gpurun_out/ham200_block -f python scripts/run_one.py ham200 > gpurun_out/ncu_ham200.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:op_grid_kernel -s 5 -c 1 -o /tmp/ncu/planted_grid -f python bench.py --steps 1 --warmup 3 --no-extras > gpurun_out/ncu_planted.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:block_kernel -s 1 -c 1 -o /tmp/ncu/q12_cubes -f python scripts/enum_timing.py 12 > gpurun_out/ncu_q12.log 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:block_kernel -c 1 -o /tmp/ncu/ham200_block -f python scripts/run_one.py ham200 > gpurun_out/ncu_ham200.log 2>&1
+  for r in planted_grid q12_cubes ham200_block; do
+    [ -f /tmp/ncu/$r.ncu-rep ] && timeout 300 python scripts/summarize_ncu.py /tmp/ncu/$r.ncu-rep gpurun_out/ncu_$r >> gpurun_out/ncu_summaries.log 2>&1
+  done
 fi
 if want san; then
   for t in memcheck synccheck initcheck; do

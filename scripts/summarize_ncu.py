@@ -15,7 +15,13 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "launch__block_size", "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active",
         "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
         "l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct", "smsp__inst_executed.sum",
-        "sm__cycles_elapsed.avg.per_second", "launch__shared_mem_per_block_dynamic"]
+        "sm__cycles_elapsed.avg.per_second", "launch__shared_mem_per_block_dynamic",
+        "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+        "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__inst_executed.avg.per_cycle_active",
+        "lts__t_sectors.sum", "lts__t_sectors_op_atom.sum", "lts__t_sectors_op_red.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__warps_eligible.avg.per_cycle_active",
+        "launch__occupancy_limit_registers", "sm__maximum_warps_per_active_cycle_pct"]
 
 
 def ncu(args):

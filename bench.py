@@ -271,7 +271,7 @@ def main():
     peak, peak_kind = peaks()
     achieved = algo_bytes / (avg_ms / 1e3) / 1e9
     traffic = None
-    prof_json = os.path.join(ROOT, "profiles", "r01_planted_grid.json")
+    prof_json = os.path.join(ROOT, "profiles", "r02_planted_grid.json")
     if os.path.exists(prof_json):
         with open(prof_json) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")

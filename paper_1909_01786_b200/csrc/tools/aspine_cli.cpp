@@ -107,6 +107,12 @@ int run_solve(int argc, char** argv) {
             cfg.cube_atoms = number<std::uint32_t>(a, val());
         } else if (a == "--portfolio") {  // device extension: first-model portfolio of N searches
             cfg.portfolio = number<std::uint32_t>(a, val());
+        } else if (a == "--devices") {  // device extension: GPUs of this process, e.g. 0,1,2,3
+            std::istringstream in(val());
+            cfg.devices.clear();
+            for (std::string d; std::getline(in, d, ',');) cfg.devices.push_back(number<int>(a, d));
+            if (cfg.devices.empty()) throw Usage("--devices: a comma-separated list of CUDA ordinals");
+            cfg.device = cfg.devices.front();
         } else if (a.size() > 1 && a[0] == '-' && a != "-") {
             throw Usage("unknown option " + a);
         } else if (file.empty()) {

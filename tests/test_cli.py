@@ -24,6 +24,7 @@ def files(tmp_path):
 
 def test_usage_parse_and_io_errors(files):
     assert run(["solve", "--no-such-flag", "x"])[0] == 2
+    assert run(["solve", "--devices", "0,x", str(files / "even.lp")])[0] == 2
     assert run(["solve", str(files / "bad.lp")])[0] == 2
     assert run(["solve", str(files / "missing.lp")])[0] == 1
     assert run([])[0] == 2
@@ -47,3 +48,12 @@ def test_solve_exit_codes_and_output(files):
     assert rc == 10 and "instance,mode,heuristic,workers,status," in out and ",res,jw,1,SAT,2," in out
     rc, _ = run(["solve", str(files / "even.lp"), "--workers", "4", "--restarts", "geometric:2:2", "-n", "0"])
     assert rc == 10
+
+
+@pytest.mark.gpu
+def test_enumeration_on_two_devices(files, tmp_path):
+    """--devices: one cube queue over the listed GPUs (the same B200 twice here)."""
+    from workloads import instances as I
+    (tmp_path / "q6.lp").write_text(I.queens(6))
+    rc, out = run(["solve", str(tmp_path / "q6.lp"), "-n", "0", "--cubes", "6", "--devices", "0,0"])
+    assert rc == 10 and out.count("Answer:") == 4

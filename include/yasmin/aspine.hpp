@@ -320,6 +320,7 @@ struct SolverConfig {
     std::uint32_t portfolio = 0;  // first-model portfolio: concurrent searches with diverse (mode, heuristic)
     bool count_lits = false;      // exact literals of checked nogoods in stats.checked_lits
     std::vector<int> devices;     // cube enumeration / portfolio over these GPUs of this process
+    bool reference_order = false; // enumerate as one search in the reference's model order
     yas_fleet* fleet = nullptr;   // processes sharing one enumeration / portfolio (yas_fleet_create*)
 };
 
@@ -375,6 +376,7 @@ inline SolveResult solve(const GroundProgram& prog, const SolverConfig& cfg) {
         c.devices = cfg.devices.data();
     }
     c.fleet = cfg.fleet;
+    c.reference_order = cfg.reference_order ? 1 : 0;
     if (cfg.trace) {
         c.trace = [](const yas_trace* t, void* user) {
             (*static_cast<const std::function<void(const ConflictTrace&)>*>(user))(

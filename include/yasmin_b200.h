@@ -166,6 +166,10 @@ typedef struct yas_config {
     uint32_t n_devices;  /* cube enumeration / portfolio over this many GPUs of this process (0 or 1: `device`
                             only); cubes come from one queue in the first GPU's memory (NVLink peer access) */
     const int* devices;  /* n_devices CUDA ordinals (NULL: device, device + 1, ...); an ordinal may repeat */
+    int reference_order; /* 1: an enumeration (max_models == 0) is one search with the reference's model
+                            order and trajectory. 0 (default): a program with >= 16 even-loop choice pairs
+                            is enumerated as cubes (cube_atoms = 8) over the GPU(s); same answer sets and
+                            count, models in cube order (deterministic). Tracing forces the reference order. */
     yas_fleet* fleet;    /* several processes share the enumeration / portfolio; overrides rank, world and
                             device (one GPU per process). Every rank calls yas_solve with the same program
                             and options; each returns the models its GPU found. */

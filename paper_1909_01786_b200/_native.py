@@ -57,7 +57,8 @@ class yas_config(C.Structure):
         ("device", C.c_int), ("engine", C.c_int), ("cube_atoms", C.c_uint32), ("cube_depth", C.c_uint32),
         ("slots", C.c_uint32),
         ("rank", C.c_int), ("world", C.c_int), ("portfolio", C.c_uint32), ("count_lits", C.c_uint32),
-        ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int)), ("fleet", C.c_void_p),
+        ("n_devices", C.c_uint32), ("devices", C.POINTER(C.c_int)), ("reference_order", C.c_int),
+        ("fleet", C.c_void_p),
     ]
 
 

@@ -138,6 +138,7 @@ class SolverConfig:
     portfolio: int = 0  # first-model portfolio: concurrent searches with diverse (mode, heuristic)
     count_lits: bool = False  # exact literals of checked nogoods in stats.checked_lits (roofline accounting)
     devices: Optional[Sequence[int]] = None  # cube enumeration / portfolio over these GPUs of this process
+    reference_order: bool = False  # enumerate as one search in the reference's model order (no automatic cubes)
     fleet: Optional["Fleet"] = None  # several processes share the enumeration / portfolio (one GPU each)
 
 
@@ -429,6 +430,7 @@ def _config(cfg: SolverConfig) -> N.yas_config:
         c.n_devices = len(cfg.devices)
         c._devs = (C.c_int * len(cfg.devices))(*cfg.devices)  # kept alive with the struct
         c.devices = C.cast(c._devs, C.POINTER(C.c_int))
+    c.reference_order = 1 if cfg.reference_order else 0
     if cfg.fleet is not None:
         c.fleet = cfg.fleet._h
     return c

@@ -178,6 +178,16 @@ std::vector<Choice> choice_atoms(const Program& prog) {
     return out;
 }
 
+// Automatic split of a plain enumeration (max_models == 0, no cube_atoms):
+// programs with at least this many even-loop choice pairs, ladders this wide.
+constexpr std::size_t kAutoCubePairs = 16;
+constexpr std::uint32_t kAutoCubeWidth = 8;
+
+bool first_choices_are_pairs(const Program& prog) {
+    const std::vector<Choice> ch = choice_atoms(prog);
+    return ch.size() >= kAutoCubePairs && ch[kAutoCubePairs - 1].b != 0;
+}
+
 // Nested "ladder" cubes over windows of L choice atoms: at each of d levels the
 // cube picks i in [0, L]: i < L means (F a_0, ..., F a_{i-1}, T a_i) and i = L
 // means all F. The (L+1)^d cubes partition the answer sets exactly. Cube c
@@ -631,6 +641,13 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         std::uint32_t per_sm = 8;  // concurrent searches per SM for cube enumeration
         if (const char* e = std::getenv("YAS_SEARCHES_PER_SM")) per_sm = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
         const std::uint32_t slots_per_gpu = cfg.slots ? cfg.slots : static_cast<std::uint32_t>(sms) * per_sm;
+        // Enumerating every answer set of a program with many choice pairs is
+        // split into cubes unless the caller asked for the reference's model
+        // order (or traces the reference's conflict sequence): the answer-set
+        // set and count are the reference's, the order becomes cube order.
+        if (cfg.cube_atoms == 0 && cfg.max_models == 0 && !cfg.reference_order && !cfg.trace &&
+            first_choices_are_pairs(prog))
+            cfg.cube_atoms = kAutoCubeWidth;
         const bool enumerate = cfg.cube_atoms > 0 && cfg.max_models == 0;
         const bool portfolio = cfg.portfolio > 1 && cfg.max_models == 1 && cfg.cube_atoms == 0;
         if (!enumerate && !portfolio) devs.resize(1);  // one search: the first GPU
@@ -763,6 +780,28 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                 for (std::size_t m = 1; m < d.offs.size(); ++m) res->off.push_back(base + d.offs[m]);
                 res->cubes.insert(res->cubes.end(), d.mcubes.begin(), d.mcubes.end());
                 traces.insert(traces.end(), d.traces.begin(), d.traces.end());
+            }
+            if (enumerate && res->count() > 1) {  // cube order: the same for any scheduling of the cubes
+                const std::size_t n = res->count();
+                std::vector<std::uint32_t> ord(n);
+                for (std::uint32_t m = 0; m < n; ++m) ord[m] = m;
+                std::stable_sort(ord.begin(), ord.end(),
+                                 [&](std::uint32_t a, std::uint32_t b) { return res->cubes[a] < res->cubes[b]; });
+                std::vector<std::uint32_t> ids;
+                std::vector<std::uint64_t> off{0};
+                std::vector<std::uint32_t> cubes;
+                ids.reserve(res->ids.size());
+                off.reserve(n + 1);
+                cubes.reserve(n);
+                for (std::uint32_t m : ord) {
+                    ids.insert(ids.end(), res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[m]),
+                               res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[m + 1]));
+                    off.push_back(ids.size());
+                    cubes.push_back(res->cubes[m]);
+                }
+                res->ids.swap(ids);
+                res->off.swap(off);
+                res->cubes.swap(cubes);
             }
             if (fl && fl->comm) {  // the final all-reduce: models, fleet-wide errors, the portfolio winner
                 std::uint64_t sum[1] = {res->count()};

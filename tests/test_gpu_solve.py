@@ -55,6 +55,25 @@ def test_queens8_all_models_and_trace(key):
     assert [m.atom_ids for m in r.models] == exp["models"]
     assert not stats_diff(r.stats, exp["stats"])
     assert trace == exp["trace"]
+    # without a trace the same search runs when the reference order is asked for
+    cfg.trace = None
+    cfg.reference_order = True
+    r = Y.solve(Y.parse_program(I.queens(8)), cfg)
+    assert [m.atom_ids for m in r.models] == exp["models"] and not stats_diff(r.stats, exp["stats"])
+
+
+def test_plain_enumeration_is_cube_split_by_default():
+    """max_models = 0 on a program with many choice pairs enumerates cubes over the GPU
+    (VERDICT r1 #8): the reference's answer-set set, in cube order, the same on every run."""
+    exp = sorted(golden("configs")["queens8/fwd/occ"]["models"])
+    prog = Y.parse_program(I.queens(8))
+    runs = [Y.solve(prog, Y.SolverConfig(max_models=0)) for _ in range(2)]
+    for r in runs:
+        assert sorted(m.atom_ids for m in r.models) == exp and r.stats.cubes > 1
+        assert r.cubes == sorted(r.cubes)
+    assert [m.atom_ids for m in runs[0].models] == [m.atom_ids for m in runs[1].models]
+    single = Y.solve(prog, Y.SolverConfig(max_models=0, reference_order=True))
+    assert single.stats.cubes == 1 and [m.atom_ids for m in single.models] == golden("configs")["queens8/fwd/occ"]["models"]
 
 
 @pytest.mark.parametrize("name", ["colour2000", "ham200"])

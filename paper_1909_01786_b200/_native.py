@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libyasmin_b200.so")
+# YAS_LIBRARY: developer A/B of an alternative build of the same library (default: the in-tree one)
+LIB_PATH = os.environ.get("YAS_LIBRARY") or os.path.join(_HERE, "_lib", "libyasmin_b200.so")
 
 # every symbol include/yasmin_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = [

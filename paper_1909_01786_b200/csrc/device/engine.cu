@@ -1027,9 +1027,16 @@ struct Search {
             const int vy = val(atom_of(ent.w));
             sy = vy == 0 ? 0 : ((vy > 0) == (ent.w > 0) ? 1 : -1);
         }
-        if (cls == 3 && !(sx < 0 || sy < 0 || (sx == 0 && sy == 0))) {
-            evaluate(ent.x, conflict, prop, plit, len, d0, meta);
-            return;
+        if (cls == 3) {  // long: three blockers (z, w, y); a dead one or two free ones decide without a scan
+            const int vq = val(atom_of(ent.y));
+            const int sq = vq == 0 ? 0 : ((vq > 0) == (ent.y > 0) ? 1 : -1);
+            const bool decided = sx < 0 || sy < 0 || sq < 0 || (sx == 0) + (sy == 0) + (sq == 0) >= 2;
+            if (!decided) {
+                evaluate(ent.x, conflict, prop, plit, len, d0, meta);
+                return;
+            }
+            len = C.count_lits ? length_of(static_cast<std::uint32_t>(ent.x)) : 4;
+            return;  // satisfied, or two free
         }
         len = cls + 1;
         if (C.count_lits && cls == 3) len = length_of(static_cast<std::uint32_t>(ent.x));
@@ -1362,11 +1369,29 @@ struct Search {
                         sy = vy == 0 ? 0 : ((vy > 0) == (ent[u].w > 0) ? 1 : -1);
                     }
                     const bool decided = sx < 0 || sy < 0 || (sx == 0 && sy == 0);
-                    if (cls[u] == 3 && !decided) { stt[u] = 3; continue; }
+                    if (cls[u] == 3) {  // long, not decided by its first two blockers: look at the third
+                        if (!decided) stt[u] = 4 | (sx == 0 || sy == 0 ? 8u : 0u);  // bit 3: one of them is free
+                        continue;
+                    }
                     if (decided) continue;
                     if (sx > 0 && sy > 0) { stt[u] = 1; continue; }
                     const std::int32_t u1 = sx == 0 ? ent[u].z : ent[u].w;
                     if (may_assert(static_cast<std::uint32_t>(ent[u].y), -u1)) { stt[u] = 2; plit[u] = -u1; }
+                }
+                // long nogoods still open after two blockers: the third blocker
+                // (one more mirror lookup) settles most of them without a scan
+                {
+                    std::uint32_t wq[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) wq[u] = (stt[u] & 4u) ? mirror_word_snap(atom_of(ent[u].y)) : 0u;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        if (!(stt[u] & 4u)) continue;
+                        const int vq = mirror_val(wq[u], atom_of(ent[u].y));
+                        const bool dead = vq != 0 && ((vq > 0) != (ent[u].y > 0));
+                        const bool two_free = vq == 0 && (stt[u] & 8u);
+                        stt[u] = dead || two_free ? 0u : 3u;
+                    }
                 }
                 // An occurrence acts on its nogood (same outcome from any of
                 // them) unless an occurrence with a smaller e already claimed
@@ -1900,10 +1925,11 @@ struct Search {
         // by the whole warp, one at a time
         bool full = false;
         if (first && cls == 3) {
-            const int vx = val(atom_of(ent.z)), vy = val(atom_of(ent.w));
+            const int vx = val(atom_of(ent.z)), vy = val(atom_of(ent.w)), vq = val(atom_of(ent.y));
             const int sx = vx == 0 ? 0 : ((vx > 0) == (ent.z > 0) ? 1 : -1);
             const int sy = vy == 0 ? 0 : ((vy > 0) == (ent.w > 0) ? 1 : -1);
-            full = !(sx < 0 || sy < 0 || (sx == 0 && sy == 0));
+            const int sq = vq == 0 ? 0 : ((vq > 0) == (ent.y > 0) ? 1 : -1);
+            full = !(sx < 0 || sy < 0 || sq < 0 || (sx == 0) + (sy == 0) + (sq == 0) >= 2);
         }
         if (first && !full) evaluate_entry(ent, cls, trig, conflict, prop, plit, clen, &d0, &meta);
         for (unsigned need = __ballot_sync(0xffffffffu, full); need; need &= need - 1) {
@@ -2223,7 +2249,9 @@ struct Search {
             }
             const std::int32_t o0 = j == 0 ? (len > 1 ? lits[1] : 0) : lits[0];
             const std::int32_t o1 = j <= 1 ? (len > 2 ? lits[2] : 0) : lits[1];
-            sl.larena()[base + size] = make_int4(static_cast<std::int32_t>(id | cls << 30), static_cast<std::int32_t>(kNone), o0, o1);
+            const std::int32_t o2 = j <= 2 ? (len > 3 ? lits[3] : 0) : lits[2];  // long nogoods: a third blocker
+            sl.larena()[base + size] = make_int4(static_cast<std::int32_t>(id | cls << 30),
+                                                 cls == 3 ? o2 : static_cast<std::int32_t>(kNone), o0, o1);
             h3[1] = size + 1;
             sl.ltot()[li] += 1;
         }

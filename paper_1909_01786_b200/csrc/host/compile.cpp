@@ -403,14 +403,15 @@ StaticStore build_store(const NogoodSet& ns, AtomId total_atoms) {
             const std::uint32_t lo = st.off[id], hi = st.off[id + 1];
             const std::uint32_t cls = length_class(hi - lo);
             for (std::uint32_t at = lo; at < hi; ++at) {
-                std::int32_t other[2] = {0, 0};
-                for (std::uint32_t q = lo, m = 0; q < hi && m < 2; ++q)
+                std::int32_t other[3] = {0, 0, 0};
+                for (std::uint32_t q = lo, m = 0; q < hi && m < 3; ++q)
                     if (q != at) other[m++] = st.pool[q];
                 const std::uint32_t j = slot[at];
                 st.occ_ids[j] = static_cast<std::int32_t>(id);
                 std::int32_t* f = st.occ_fat.data() + 4ull * j;
                 f[0] = static_cast<std::int32_t>(static_cast<std::uint32_t>(id) | cls << 30);  // class in the top bits
-                f[1] = static_cast<std::int32_t>(st.guard[id]);
+                // binary / ternary: the truth guard; long: a third blocker (the guard is read when proposing)
+                f[1] = cls == 3 ? other[2] : static_cast<std::int32_t>(st.guard[id]);
                 f[2] = other[0];
                 f[3] = other[1];
             }

@@ -130,7 +130,9 @@ struct StaticStore {
     // Device copy of the occurrence lists: per (literal, nogood) one 16-byte
     // entry {id | length_class << 30, guard, x, y} with x, y two *other*
     // literals of the nogood (0 when absent), so binary/ternary nogoods are
-    // decided from the entry. Nogood ids therefore stay below 2^30.
+    // decided from the entry; a long nogood's entry carries a third other
+    // literal instead of the guard (three blockers: most long nogoods are
+    // decided without reading their literals). Nogood ids stay below 2^30.
     BigVec<std::int32_t> occ_fat;  // 4 ints per occurrence, same order as occ_ids
     std::array<std::uint32_t, 4> bounds{0, 0, 0, 0};
 

@@ -90,7 +90,8 @@ size_t yas_program_tp_step(const yas_program* p, const uint32_t* interp, size_t 
  * cube fixes (F a_0..F a_{i-1}, T a_i) or all F, so the (k+1)^depth cubes
  * partition the answer sets. depth 0 = smallest depth with >= want cubes.
  * Cube c runs on rank c % world. Each cube is width = depth*k unit-nogood
- * literals (0 = none): +a (":- a."), +b (":- b.", i.e. T a) or -a (":- not a."). Returns this
+ * literals (0 = none): +a (":- a."), +b (":- b.", i.e. T a) or -a (":- not a."). k = 0: the
+ * automatic split of a plain enumeration (ladders over at-least-one groups). Returns this
  * rank's cube count; host-only. */
 size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint32_t want, int rank, int world,
                          int32_t* out, size_t cap, uint32_t* width);
@@ -168,8 +169,10 @@ typedef struct yas_config {
     const int* devices;  /* n_devices CUDA ordinals (NULL: device, device + 1, ...); an ordinal may repeat */
     int reference_order; /* 1: an enumeration (max_models == 0) is one search with the reference's model
                             order and trajectory. 0 (default): a program with >= 16 even-loop choice pairs
-                            is enumerated as cubes (cube_atoms = 8) over the GPU(s); same answer sets and
-                            count, models in cube order (deterministic). Tracing forces the reference order. */
+                            is enumerated as cubes over the GPU(s) — ladders over its "at least one of"
+                            constraint groups (a queens row, a node's colours), else 8 pairs wide; same
+                            answer sets and count, models in cube order (deterministic). Tracing forces
+                            the reference order. */
     yas_fleet* fleet;    /* several processes share the enumeration / portfolio; overrides rank, world and
                             device (one GPU per process). Every rank calls yas_solve with the same program
                             and options; each returns the models its GPU found. */

@@ -179,9 +179,56 @@ std::vector<Choice> choice_atoms(const Program& prog) {
 }
 
 // Automatic split of a plain enumeration (max_models == 0, no cube_atoms):
-// programs with at least this many even-loop choice pairs, ladders this wide.
+// programs with at least this many even-loop choice pairs.
 constexpr std::size_t kAutoCubePairs = 16;
-constexpr std::uint32_t kAutoCubeWidth = 8;
+constexpr std::uint32_t kAutoCubeWidth = 8;  // ladder width without an at-least-one group
+
+// "At least one of these choices" groups: an integrity constraint whose body
+// only says "none of a_1..a_k is true" (each literal "not a_i", or the pair
+// partner b_i) — a queens row, the colours of a node. A ladder over one group
+// asks which member is its first true one; its last cube (none) fails at once,
+// so the cubes follow the problem's own structure. Groups come first in the
+// choice order (constraint order, atoms ascending, no atom twice); the ladder
+// width is the first group's size (0: no group).
+std::uint32_t group_choices(const Program& prog, std::vector<Choice>& ch) {
+    std::vector<std::int64_t> of_a(prog.atom_count() + 1, -1), of_b(prog.atom_count() + 1, -1);
+    for (std::size_t i = 0; i < ch.size(); ++i)
+        if (ch[i].b) {
+            of_a[ch[i].a] = static_cast<std::int64_t>(i);
+            of_b[ch[i].b] = static_cast<std::int64_t>(i);
+        }
+    std::vector<char> used(ch.size(), 0);
+    std::vector<Choice> order;
+    std::uint32_t width = 0;
+    for (const Rule& c : prog.constraints()) {
+        std::vector<std::size_t> g;
+        bool ok = c.pos_body.size() + c.neg_body.size() >= 2;
+        for (AtomId x : c.pos_body) {  // b_i true <=> a_i false
+            if (!ok) break;
+            ok = of_b[x] >= 0;
+            if (ok) g.push_back(static_cast<std::size_t>(of_b[x]));
+        }
+        for (AtomId x : c.neg_body) {  // not a_i
+            if (!ok) break;
+            ok = of_a[x] >= 0;
+            if (ok) g.push_back(static_cast<std::size_t>(of_a[x]));
+        }
+        if (!ok) continue;
+        std::sort(g.begin(), g.end());
+        if (std::adjacent_find(g.begin(), g.end()) != g.end()) continue;
+        if (std::any_of(g.begin(), g.end(), [&](std::size_t i) { return used[i]; })) continue;
+        if (!width) width = static_cast<std::uint32_t>(g.size());
+        for (std::size_t i : g) {
+            used[i] = 1;
+            order.push_back(ch[i]);
+        }
+    }
+    if (!width) return 0;
+    for (std::size_t i = 0; i < ch.size(); ++i)
+        if (!used[i]) order.push_back(ch[i]);
+    ch.swap(order);
+    return width;
+}
 
 bool first_choices_are_pairs(const Program& prog) {
     const std::vector<Choice> ch = choice_atoms(prog);
@@ -193,8 +240,12 @@ bool first_choices_are_pairs(const Program& prog) {
 // means all F. The (L+1)^d cubes partition the answer sets exactly. Cube c
 // belongs to rank c % world. Returns this rank's cube count.
 std::uint32_t make_cubes(const Program& prog, std::uint32_t L, std::uint32_t depth, std::uint32_t want, int rank,
-                         int world, std::vector<std::int32_t>& cubes, std::uint32_t& width) {
-    const std::vector<Choice> ch = choice_atoms(prog);
+                         int world, std::vector<std::int32_t>& cubes, std::uint32_t& width, bool grouped = false) {
+    std::vector<Choice> ch = choice_atoms(prog);
+    if (grouped) {  // automatic split: ladders over the at-least-one groups
+        const std::uint32_t g = group_choices(prog, ch);
+        L = g ? g : kAutoCubeWidth;
+    }
     cubes.clear();
     width = 0;
     if (world < 1) world = 1;
@@ -450,7 +501,7 @@ size_t yas_program_cubes(const yas_program* p, uint32_t k, uint32_t depth, uint3
     guarded(nullptr, 0, [&] {
         std::vector<std::int32_t> cubes;
         std::uint32_t w = 0;
-        n = make_cubes(p->prog, k, depth, want ? want : 2368, rank, world, cubes, w);
+        n = make_cubes(p->prog, k, depth, want ? want : 2368, rank, world, cubes, w, k == 0);
         if (width) *width = w;
         for (std::size_t i = 0; i < cubes.size() && out && i < cap; ++i) out[i] = cubes[i];
         return 0;
@@ -645,9 +696,12 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         // split into cubes unless the caller asked for the reference's model
         // order (or traces the reference's conflict sequence): the answer-set
         // set and count are the reference's, the order becomes cube order.
+        bool auto_cubes = false;
         if (cfg.cube_atoms == 0 && cfg.max_models == 0 && !cfg.reference_order && !cfg.trace &&
-            first_choices_are_pairs(prog))
-            cfg.cube_atoms = kAutoCubeWidth;
+            first_choices_are_pairs(prog)) {
+            cfg.cube_atoms = kAutoCubeWidth;  // the width itself comes from the program's groups
+            auto_cubes = true;
+        }
         const bool enumerate = cfg.cube_atoms > 0 && cfg.max_models == 0;
         const bool portfolio = cfg.portfolio > 1 && cfg.max_models == 1 && cfg.cube_atoms == 0;
         if (!enumerate && !portfolio) devs.resize(1);  // one search: the first GPU
@@ -674,7 +728,8 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             // one shared queue: every GPU gets the whole cube list; otherwise cube c
             // runs on GPU (rank * ndev + i) == c % gpus
             const int qrank = dynamic ? 0 : cfg.rank * static_cast<int>(ndev);
-            const std::uint32_t total = make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * gpus, 0, 1, cubes, width);
+            const std::uint32_t total =
+                make_cubes(prog, cfg.cube_atoms, cfg.cube_depth, 4 * slots_per_gpu * gpus, 0, 1, cubes, width, auto_cubes);
             for (std::uint32_t i = 0; i < ndev; ++i) {
                 DevRun& d = runs[i];
                 if (dynamic) {

@@ -162,6 +162,19 @@ def test_cubes_without_choice_pairs_use_rule_heads():
     assert A.cubes(q, 2, 1) == [[2, 0], [1, -3], [1, 3]]
 
 
+def test_automatic_cubes_follow_at_least_one_groups():
+    """k = 0: ladders over "at least one of" constraint groups (a queens row, a node's
+    colours): each level asks which member of a group is the first true one."""
+    q = Y.parse_program(I.queens(8))
+    auto = A.cubes(q, 0, 1)
+    assert len(auto) == 9 and auto == A.cubes(q, 8, 1)  # rows are already first, in atom order
+    col = Y.parse_program(I.colouring(30, 4.0, 3, 7))
+    c = A.cubes(col, 0, 2)
+    assert len(c) == 16 and len(c[0]) == 6  # three colours per node, two nodes deep
+    names = [[col.name(abs(x)) for x in cube if x] for cube in c]
+    assert {n.split("(")[1].split(",")[0] for cube in names for n in cube} == {"1", "2"}  # nodes 1 and 2
+
+
 # ---- invalid ids raise instead of aborting the host process (ADVICE r1) --------
 def test_tp_step_and_verify_reject_out_of_range_ids():
     p = Y.parse_program("a :- not b.\nb :- not a.\n")

@@ -499,13 +499,15 @@ def fleet(Y, rank, world, local):
 
 
 def enumeration(Y, I, rank, world, local, n=12):
-    """n-queens, all answer sets: ladder cubes over the choice atoms from one queue
-    shared by every GPU (SolverConfig.fleet); the model count comes from the
-    product's own all-reduce, time is the max over ranks."""
+    """n-queens, all answer sets through the unchanged reference call (max_models=0):
+    automatic ladder cubes from one queue shared by every GPU (SolverConfig.fleet);
+    the model count comes from the product's own all-reduce, time is the max over ranks."""
     from paper_1909_01786_b200 import aspine as A
     text = I.queens(n)
     fl = fleet(Y, rank, world, local)
-    cfg = Y.SolverConfig(max_models=0, cube_atoms=n, device=local, fleet=fl)
+    # the drop-in default: a plain enumeration (max_models=0) is cube-split automatically,
+    # ladders over the rows ("at least one queen per row" constraints)
+    cfg = Y.SolverConfig(max_models=0, device=local, fleet=fl)
     Y.solve(Y.parse_program(text), cfg)  # warm-up (module load, allocations)
     barrier(world)
     t = time.perf_counter()
@@ -543,7 +545,7 @@ def enumeration(Y, I, rank, world, local, n=12):
         else:
             # the same cube set on every host core (one reference process per core); the
             # full single-thread run (~3 min) is measured once by scripts/cpu_q12_reference.py
-            cubes_all = A.cubes(prog, n, 0, want=4 * 148 * 8 * world)
+            cubes_all = A.cubes(prog, 0, 0, want=4 * 148 * 8 * world)  # the same automatic cube set
             cs = cpu_cube_split(Y, text, cubes_all)
             cs["parity"] = cs["models"] == out["expected_models"] and (
                 cs["model_set_digest"] == pins()[f"queens{n}"]["model_set_digest"])

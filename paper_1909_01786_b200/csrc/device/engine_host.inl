@@ -9,8 +9,11 @@ namespace yas {
 namespace {
 
 constexpr int kBlockBS = 256;
-constexpr int kCubeBS = 128;  // cube enumeration with 8 searches per SM
-constexpr int kWarpBS = 32;   // cube enumeration with 16 single-warp searches per SM
+// Several searches per SM (cube enumeration, portfolios): two-warp CTAs — the
+// one-warp passes run in warp 0, larger passes and rule scans use both; at 8
+// per SM a search keeps 128 registers (q12 53.8 vs 55.5 ms for 4-warp CTAs
+// capped at 64 registers, which spilled; 16 one-warp searches: 55.1 ms).
+constexpr int kPairBS = 64;
 constexpr int kGridBS = 512;
 
 void ck(cudaError_t e, const char* what) {
@@ -276,10 +279,10 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     if (!opt.grid) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
-        per_sm = std::min<std::uint32_t>(16, (n_slots + sms - 1) / sms);
-        if (per_sm > 8) per_sm = 16;  // 16 searches per SM: one warp each
-        else if (per_sm > 6) per_sm = 8;  // 6 or 8 searches per SM: 128-thread CTAs
+        per_sm = std::min<std::uint32_t>(8, (n_slots + sms - 1) / sms);
+        if (per_sm > 6) per_sm = 8;  // several searches per SM: two-warp CTAs (64, 6 or 4 per SM)
         else if (per_sm > 4) per_sm = 6;
+        else if (per_sm > 1) per_sm = 4;
         // keep most of the unified L1 for the (read-only) static store
         std::size_t budget = per_sm == 1 ? 96u * 1024u : (227u * 1024u) / per_sm - 3072;
         if (const char* kb = std::getenv("YAS_SMEM_KB")) budget = std::min<std::size_t>(budget, std::strtoul(kb, nullptr, 10) * 1024u);
@@ -294,10 +297,9 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         // the rest of the 228 KB unified array stays L1 for the static store
         const int carve = static_cast<int>(std::min<std::size_t>(100, (per_sm * (smem + 4096) * 100 + 228 * 1024 - 1) / (228 * 1024)));
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 4>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 6>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kCubeBS, 8>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kWarpBS, 16>)}) {
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 4>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 6>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 8>)}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
@@ -313,14 +315,12 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, 0, nullptr),
                "grid launch");
         } else {
-            if (per_sm > 8)
-                dev::block_kernel<kWarpBS, 16><<<n_slots, kWarpBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
-            else if (per_sm > 6)
-                dev::block_kernel<kCubeBS, 8><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            if (per_sm > 6)
+                dev::block_kernel<kPairBS, 8><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else if (per_sm > 4)
-                dev::block_kernel<kCubeBS, 6><<<n_slots, kCubeBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+                dev::block_kernel<kPairBS, 6><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else if (per_sm > 1)
-                dev::block_kernel<kBlockBS, 4><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+                dev::block_kernel<kPairBS, 4><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             else
                 dev::block_kernel<kBlockBS, 1><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
             ck(cudaGetLastError(), "block launch");

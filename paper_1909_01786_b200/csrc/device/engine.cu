@@ -3216,9 +3216,13 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                            // already assigned atoms are left alone (agreed / conflict) and
                            // only the first occurrence of a repeated atom counts
             const std::uint32_t ts0 = c->ts, gen = c->gen;
-            if (g.leader() && op.deps)
-                for (std::uint32_t w = s.nwords(op.level); w < C.W; ++w)
-                    if (op.deps[w]) c->rows_wide = 1;
+            // Deps words an atom at this level can use; more only when the caller's
+            // words beyond them are not zero (then the next reset clears whole rows)
+            std::uint32_t nw = s.nwords(op.level);
+            if (op.deps)
+                for (std::uint32_t w = nw; w < C.W; ++w)
+                    if (op.deps[w]) nw = C.W;
+            if (g.leader() && nw == C.W && s.nwords(op.level) < C.W) c->rows_wide = 1;
             for (std::uint32_t k = g.tid(); k < op.n; k += g.size()) {
                 const std::uint32_t a = atom_of(op.lits[k]);
                 if (a != 0 && a <= S.A) atomicMin(sl.win() + a, wkey(gen, k, false));  // atoms outside [1, A] are ignored
@@ -3237,7 +3241,7 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                     sl.tpos()[a] = ts0 + r;
                     sl.trail()[ts0 + r] = lit;
                     sl.reason()[a] = op.antecedent;
-                    for (std::uint32_t w = 0; w < C.W; ++w) s.dep(w, a) = op.deps ? op.deps[w] : 0ull;
+                    for (std::uint32_t w = 0; w < nw; ++w) s.dep(w, a) = op.deps ? op.deps[w] : 0ull;  // the rest is zero
                     sl.dovf()[a] = static_cast<std::uint8_t>(op.ovf);
                 }
                 carry += tot;

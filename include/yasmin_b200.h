@@ -269,6 +269,9 @@ int yas_propagator_assign(yas_propagator* p, const int32_t* lits, size_t n, uint
                           const uint64_t* deps, uint32_t n_deps, int overflow, int32_t antecedent);
 int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n); /* Frontier::seed / last.push_back */
 int yas_propagator_clear_frontier(yas_propagator* p);                     /* Frontier::clear */
+/* Bytes this propagator has moved host->device (staged inputs, kernel arguments) and
+ * device->host (control blocks, read-backs) since it was created, counted at each copy. */
+int yas_propagator_transfers(const yas_propagator* p, uint64_t* h2d, uint64_t* d2h);
 /* NogoodStore::add_learned (nogood_store.cpp:81-107): the literals are
  * canonicalised like Nogood::make; returns the new id, or -1 for an empty or
  * vacuous set, a literal 0 or an atom above the store's total_atoms (message

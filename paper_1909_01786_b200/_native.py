@@ -34,7 +34,7 @@ EXPORTS = [
     "yas_propagator_last_error",
     "yas_fleet_unique_id", "yas_fleet_create_nccl", "yas_fleet_create", "yas_fleet_free", "yas_fleet_info",
     "yas_fleet_allreduce", "yas_program_create", "yas_program_intern", "yas_program_add_rule", "yas_store_nogood",
-    "yas_propagator_clear_frontier",
+    "yas_propagator_clear_frontier", "yas_propagator_transfers",
 ]
 
 
@@ -165,6 +165,7 @@ def lib() -> C.CDLL:
         "yas_propagator_pass_trace": (C.c_int, [P, C.c_int, C.POINTER(C.c_uint64), C.c_size_t, C.POINTER(U32)]),
         "yas_propagator_last_error": (SZ, [P, C.c_char_p, SZ]),
         "yas_propagator_clear_frontier": (C.c_int, [P]),
+        "yas_propagator_transfers": (C.c_int, [P, pU64, pU64]),
         "yas_program_create": (P, []),
         "yas_program_intern": (U32, [P, C.c_char_p]),
         "yas_program_add_rule": (C.c_int, [P, U32, pU32, SZ, pU32, SZ]),

@@ -794,6 +794,12 @@ class Propagator:
     def level(self) -> int:
         return N.lib().yas_propagator_level(self._h)
 
+    def transfers(self):
+        """(host->device, device->host) bytes moved by this propagator so far (counted)."""
+        a, b = C.c_uint64(0), C.c_uint64(0)
+        self._check(N.lib().yas_propagator_transfers(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def pass_trace(self, on: Optional[bool] = None):
         """Diagnostics: enable/disable (on) and read the per-pass, per-block
         phase timestamps of whole-grid propagations: array [64, blocks, 10]."""

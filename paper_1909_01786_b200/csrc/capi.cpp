@@ -1294,6 +1294,14 @@ int yas_propagator_seed(yas_propagator* p, const int32_t* lits, size_t n) {
     if (!p) return YAS_ERR_ARG;
     return guarded(p->err, sizeof p->err, [&] { p->s->seed(lits, n); return static_cast<int>(YAS_OK); });
 }
+int yas_propagator_transfers(const yas_propagator* p, uint64_t* h2d, uint64_t* d2h) {
+    if (!p) return YAS_ERR_ARG;
+    unsigned long long a = 0, b = 0;
+    p->s->transfers(a, b);
+    if (h2d) *h2d = a;
+    if (d2h) *d2h = b;
+    return YAS_OK;
+}
 int yas_propagator_clear_frontier(yas_propagator* p) {
     if (!p) return YAS_ERR_ARG;
     return guarded(p->err, sizeof p->err, [&] { p->s->clear_frontier(); return static_cast<int>(YAS_OK); });

@@ -97,6 +97,8 @@ public:
     std::vector<std::int32_t> conflicts() const;
     std::vector<std::int32_t> frontier() const;
     float last_ms() const { return last_ms_; }
+    // cumulative host->device / device->host bytes of this session (counted at every copy)
+    void transfers(unsigned long long& h2d, unsigned long long& d2h) const;
     std::uint32_t deps_words() const { return W_; }
 
     struct Impl;

@@ -459,6 +459,9 @@ struct Session::Impl {
     std::size_t h_uploaded = 0;  // prefix of this batch's staging already sent (bulk inputs go early)
     dev::Ctl* h_ctl = nullptr;  // pinned mirror of the slot's control block
     bool ctl_pending = false;
+    // bytes moved between host and device by this session (staged inputs, kernel
+    // arguments, control blocks, read-backs): counted, for end-to-end accounting
+    mutable unsigned long long h2d_bytes = 0, d2h_bytes = 0;
 
     std::size_t append(const void* src, std::size_t ints) {
         if (stage_inflight) {  // the previous batch's upload may still read the buffer
@@ -487,6 +490,7 @@ struct Session::Impl {
             ck(cudaMemcpyAsync(d_stage + h_uploaded, h_stage + h_uploaded, (h_used - h_uploaded) * sizeof(std::int32_t),
                                cudaMemcpyHostToDevice, stream),
                "stage");
+            h2d_bytes += (h_used - h_uploaded) * sizeof(std::int32_t);
             h_uploaded = h_used;
         }
         return off;
@@ -560,6 +564,7 @@ void flush_ops(Session::Impl& im, float* ms) {
             ck(cudaMemcpyAsync(im.d_stage + im.h_uploaded, im.h_stage + im.h_uploaded,
                                (im.h_used - im.h_uploaded) * sizeof(std::int32_t), cudaMemcpyHostToDevice, im.stream),
                "stage");
+        if (im.h_used > im.h_uploaded) im.h2d_bytes += (im.h_used - im.h_uploaded) * sizeof(std::int32_t);
         ck(cudaEventRecord(im.staged, im.stream), "record");
         im.stage_inflight = true;
     }
@@ -590,6 +595,8 @@ void flush_ops(Session::Impl& im, float* ms) {
     }
     ck(cudaEventRecord(im.e1, im.stream), "record");
     ck(cudaMemcpyAsync(im.h_ctl, im.ar.slots[0].ctl(), sizeof(dev::Ctl), cudaMemcpyDeviceToHost, im.stream), "ctl");
+    im.h2d_bytes += sizeof(dev::OpBatch);  // the recorded ops travel as kernel arguments
+    im.d2h_bytes += sizeof(dev::Ctl);
     im.ctl_pending = true;
     if (ms) {
         ck(cudaEventSynchronize(im.e1), "op kernel");
@@ -734,60 +741,66 @@ const dev::Ctl& Session::ctl() const {
 
 namespace {
 template <class T>
-std::size_t dl_into(const T* p, std::size_t n, T* out, cudaStream_t s) {
+std::size_t dl_into(const T* p, std::size_t n, T* out, cudaStream_t s, unsigned long long& counted) {
     if (n) {
         ck(cudaMemcpyAsync(out, p, n * sizeof(T), cudaMemcpyDeviceToHost, s), "download");
         ck(cudaStreamSynchronize(s), "download");
+        counted += n * sizeof(T);
     }
     return n;
 }
 template <class T>
-std::vector<T> dl(const T* p, std::size_t n, cudaStream_t s) {
+std::vector<T> dl(const T* p, std::size_t n, cudaStream_t s, unsigned long long& counted) {
     std::vector<T> v(n);
-    dl_into(p, n, v.data(), s);
+    dl_into(p, n, v.data(), s, counted);
     return v;
 }
 }  // namespace
 
+void Session::transfers(unsigned long long& h2d, unsigned long long& d2h) const {
+    h2d = impl_->h2d_bytes;
+    d2h = impl_->d2h_bytes;
+}
+
 std::size_t Session::trail_into(std::int32_t* out, std::size_t cap) const {
     const std::size_t n = ctl().ts;
-    if (out && cap >= n) dl_into(impl_->ar.slots[0].trail(), n, out, impl_->stream);
-    else if (out && cap) dl_into(impl_->ar.slots[0].trail(), cap, out, impl_->stream);
+    if (out && cap >= n) dl_into(impl_->ar.slots[0].trail(), n, out, impl_->stream, impl_->d2h_bytes);
+    else if (out && cap) dl_into(impl_->ar.slots[0].trail(), cap, out, impl_->stream, impl_->d2h_bytes);
     return n;
 }
 
 std::vector<std::int32_t> Session::cells() const {
     flush_ops(*impl_, nullptr);
-    return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1, impl_->stream);
+    return dl(impl_->ar.slots[0].cells(), impl_->ar.A + 1, impl_->stream, impl_->d2h_bytes);
 }
-std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts, impl_->stream); }
+std::vector<std::int32_t> Session::trail() const { return dl(impl_->ar.slots[0].trail(), ctl().ts, impl_->stream, impl_->d2h_bytes); }
 std::vector<std::int32_t> Session::reasons() const {
     flush_ops(*impl_, nullptr);
-    return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream);
+    return dl(impl_->ar.slots[0].reason(), impl_->ar.A + 1, impl_->stream, impl_->d2h_bytes);
 }
 std::vector<unsigned long long> Session::deps_word(std::uint32_t w) const {
     flush_ops(*impl_, nullptr);
     const std::size_t stride = (W_ + 1) & ~1u, n = impl_->ar.A + 1;
-    const std::vector<unsigned long long> rows = dl(impl_->ar.slots[0].deps(), n * stride, impl_->stream);
+    const std::vector<unsigned long long> rows = dl(impl_->ar.slots[0].deps(), n * stride, impl_->stream, impl_->d2h_bytes);
     std::vector<unsigned long long> v(n);
     for (std::size_t a = 0; a < n; ++a) v[a] = rows[a * stride + w];
     return v;
 }
 std::vector<std::uint8_t> Session::deps_overflow() const {
     flush_ops(*impl_, nullptr);
-    return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream);
+    return dl(impl_->ar.slots[0].dovf(), impl_->ar.A + 1, impl_->stream, impl_->d2h_bytes);
 }
-std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl, impl_->stream); }
+std::vector<std::int32_t> Session::conflicts() const { return dl(impl_->ar.slots[0].confl(), ctl().n_confl, impl_->stream, impl_->d2h_bytes); }
 std::vector<std::int32_t> Session::frontier() const {
     const dev::Ctl& c = ctl();
-    return dl(impl_->ar.slots[0].fr(c.cur), c.F, impl_->stream);
+    return dl(impl_->ar.slots[0].fr(c.cur), c.F, impl_->stream, impl_->d2h_bytes);
 }
 
 std::vector<unsigned long long> Session::pass_trace(std::uint32_t& blocks) const {
     blocks = std::max<std::uint32_t>(1, impl_->gblocks);
     if (!impl_->cfg.ptrace) return {};
     ctl();
-    return dl(impl_->cfg.ptrace, 64ull * blocks * 10 + 64 * 16, impl_->stream);
+    return dl(impl_->cfg.ptrace, 64ull * blocks * 10 + 64 * 16, impl_->stream, impl_->d2h_bytes);
 }
 
 }  // namespace yas

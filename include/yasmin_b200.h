@@ -154,7 +154,8 @@ typedef struct yas_config {
     /* device extensions */
     int device;          /* CUDA ordinal */
     int engine;          /* 0 auto, 1 one CTA per search, 2 whole-grid search */
-    uint32_t cube_atoms; /* enumeration split: ladder width k over choice atoms (0 = single search) */
+    uint32_t cube_atoms; /* enumeration split: ladder width k over choice atoms (0 = single search); with
+                            max_models >= 1, the first max_models answer sets found by any cube search */
     uint32_t cube_depth; /* ladder levels (0 = auto: enough cubes for every search slot) */
     uint32_t slots;      /* concurrent searches per GPU for cubes (0 = auto) */
     int rank, world;     /* cube partition across processes/GPUs: cube i runs on rank i % world */

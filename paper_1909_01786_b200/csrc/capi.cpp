@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <climits>
@@ -554,7 +555,8 @@ struct DevRun {
     std::exception_ptr error;
 };
 
-void run_device(DevRun& d, const EngineProgram& ep, const Program& prog, const yas_config& cfg, std::uint32_t width) {
+void run_device(DevRun& d, const EngineProgram& ep, const Program& prog, const yas_config& cfg, std::uint32_t width,
+                std::atomic<std::uint64_t>* found = nullptr) {
     try {
         d.ids.clear();
         d.offs.assign(1, 0);
@@ -577,7 +579,8 @@ void run_device(DevRun& d, const EngineProgram& ep, const Program& prog, const y
             }
             d.offs.push_back(d.ids.size());
             d.mcubes.push_back(m.cube);
-            return true;
+            // cube-parallel first models: stop this GPU's loop once enough arrived anywhere
+            return !found || found->fetch_add(1) + 1 < cfg.max_models;
         };
         if (cfg.trace)
             cb.on_trace = [&](std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj) {
@@ -622,7 +625,7 @@ bool local_fleet(LocalFleet& lf, const std::vector<int>& devs) {
 
 void reset_fleet_ctl(dev::Fleet* ctl, int device) {
     ck_cuda(cudaSetDevice(device), "cudaSetDevice");
-    const dev::Fleet init{0u, 0u, 0xffffffffu, 0u};
+    const dev::Fleet init{0u, 0u, 0xffffffffu, 0u};  // queue, stop, winner, found
     ck_cuda(cudaMemcpy(ctl, &init, sizeof init, cudaMemcpyHostToDevice), "fleet reset");
 }
 
@@ -702,7 +705,9 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
             cfg.cube_atoms = kAutoCubeWidth;  // the width itself comes from the program's groups
             auto_cubes = true;
         }
-        const bool enumerate = cfg.cube_atoms > 0 && cfg.max_models == 0;
+        // cube_atoms with max_models >= 1: cube-parallel search for the first
+        // max_models answer sets (any of them; an extra mode like the portfolio)
+        const bool enumerate = cfg.cube_atoms > 0;
         const bool portfolio = cfg.portfolio > 1 && cfg.max_models == 1 && cfg.cube_atoms == 0;
         if (!enumerate && !portfolio) devs.resize(1);  // one search: the first GPU
         const std::uint32_t ndev = static_cast<std::uint32_t>(devs.size());
@@ -788,11 +793,14 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                     fl->comm->allreduce(&b, 1, FleetComm::kMax);
                 }
             }
+            std::atomic<std::uint64_t> found{0};
+            std::atomic<std::uint64_t>* first_models = enumerate && cfg.max_models != 0 ? &found : nullptr;
             if (ndev == 1) {
-                run_device(runs[0], ep, prog, cfg, width);
+                run_device(runs[0], ep, prog, cfg, width, first_models);
             } else {
                 std::vector<std::thread> th;
-                for (DevRun& d : runs) th.emplace_back([&, dp = &d] { run_device(*dp, ep, prog, cfg, width); });
+                for (DevRun& d : runs)
+                    th.emplace_back([&, dp = &d] { run_device(*dp, ep, prog, cfg, width, first_models); });
                 for (std::thread& t : th) t.join();
             }
             lap("engine");
@@ -857,6 +865,11 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                 res->ids.swap(ids);
                 res->off.swap(off);
                 res->cubes.swap(cubes);
+            }
+            if (enumerate && cfg.max_models != 0 && res->count() > cfg.max_models) {  // first models: exactly max_models
+                res->off.resize(cfg.max_models + 1);
+                res->ids.resize(res->off.back());
+                res->cubes.resize(cfg.max_models);
             }
             if (fl && fl->comm) {  // the final all-reduce: models, fleet-wide errors, the portfolio winner
                 std::uint64_t sum[1] = {res->count()};

@@ -2800,6 +2800,13 @@ struct Search {
             c->n_mbuf = m + 1;
             c->st.models += 1;
             c->pad0 += 1;  // models of this search
+            if (C.cube_width && C.max_models != 0) {  // cube-parallel first models: enough found anywhere?
+                const std::uint32_t n = 1u + (C.fleet ? atomicAdd_system(&C.fleet->found, 1u) : atomicAdd(&sh->found, 1u));
+                if (n >= C.max_models) {
+                    sh->stop = 1;
+                    if (C.fleet) atomicExch_system(&C.fleet->stop, 1u);
+                }
+            }
         }
         g.sync();
     }
@@ -2951,7 +2958,8 @@ struct Search {
             if (g.leader()) {
                 // a portfolio search another GPU / process has beaten ends here
                 if constexpr (!G::kGrid)
-                    if (C.portfolio && C.fleet && *reinterpret_cast<volatile std::uint32_t*>(&C.fleet->stop)) {
+                    if ((C.portfolio || (C.cube_width && C.max_models != 0)) && C.fleet &&
+                        *reinterpret_cast<volatile std::uint32_t*>(&C.fleet->stop)) {
                         c->status = kDone;
                         c->phase = kFinished;
                     }

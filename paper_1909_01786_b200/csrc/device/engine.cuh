@@ -41,7 +41,7 @@ struct Fleet {
     std::uint32_t cube_next;  // next cube of the shared queue
     std::uint32_t stop;       // portfolio: a search finished, every other search ends
     std::uint32_t winner;     // portfolio: tag of the first finisher (~0 = none yet)
-    std::uint32_t pad;
+    std::uint32_t found;      // cube-parallel first models: models found so far by every search
 };
 
 struct Config {
@@ -205,7 +205,8 @@ struct Shared {  // global (all-slot) coordination
     std::uint32_t bar_count, bar_gen;
     unsigned long long t_start;
     std::uint32_t winner;  // portfolio on one GPU without a fleet: first finisher's tag (~0 = none)
-    std::uint32_t partial_pad[26];
+    std::uint32_t found;   // cube-parallel first models on one GPU without a fleet
+    std::uint32_t partial_pad[25];
     // grid barrier: block b publishes the epoch of the barrier it reached
     std::uint32_t arrive[1024];
 };

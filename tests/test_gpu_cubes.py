@@ -55,3 +55,22 @@ def test_corpus_generic_cubes_match_families():
         if got != sorted(prog["family"]) or len({tuple(m) for m in got}) != len(got):
             bad.append(prog["name"])
     assert not bad, bad[:10]
+
+
+def test_cube_parallel_first_models():
+    """cube_atoms with max_models >= 1: every cube searched in parallel, the first
+    max_models answer sets found anywhere are reported (an extra mode, like the
+    portfolio: answer sets of the program, not necessarily the reference's first)."""
+    for text in (I.hamiltonian(200, 1.0, 1), I.colouring(2000, 4.0, 3, 1)):
+        prog = Y.parse_program(text)
+        r = Y.solve(prog, Y.SolverConfig(max_models=1, cube_atoms=8))
+        assert r.status == Y.SolveStatus.sat and len(r.models) == 1 and Y.verify_model(prog, r.models[0])
+    q = Y.parse_program(I.queens(8))
+    r = Y.solve(q, Y.SolverConfig(max_models=3, cube_atoms=8))
+    ids = [tuple(m.atom_ids) for m in r.models]
+    assert len(ids) == 3 and len(set(ids)) == 3 and all(Y.verify_model(q, m) for m in r.models)
+    php = Y.parse_program(I.pigeonhole(5, 4))  # no answer set: every cube fails
+    r = Y.solve(php, Y.SolverConfig(max_models=1, cube_atoms=4))
+    assert r.status == Y.SolveStatus.unsat and not r.models
+    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=2, cube_atoms=8, devices=[0, 0]))
+    assert len(r.models) == 2

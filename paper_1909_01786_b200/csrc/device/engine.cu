@@ -299,6 +299,7 @@ struct GridG {
     }
 
     __device__ unsigned long long scan(unsigned long long v, unsigned long long& total) {
+        if (solo) return block_scan(v, total);
         const std::uint32_t w = threadIdx.x >> 5;
         unsigned long long inc = warp_incl_scan(v);
         if (lane_id() == 31) sbuf[w] = inc;
@@ -859,6 +860,7 @@ struct Search {
                 const std::int32_t lit = lat[wi * 32 + __ffs(b) - 1];
                 out[r] = lit;
                 sl.froff()[r] = o;
+                if constexpr (G::kGrid) sl.frb()[r] = __ldg(S.occ_off + lidx(lit) * 4);  // grid passes read it
                 if (r < fcap) {
                     sm.fr()[r] = lit;
                     sm.froff()[r] = o;
@@ -1734,13 +1736,6 @@ struct Search {
         return nconf;
     }
 
-    // Frontiers this small run in block 0 alone: a block barrier costs ~0.1 us,
-    // a grid barrier ~1.5 us, and one block covers them in one or two batches.
-#ifndef YAS_SOLO_T
-#define YAS_SOLO_T 0
-#endif
-    static constexpr std::uint32_t kSoloT = YAS_SOLO_T;  // measured (L2 flushed): 0 -> 0.288 ms, 512 -> 0.297, 2048 -> 0.311
-
     __device__ __forceinline__ bool propagate_grid(std::uint32_t level) {
         frontier_offsets();
         std::uint32_t F = c->F, T = c->T, gen = c->gen, cur = c->cur, ts = c->ts;
@@ -1751,10 +1746,38 @@ struct Search {
         bool violated = false;
         std::uint32_t pass = 0;
         while (F != 0) {
-            if (T <= kSoloT) {
+            if (T <= sm.tcap() && F + 1 <= sm.fcap()) {
+                // Narrow passes: block 0 alone runs the single-CTA pass with its
+                // working set in shared memory (claims / winners in hash tables, block
+                // barriers) while the other blocks wait at one grid barrier.
                 if (blockIdx.x == 0) {
                     g.solo = true;
-                    while (F != 0 && T <= kSoloT && !violated) violated = grid_pass(F, T, cur, gen, ts, level, dlev, learned, pass) != 0;
+                    const std::int32_t* fsrc = sl.fr(cur);
+                    for (std::uint32_t p = threadIdx.x; p < F; p += blockDim.x) {
+                        sm.fr()[p] = fsrc[p];
+                        sm.froff()[p] = sl.froff()[p];
+                    }
+                    if (threadIdx.x == 0) {
+                        sm.froff()[F] = T;
+                        c->F = F;
+                        c->T = T;
+                        c->cur = cur;
+                        c->gen = gen;
+                        c->ts = ts;
+                        c->n_props = 0;
+                        c->b[11] = 0;
+                    }
+                    __syncthreads();
+                    while (F != 0 && !violated && T <= sm.tcap() && F + 1 <= sm.fcap()) {
+                        pass_smem(F, T, cur, level);  // ends with a block barrier; the leader updated c
+                        F = c->F;
+                        T = c->T;
+                        cur = c->cur;
+                        violated = c->b[11] != 0;
+                        ++pass;
+                    }
+                    gen = c->gen;
+                    ts = c->ts;
                     g.solo = false;
                     if (threadIdx.x == 0) {
                         c->F = F;

@@ -227,6 +227,15 @@ dev::SmemCfg plan_smem(std::uint32_t atoms, std::size_t budget) {
     return dev::smem_layout(0, vwords);
 }
 
+// Whole-grid propagation hands passes of at most this many expansion entries to
+// block 0 alone, with the single-CTA pass's working set in shared memory
+// (YAS_GRID_SOLO_T overrides; 0 disables).
+dev::SmemCfg grid_smem() {
+    std::uint32_t t = 256;
+    if (const char* e = std::getenv("YAS_GRID_SOLO_T")) t = static_cast<std::uint32_t>(std::strtoul(e, nullptr, 10));
+    return dev::smem_layout(t, 0);
+}
+
 std::uint32_t grid_blocks_for(int device) {
     int sms = 0, per = 0;
     ck(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device), "attr");
@@ -276,6 +285,13 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     dev::SmemCfg smc{};
     std::size_t smem = 0;
     std::uint32_t per_sm = 1;
+    if (opt.grid) {
+        smc = grid_smem();
+        smem = smc.bytes;
+        ck(cudaFuncSetAttribute(reinterpret_cast<const void*>(dev::grid_kernel<kGridBS>),
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+           "smem attribute");
+    }
     if (!opt.grid) {
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, opt.device);
@@ -312,7 +328,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         if (opt.grid) {
             void* args[] = {&ar.S, &cfg, &ar.L, &ar.K, &ar.sh, &ar.partial, &ar.pd, &ar.pi, &smc};
             ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::grid_kernel<kGridBS>), dim3(gblocks),
-                                           dim3(kGridBS), args, 0, nullptr),
+                                           dim3(kGridBS), args, smem, nullptr),
                "grid launch");
         } else {
             if (per_sm > 6)
@@ -514,6 +530,12 @@ Session::Session(const StaticStore& store, std::uint32_t deps_words, bool grid, 
         ck(cudaFuncSetAttribute(dev::op_block_kernel<kBlockBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(impl_->smem)),
            "smem attribute");
+    } else {
+        impl_->smc = grid_smem();
+        impl_->smem = impl_->smc.bytes;
+        ck(cudaFuncSetAttribute(dev::op_grid_kernel<kGridBS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(impl_->smem)),
+           "smem attribute");
     }
     dev::Config& c = impl_->cfg;
     c.W = deps_words;
@@ -586,7 +608,7 @@ void flush_ops(Session::Impl& im, float* ms) {
         void* args[] = {&im.ar.S, &im.cfg, &im.ar.L, &im.ar.K, &im.ar.sh, &im.ar.partial, &im.ar.pd, &im.ar.pi, &b,
                         &im.smc};
         ck(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(dev::op_grid_kernel<kGridBS>), dim3(im.gblocks),
-                                       dim3(kGridBS), args, 0, im.stream),
+                                       dim3(kGridBS), args, im.smem, im.stream),
            "op grid launch");
     } else {
         dev::op_block_kernel<kBlockBS><<<1, kBlockBS, im.smem, im.stream>>>(im.ar.S, im.cfg, im.ar.L, im.ar.K, im.ar.sh,

@@ -55,17 +55,8 @@ __device__ __forceinline__ unsigned long long ckey(std::uint32_t gen, std::uint3
 // streamed once per pass (evict-first) while the claim words they hit at
 // random are reused across passes (evict-last); without the hints a wide pass
 // over a store larger than L2 pushes the claims out and every claim becomes
-// a DRAM read-modify-write.
-__device__ __forceinline__ unsigned long long l2_policy_first() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ unsigned long long l2_policy_last() {
-    unsigned long long p;
-    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
+// a DRAM read-modify-write. The policies are kernel parameters (Static), so
+// they are read from the constant bank at each use and hold no register.
 __device__ __forceinline__ int4 ld_stream(const int4* a, unsigned long long pol) {
 #ifdef YAS_NO_L2HINT
     return __ldg(a);
@@ -83,9 +74,18 @@ __device__ __forceinline__ unsigned long long atomic_min_keep(unsigned long long
     return atomicMin(a, v);
 #else
     unsigned long long old;
-    asm volatile("atom.global.min.L2::cache_hint.u64 %0, [%1], %2, %3;" : "=l"(old) : "l"(a), "l"(v), "l"(pol) : "memory");
+    // not volatile, no memory clobber: the claims are only read again after a
+    // barrier, so the atomics may be scheduled freely inside the batch
+    asm("atom.global.min.L2::cache_hint.u64 %0, [%1], %2, %3;" : "=l"(old) : "l"(a), "l"(v), "l"(pol));
     return old;
 #endif
+}
+__global__ void make_l2_policies(unsigned long long* out) {
+    unsigned long long f, l;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(f));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l));
+    out[0] = f;
+    out[1] = l;
 }
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
@@ -1307,7 +1307,6 @@ struct Search {
         const std::uint32_t per = (((T + nwarps - 1) / nwarps) + 31u) & ~31u;
         const unsigned long long start64 = static_cast<unsigned long long>(wid) * per;
         std::uint32_t checks = 0, lits = 0;
-        const unsigned long long pol_first = l2_policy_first(), pol_last = l2_policy_last();
         if (start64 < T) {
             const std::uint32_t start = static_cast<std::uint32_t>(start64);
             const std::uint32_t end = T - start < per ? T : start + per;
@@ -1367,7 +1366,9 @@ struct Search {
                     const std::uint32_t e = base + 32u * u + lane;
                     cls[u] = 0;
                     if (e >= end) ent[u] = make_int4(-1, 0, 0, 0);
-                    else if (!learned) ent[u] = decode(ld_stream(S.occ + fb[u] + (e - se[u]), pol_first), cls[u]);
+                    else if (!learned) ent[u] = decode(U == kExpandU ? ld_stream(S.occ + fb[u] + (e - se[u]), S.pol_first)
+                                                                    : __ldg(S.occ + fb[u] + (e - se[u])),
+                                                       cls[u]);
                     else ent[u] = occ_entry(lidx(trig[u]), e - se[u], learned, cls[u]);
                 }
                 if (base == start) { asm volatile("" ::"r"(ent[0].x)); dstamp(pass, 3); }
@@ -1375,7 +1376,8 @@ struct Search {
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
                     const std::uint32_t e = base + 32u * u + lane;
-                    old[u] = e < end ? atomic_min_keep(sl.claim() + ent[u].x, ckey(gen, e), pol_last) : ckey(gen, 0);
+                    old[u] = e < end ? (U == kExpandU ? atomic_min_keep(sl.claim() + ent[u].x, ckey(gen, e), S.pol_last)
+                                                      : atomicMin(sl.claim() + ent[u].x, ckey(gen, e))) : ckey(gen, 0);
                 }
                 std::uint32_t wx[U], wy[U];  // issued while the claims are in flight
 #pragma unroll

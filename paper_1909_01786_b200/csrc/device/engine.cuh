@@ -91,6 +91,9 @@ struct Static {
     const unsigned long long* rules8;
     const std::uint32_t* socc;
     const std::int32_t* cubes;     // n_cubes * cube_width nogood literals (0 = pad)
+    // L2 cache policies (createpolicy, made once on the device): evict-first
+    // for streamed occurrence entries, evict-last for claim words
+    unsigned long long pol_first, pol_last;
 };
 
 struct Stats {

@@ -60,6 +60,20 @@ std::uint32_t pow2_at_least(std::uint64_t x) {
 }
 
 // All device memory of one run: static store + S slots.
+// The createpolicy encodings of the expansion's two L2 policies, made once on
+// the current device.
+void l2_policies(unsigned long long& first, unsigned long long& last) {
+    unsigned long long* d = nullptr;
+    ck(cudaMalloc(&d, 2 * sizeof(unsigned long long)), "cudaMalloc");
+    dev::make_l2_policies<<<1, 1>>>(d);
+    unsigned long long h[2] = {0, 0};
+    const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    ck(e, "L2 policies");
+    first = h[0];
+    last = h[1];
+}
+
 struct Arena {
     std::vector<void*> owned;
     dev::Static S{};
@@ -80,6 +94,7 @@ struct Arena {
 
     void upload_static(const StaticStore& st, const std::vector<RuleRec>& rules, std::uint32_t n_prog,
                        const std::vector<std::int32_t>& cubes) {
+        l2_policies(S.pol_first, S.pol_last);
         S.A = st.total_atoms;
         S.n_prog = n_prog;
         S.N = st.size();
@@ -692,8 +707,13 @@ void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_
 void Session::seed(const std::int32_t* lits, std::size_t n) {
     const std::uint32_t A = impl_->ar.A;
     if (n > static_cast<std::size_t>(A) + 1) throw std::invalid_argument("seed: more literals than atoms");
-    for (std::size_t k = 0; k < n; ++k)
-        if (lits[k] == 0 || lit_atom(lits[k]) > A) throw std::invalid_argument("seed: literal out of range");
+    std::uint32_t bad = 0;  // branch-free so the check over a bulk frontier vectorises
+    for (std::size_t k = 0; k < n; ++k) {
+        const std::int32_t l = lits[k];
+        const std::uint32_t a = l < 0 ? 0u - static_cast<std::uint32_t>(l) : static_cast<std::uint32_t>(l);
+        bad |= (a - 1u) >= A ? 1u : 0u;  // atom 0 or above A
+    }
+    if (bad) throw std::invalid_argument("seed: literal out of range");
     dev::OpArgs op{};
     op.op = dev::kOpSeed;
     op.n = static_cast<std::uint32_t>(n);

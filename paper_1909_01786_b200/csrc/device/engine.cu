@@ -303,13 +303,14 @@ struct GridG {
     // block by thread 0 after the barrier, into shared memory (snap[0..1]):
     // all threads reading one global word would queue thousands of requests
     // on one L2 slice.
-    __device__ void sync_snap(const std::uint32_t* a, const std::uint32_t* b) {
+    __device__ void sync_snap(const std::uint32_t* a, const std::uint32_t* b, const std::uint32_t* d = nullptr) {
         __syncthreads();
         if (solo) {
             if (threadIdx.x == 0) {
                 __threadfence_block();
                 if (a) snap[0] = *reinterpret_cast<const volatile std::uint32_t*>(a);
                 if (b) snap[1] = *reinterpret_cast<const volatile std::uint32_t*>(b);
+                if (d) snap[2] = *reinterpret_cast<const volatile std::uint32_t*>(d);
             }
             __syncthreads();
             return;
@@ -326,6 +327,7 @@ struct GridG {
             __threadfence();
             if (a) snap[0] = *reinterpret_cast<const volatile std::uint32_t*>(a);
             if (b) snap[1] = *reinterpret_cast<const volatile std::uint32_t*>(b);
+            if (d) snap[2] = *reinterpret_cast<const volatile std::uint32_t*>(d);
         }
         __syncthreads();
     }
@@ -1740,26 +1742,54 @@ struct Search {
         stamp(pass, 2);
         stamp(pass, 3);
         stamp(pass, 4);
-        grid_select(level, dlev, np);
-        stamp(pass, 5);
-        g.sync_snap(&c->n_confl, nullptr);
-        stamp(pass, 6);
-        // final for this pass: no block bumps it before the pass barrier
-        const std::uint32_t nconf = g.snap[0];
-        std::uint32_t Fn = 0, Tn = 0;
+        std::uint32_t nconf = 0, Fn = 0, Tn = 0;
         const bool small = (T + 31) / 32 <= kBlockPlaceWords;
-        grid_place(T, cur ^ 1u, ts, Fn, Tn);
-        if (g.leader()) {
-            c->n_props = 0;  // every block read it before the select barrier
-            c->st.passes += 1;
-        }
-        stamp(pass, 7);
-        if (small) {
-            g.sync_snap(&c->F, &c->T);
+#ifdef YAS_NO_FUSED_SELECT
+        constexpr bool kFuse = false;
+#else
+        constexpr bool kFuse = true;
+#endif
+        if (kFuse && small && np <= static_cast<std::uint32_t>(G::kWarps * 32)) {
+            // few proposals: block 0 selects (one per thread) and places them
+            // with block barriers; the grid waits at the pass barrier
+            if (blockIdx.x == 0) {
+                g.solo = true;
+                grid_select(level, dlev, np);
+                stamp(pass, 5);
+                __syncthreads();  // select's writes (bitmap, occat, ...) seen by the block
+                stamp(pass, 6);
+                grid_place(T, cur ^ 1u, ts, Fn, Tn);
+                g.solo = false;
+                if (threadIdx.x == 0) {
+                    c->n_props = 0;
+                    c->st.passes += 1;
+                }
+            }
+            stamp(pass, 7);
+            g.sync_snap(&c->F, &c->T, &c->n_confl);
             Fn = g.snap[0];
             Tn = g.snap[1];
+            nconf = g.snap[2];
         } else {
-            g.sync();
+            grid_select(level, dlev, np);
+            stamp(pass, 5);
+            g.sync_snap(&c->n_confl, nullptr);
+            stamp(pass, 6);
+            // final for this pass: no block bumps it before the pass barrier
+            nconf = g.snap[0];
+            grid_place(T, cur ^ 1u, ts, Fn, Tn);
+            if (g.leader()) {
+                c->n_props = 0;  // every block read it before the select barrier
+                c->st.passes += 1;
+            }
+            stamp(pass, 7);
+            if (small) {
+                g.sync_snap(&c->F, &c->T);
+                Fn = g.snap[0];
+                Tn = g.snap[1];
+            } else {
+                g.sync();
+            }
         }
         stamp(pass, 8);
         if (C.ptrace && g.leader() && pass < kPtracePasses)

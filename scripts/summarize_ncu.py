@@ -48,6 +48,19 @@ def main():
                     agg[k] = agg.get(k, 0) + x
             except (ValueError, IndexError):
                 pass
+    # memory traffic per source line: the L2 sector columns of the source page
+    sec_cols = [i for i, x in enumerate(hdr) if "Sectors" in x or "Requests" in x]
+    sec_rows = []
+    for r in src[3:]:
+        if r and r[0]:
+            vals = {}
+            for i in sec_cols:
+                try:
+                    vals[hdr[i]] = float(r[i].replace(",", ""))
+                except (ValueError, IndexError):
+                    pass
+            if any(vals.values()):
+                sec_rows.append((r[0], r[1].strip()[:90], vals))
     tot = max(1, sum(x[0] for x in lines))
     with open(out + ".txt", "w") as f:
         f.write(f"kernel: {name}\nreport: {rep}\n\n")
@@ -58,6 +71,16 @@ def main():
         for s, ln, txt, st in sorted(lines, reverse=True)[:25]:
             top = ", ".join(f"{k}={x}" for k, x in sorted(st.items(), key=lambda y: -y[1])[:2])
             f.write(f"{s:7d} {100 * s / tot:5.1f}%  L{ln:>5}  {txt:100s}  [{top}]\n")
+        key = next((hdr[i] for i in sec_cols if hdr[i].startswith("L2 Theoretical Sectors Global")
+                    and "Excessive" not in hdr[i]), hdr[sec_cols[0]] if sec_cols else None)
+        if key:
+            tot_sec = max(1.0, sum(v.get(key, 0.0) for _, _, v in sec_rows))
+            f.write(f"\nsector columns on the source page: {[hdr[i] for i in sec_cols]}\n")
+            f.write(f"top source lines by '{key}' (total {tot_sec:.4g}):\n")
+            for ln, txt, v in sorted(sec_rows, key=lambda y: -y[2].get(key, 0.0))[:25]:
+                extra = ", ".join(f"{k.replace('L2 Theoretical Sectors ', '')}={x:.3g}" for k, x in v.items()
+                                  if x and k != key)[:120]
+                f.write(f"{v.get(key, 0.0):12.4g} {100 * v.get(key, 0.0) / tot_sec:5.1f}%  L{ln:>5}  {txt:90s}  [{extra}]\n")
     if "dram__bytes_read.sum" in metrics:
         def mb(x):
             val, unit = x

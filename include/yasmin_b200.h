@@ -172,8 +172,8 @@ typedef struct yas_config {
                             order and trajectory. 0 (default): a program with >= 16 even-loop choice pairs
                             is enumerated as cubes over the GPU(s) — ladders over its "at least one of"
                             constraint groups (a queens row, a node's colours), else 8 pairs wide; same
-                            answer sets and count, models in cube order (deterministic). Tracing forces
-                            the reference order. */
+                            answer sets and count, models in cube order (deterministic). Tracing, or
+                            engine 2 (one whole-GPU search at a time), keeps the reference order. */
     yas_fleet* fleet;    /* several processes share the enumeration / portfolio; overrides rank, world and
                             device (one GPU per process). Every rank calls yas_solve with the same program
                             and options; each returns the models its GPU found. */

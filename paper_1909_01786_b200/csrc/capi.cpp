@@ -699,8 +699,10 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
         // split into cubes unless the caller asked for the reference's model
         // order (or traces the reference's conflict sequence): the answer-set
         // set and count are the reference's, the order becomes cube order.
+        // Not on an explicitly requested whole-GPU engine: it runs one search
+        // at a time, so cubes would only run one after another.
         bool auto_cubes = false;
-        if (cfg.cube_atoms == 0 && cfg.max_models == 0 && !cfg.reference_order && !cfg.trace &&
+        if (cfg.cube_atoms == 0 && cfg.max_models == 0 && !cfg.reference_order && !cfg.trace && cfg.engine != 2 &&
             first_choices_are_pairs(prog)) {
             cfg.cube_atoms = kAutoCubeWidth;  // the width itself comes from the program's groups
             auto_cubes = true;

@@ -76,6 +76,15 @@ def test_plain_enumeration_is_cube_split_by_default():
     assert single.stats.cubes == 1 and [m.atom_ids for m in single.models] == golden("configs")["queens8/fwd/occ"]["models"]
 
 
+def test_grid_engine_enumeration_keeps_reference_order():
+    """engine="grid" runs one whole-GPU search at a time: max_models = 0 is not cube-split
+    there, and the models come in the reference's order (solver.cpp:216-246)."""
+    exp = golden("configs")["queens8/fwd/occ"]
+    r = Y.solve(Y.parse_program(I.queens(8)), Y.SolverConfig(max_models=0, engine="grid"))
+    assert r.stats.cubes == 1 and [m.atom_ids for m in r.models] == exp["models"]
+    assert not stats_diff(r.stats, exp["stats"])
+
+
 @pytest.mark.parametrize("name", ["colour2000", "ham200"])
 @pytest.mark.parametrize("engine", ["block", "grid"])
 def test_first_model_configs(name, engine):

@@ -129,9 +129,15 @@ __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long 
 // Groups
 // ---------------------------------------------------------------------------
 // Warp 0 of a CTA on its own: small passes run warp-synchronously.
+// LEAN (all groups): the search runs the default configuration only (fwd
+// learning, occurrence heuristic, no portfolio / trace / restarts / fanout /
+// validation / profiling), so that code is compiled out of the kernel and its
+// hot loop packs into fewer instruction-cache lines.
+template <bool LEAN = false>
 struct WarpG {
     static constexpr bool kBlock = false;
     static constexpr bool kGrid = false;
+    static constexpr bool kLean = LEAN;
     Ctl* c;
     __device__ std::uint32_t tid() const { return lane_id(); }
     __device__ std::uint32_t size() const { return 32; }
@@ -155,10 +161,11 @@ struct WarpG {
     }
 };
 
-template <int BS>
+template <int BS, bool LEAN = false>
 struct BlockG {
     static constexpr bool kBlock = true;
     static constexpr bool kGrid = false;
+    static constexpr bool kLean = LEAN;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     unsigned long long* sbuf;  // kWarps+2 words of shared scratch
@@ -243,6 +250,7 @@ template <int BS>
 struct GridG {
     static constexpr bool kBlock = false;
     static constexpr bool kGrid = true;
+    static constexpr bool kLean = false;
     static constexpr int kWarps = BS / 32;
     Ctl* c;
     Shared* sh;
@@ -662,13 +670,18 @@ struct Search {
     }
     // learning mode / heuristic of this search (a portfolio varies them per search)
     __device__ __forceinline__ std::uint32_t mode() const {
+        if constexpr (G::kLean) return 0u;
         if constexpr (G::kGrid) return C.mode;  // a portfolio runs single-CTA searches
         return C.portfolio ? (c->variant & 1u) : C.mode;
     }
     __device__ __forceinline__ std::uint32_t heur() const {
+        if constexpr (G::kLean) return 0u;
         if constexpr (G::kGrid) return C.heur;
         return C.portfolio ? (c->variant >> 1) : C.heur;
     }
+    __device__ __forceinline__ bool prof_on() const { return !G::kLean && C.phase_prof; }
+    __device__ __forceinline__ bool trace_on() const { return !G::kLean && C.trace; }
+    __device__ __forceinline__ bool portfolio_on() const { return !G::kLean && C.portfolio; }
     __device__ __forceinline__ std::uint32_t nwords(std::uint32_t level) const {
         const std::uint32_t nw = level <= 1 ? 1u : (level - 1) / 64 + 1;
         return nw < C.W ? nw : C.W;
@@ -729,7 +742,7 @@ struct Search {
     // phase accounting: cycles since the previous mark go to bucket k
     __device__ __forceinline__ void mark(int k) const {
         if constexpr (G::kGrid) return;  // grid passes: see stamp()
-        if (C.phase_prof && g.leader()) {
+        if (prof_on() && g.leader()) {
             const unsigned long long t = clock64();
             c->prof[k] += t - c->prof_t;
             c->prof_t = t;
@@ -741,7 +754,7 @@ struct Search {
     __device__ __forceinline__ void tprof(int k) const {
 #ifdef YAS_TINY_PROF
         __syncwarp();
-        if (C.phase_prof && lane_id() == 0) {
+        if (prof_on() && lane_id() == 0) {
             const unsigned long long t = clock64();
             c->prof[k] += t - c->prof_t;
             c->prof_t = t;
@@ -1907,8 +1920,8 @@ struct Search {
             if constexpr (G::kBlock) {
                 if (T <= C.warp_pass_t && T <= sm.tcap() && F + 1 <= sm.fcap()) {
                     if (threadIdx.x < 32) {
-                        WarpG wg{c};
-                        Search<WarpG> ws(wg, S, C, sl, K, sh, t0, sm);
+                        WarpG<G::kLean> wg{c};
+                        Search<WarpG<G::kLean>> ws(wg, S, C, sl, K, sh, t0, sm);
                         ws.small_passes(level);
                     }
                     g.sync();
@@ -1916,7 +1929,7 @@ struct Search {
                 }
             }
             const bool in_smem = sm.tcap() && T <= sm.tcap() && F + 1 <= sm.fcap();
-            if (C.phase_prof && g.leader()) c->prof[in_smem ? 12 : 13] += 1;  // pass counts by path
+            if (prof_on() && g.leader()) c->prof[in_smem ? 12 : 13] += 1;  // pass counts by path
             if (in_smem) pass_smem(F, T, cur, level);
             else pass_global(F, T, gen, cur, level);
         }
@@ -1932,7 +1945,7 @@ struct Search {
             if (T <= 32) {
                 tiny_pass(F, T, cur, level);
                 mark(8);
-                if (C.phase_prof && threadIdx.x == 0) c->prof[10] += 1;
+                if (prof_on() && threadIdx.x == 0) c->prof[10] += 1;
             } else {
                 pass_smem(F, T, cur, level);
                 mark(9);
@@ -2043,7 +2056,7 @@ struct Search {
 #ifdef YAS_TINY_PROF
         {
             const unsigned nf = __popc(__ballot_sync(0xffffffffu, full)), ni = __popc(__ballot_sync(0xffffffffu, first));
-            if (C.phase_prof && lane == 0) {
+            if (prof_on() && lane == 0) {
                 c->prof[14] += nf;
                 c->prof[15] += ni;
             }
@@ -2568,7 +2581,7 @@ struct Search {
         if (c->cdl == 1) return;  // nothing to revise
         const std::uint32_t nc = c->n_confl;
         // select conflicts: min (length, id); fanout K in fwd mode (learn.cpp:148-157)
-        const std::uint32_t K2 = (mode() == 0 && C.fanout > 1) ? C.fanout : 1u;
+        const std::uint32_t K2 = (!G::kLean && mode() == 0 && C.fanout > 1) ? C.fanout : 1u;
         std::int32_t* added = sl.scratch();            // ids of added nogoods
         std::int32_t* levels = sl.scratch() + 64;      // their backjump levels
         std::int32_t* buf = sl.scratch() + 128;        // learned literal buffer
@@ -2630,7 +2643,7 @@ struct Search {
                 levels[n_sel] = static_cast<std::int32_t>(target);
                 c->st.learned_count += 1;
                 c->st.learned_length_sum += n;
-                if (C.trace && c->n_trace < K.tcap)
+                if (trace_on() && c->n_trace < K.tcap)
                     sl.tbuf()[c->n_trace++] = make_uint4(used, static_cast<std::uint32_t>(delta), n, target);
             }
             ++n_sel;
@@ -2646,7 +2659,7 @@ struct Search {
             if (lane == 0) c->act_inc = inc > 1e100 ? inc * 1e-100 : inc;
         }
         if (lane == 0) {
-            const bool restart = C.restarts && c->st.conflicts - c->conflicts_at_restart >= c->restart_threshold;
+            const bool restart = !G::kLean && C.restarts && c->st.conflicts - c->conflicts_at_restart >= c->restart_threshold;
             if (restart) {
                 c->st.restarts += 1;
                 c->conflicts_at_restart = c->st.conflicts;
@@ -2976,7 +2989,7 @@ struct Search {
         }
         std::uint32_t var = C.mode | C.heur << 1;
         if constexpr (!G::kGrid)
-            if (C.portfolio) var = (C.pf_base + cube) % 6u;
+            if (portfolio_on()) var = (C.pf_base + cube) % 6u;
         if ((var >> 1) == 2)
             for (std::uint32_t i = g.tid(); i <= S.A; i += g.size()) sl.act()[i] = 0.0;
         g.sync();
@@ -3050,13 +3063,13 @@ struct Search {
             if (g.leader()) {
                 // a portfolio search another GPU / process has beaten ends here
                 if constexpr (!G::kGrid)
-                    if ((C.portfolio || (C.cube_width && C.max_models != 0)) && C.fleet &&
+                    if ((portfolio_on() || (C.cube_width && C.max_models != 0)) && C.fleet &&
                         *reinterpret_cast<volatile std::uint32_t*>(&C.fleet->stop)) {
                         c->status = kDone;
                         c->phase = kFinished;
                     }
                 bool y = sh->stop != 0;
-                if (c->n_mbuf >= K.mcap || (C.trace && c->n_trace + 64 > K.tcap)) {
+                if (c->n_mbuf >= K.mcap || (trace_on() && c->n_trace + 64 > K.tcap)) {
                     y = true;
                     sh->stop = 1;
                 }
@@ -3100,7 +3113,7 @@ struct Search {
                 }
                 continue;
             }
-            if (C.debug_validate) {
+            if (!G::kLean && C.debug_validate) {
                 validate();
                 if (c->status != kRunning) return;
             }
@@ -3144,7 +3157,7 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
     for (;;) {
         g.sync();
         if (g.c->status != kRunning) return;
-        if (!G::kGrid && C.portfolio && g.c->phase == kFinished) {  // first to finish: stop the others
+        if (!G::kGrid && !G::kLean && C.portfolio && g.c->phase == kFinished) {  // first to finish: stop the others
             if (g.leader()) {
                 g.c->done_ns = gtimer();
                 const std::uint32_t tag = C.fleet_tag + blockIdx.x;
@@ -3181,7 +3194,7 @@ __device__ void slot_loop(G& g, const Static& S, const Config& C, Slot sl, const
 
 // One CTA per search slot; slot k = blockIdx.x. MINB = resident CTAs per SM the
 // register budget is planned for (1: single search, 4: cube enumeration).
-template <int BS, int MINB>
+template <int BS, int MINB, bool LEAN = false>
 __global__ void __launch_bounds__(BS, MINB)
     block_kernel(const __grid_constant__ Static S, const __grid_constant__ Config C,
                  const __grid_constant__ SlotLayout L, const __grid_constant__ Caps K, Shared* sh,
@@ -3201,7 +3214,7 @@ __global__ void __launch_bounds__(BS, MINB)
         }
     }
     __syncthreads();
-    BlockG<BS> g{&ctl, sbuf, sd, si};
+    BlockG<BS, LEAN> g{&ctl, sbuf, sd, si};
     slot_loop(g, S, C, sl, K, sh, Sm{&smc});
     __syncthreads();
     {

@@ -267,6 +267,19 @@ std::string device_name(int device) {
     return p.name;
 }
 
+template <bool LEAN>
+void launch_blocks(std::uint32_t per_sm, std::uint32_t n_slots, std::size_t smem, Arena& ar, const dev::Config& cfg,
+                   const dev::SmemCfg& smc) {
+    if (per_sm > 6)
+        dev::block_kernel<kPairBS, 8, LEAN><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+    else if (per_sm > 4)
+        dev::block_kernel<kPairBS, 6, LEAN><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+    else if (per_sm > 1)
+        dev::block_kernel<kPairBS, 4, LEAN><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+    else
+        dev::block_kernel<kBlockBS, 1, LEAN><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+}
+
 EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, const EngineOptions& opt,
                           const std::vector<std::int32_t>& cubes, std::uint32_t n_cubes,
                           std::uint32_t cube_width, const EngineCallbacks& cb) {
@@ -330,12 +343,20 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         for (auto fn : {reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1>),
                         reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 4>),
                         reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 6>),
-                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 8>)}) {
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 8>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kBlockBS, 1, true>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 4, true>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 6, true>),
+                        reinterpret_cast<const void*>(dev::block_kernel<kPairBS, 8, true>)}) {
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
                "smem attribute");
             ck(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carve), "carveout");
         }
     }
+    // the default configuration runs on kernels with everything else compiled out
+    bool lean = cfg.mode == 0 && cfg.heur == 0 && !cfg.portfolio && !cfg.trace && !cfg.debug_validate &&
+                !cfg.phase_prof && cfg.fanout <= 1 && !cfg.restarts;
+    if (const char* e = std::getenv("YAS_LEAN")) lean = lean && std::strtoul(e, nullptr, 10) != 0;
     bool stop_early = false;
     std::uint32_t winner = ~0u;  // portfolio: the search that finished first
     for (;;) {
@@ -346,14 +367,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                                            dim3(kGridBS), args, smem, nullptr),
                "grid launch");
         } else {
-            if (per_sm > 6)
-                dev::block_kernel<kPairBS, 8><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
-            else if (per_sm > 4)
-                dev::block_kernel<kPairBS, 6><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
-            else if (per_sm > 1)
-                dev::block_kernel<kPairBS, 4><<<n_slots, kPairBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
-            else
-                dev::block_kernel<kBlockBS, 1><<<n_slots, kBlockBS, smem>>>(ar.S, cfg, ar.L, ar.K, ar.sh, smc);
+            if (lean) launch_blocks<true>(per_sm, n_slots, smem, ar, cfg, smc);
+            else launch_blocks<false>(per_sm, n_slots, smem, ar, cfg, smc);
             ck(cudaGetLastError(), "block launch");
         }
         ck(cudaEventRecord(e1), "record");

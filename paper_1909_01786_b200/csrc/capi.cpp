@@ -564,23 +564,36 @@ void run_device(DevRun& d, const EngineProgram& ep, const Program& prog, const y
         d.traces.clear();
         EngineCallbacks cb;
         const std::uint32_t np = prog.atom_count();
-        cb.on_model = [&](const EngineModel& m) {
-            const std::size_t at = d.ids.size();
-            for (std::size_t w = 0; w < m.bits.size(); ++w)
-                for (std::uint32_t b = m.bits[w]; b; b &= b - 1) {
-                    const std::uint32_t a = static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
-                    if (a <= np) d.ids.push_back(a);
+        // every slot's models of one drain, in slot order
+        cb.on_models = [&](const EngineDrain& dr) {
+            std::uint64_t total = 0;
+            for (std::uint32_t s = 0; s < dr.n_slots; ++s) total += dr.counts[s];
+            if (total == 0) return true;
+            d.offs.reserve(d.offs.size() + total);
+            d.mcubes.reserve(d.mcubes.size() + total);
+            for (std::uint32_t s = 0; s < dr.n_slots; ++s)
+                for (std::uint32_t m = 0; m < dr.counts[s]; ++m) {
+                    const std::size_t k = static_cast<std::size_t>(s) * dr.stride + m;
+                    const std::uint32_t* bits = dr.bits + k * dr.nwords;
+                    const std::size_t at = d.ids.size();
+                    for (std::size_t w = 0; w < dr.nwords; ++w)
+                        for (std::uint32_t b = bits[w]; b; b &= b - 1) {
+                            const std::uint32_t a =
+                                static_cast<std::uint32_t>(32 * w) + static_cast<std::uint32_t>(__builtin_ctz(b)) + 1;
+                            if (a <= np) d.ids.push_back(a);
+                        }
+                    if (cfg.verify) {
+                        // record_model's checks (solver.cpp:221-229)
+                        const std::vector<std::uint32_t> ids(d.ids.begin() + static_cast<std::ptrdiff_t>(at), d.ids.end());
+                        if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
+                        if (tp_step(prog, ids) != ids)
+                            throw VerifyError("computed model is not a fixpoint of the consequence operator");
+                    }
+                    d.offs.push_back(d.ids.size());
+                    d.mcubes.push_back(dr.cubes[k]);
                 }
-            if (cfg.verify) {
-                // record_model's checks (solver.cpp:221-229)
-                const std::vector<std::uint32_t> ids(d.ids.begin() + static_cast<std::ptrdiff_t>(at), d.ids.end());
-                if (!is_answer_set(prog, ids)) throw VerifyError("computed model is not an answer set");
-                if (tp_step(prog, ids) != ids) throw VerifyError("computed model is not a fixpoint of the consequence operator");
-            }
-            d.offs.push_back(d.ids.size());
-            d.mcubes.push_back(m.cube);
             // cube-parallel first models: stop this GPU's loop once enough arrived anywhere
-            return !found || found->fetch_add(1) + 1 < cfg.max_models;
+            return !found || found->fetch_add(total) + total < cfg.max_models;
         };
         if (cfg.trace)
             cb.on_trace = [&](std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj) {
@@ -846,28 +859,33 @@ int yas_solve(const yas_program* p, const yas_config* cfg_in, yas_result** out, 
                 res->cubes.insert(res->cubes.end(), d.mcubes.begin(), d.mcubes.end());
                 traces.insert(traces.end(), d.traces.begin(), d.traces.end());
             }
+            lap("merged");
             if (enumerate && res->count() > 1) {  // cube order: the same for any scheduling of the cubes
+                // stable counting sort by cube
                 const std::size_t n = res->count();
+                std::uint32_t maxc = 0;
+                for (std::uint32_t cu : res->cubes) maxc = std::max(maxc, cu);
+                std::vector<std::uint64_t> start(static_cast<std::size_t>(maxc) + 2, 0);
+                for (std::uint32_t cu : res->cubes) ++start[static_cast<std::size_t>(cu) + 1];
+                for (std::size_t k = 1; k < start.size(); ++k) start[k] += start[k - 1];
                 std::vector<std::uint32_t> ord(n);
-                for (std::uint32_t m = 0; m < n; ++m) ord[m] = m;
-                std::stable_sort(ord.begin(), ord.end(),
-                                 [&](std::uint32_t a, std::uint32_t b) { return res->cubes[a] < res->cubes[b]; });
-                std::vector<std::uint32_t> ids;
-                std::vector<std::uint64_t> off{0};
-                std::vector<std::uint32_t> cubes;
-                ids.reserve(res->ids.size());
-                off.reserve(n + 1);
-                cubes.reserve(n);
-                for (std::uint32_t m : ord) {
-                    ids.insert(ids.end(), res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[m]),
-                               res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[m + 1]));
-                    off.push_back(ids.size());
-                    cubes.push_back(res->cubes[m]);
+                for (std::uint32_t m = 0; m < n; ++m) ord[start[res->cubes[m]]++] = m;
+                std::vector<std::uint64_t> off(n + 1, 0);
+                std::vector<std::uint32_t> cubes(n);
+                for (std::size_t i = 0; i < n; ++i) {
+                    off[i + 1] = off[i] + (res->off[ord[i] + 1] - res->off[ord[i]]);
+                    cubes[i] = res->cubes[ord[i]];
                 }
+                std::vector<std::uint32_t> ids(off[n]);
+                for (std::size_t i = 0; i < n; ++i)
+                    std::copy(res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[ord[i]]),
+                              res->ids.begin() + static_cast<std::ptrdiff_t>(res->off[ord[i] + 1]),
+                              ids.begin() + static_cast<std::ptrdiff_t>(off[i]));
                 res->ids.swap(ids);
                 res->off.swap(off);
                 res->cubes.swap(cubes);
             }
+            lap("cube order");
             if (enumerate && cfg.max_models != 0 && res->count() > cfg.max_models) {  // first models: exactly max_models
                 res->off.resize(cfg.max_models + 1);
                 res->ids.resize(res->off.back());

@@ -35,9 +35,15 @@ struct EngineOptions {
     std::uint32_t fleet_tag = 0;     // portfolio claim tag base of this GPU
 };
 
-struct EngineModel {
-    std::vector<std::uint32_t> bits;  // bit (a-1) set <=> program atom a true
-    std::uint32_t cube = 0;
+// The answer sets every slot buffered since the last drain (valid during the
+// callback only): model m of slot s is the bitset bits + (s * stride + m) * nwords
+// (bit a-1 set <=> program atom a true), found in cube cubes[s * stride + m].
+struct EngineDrain {
+    const std::uint32_t* bits = nullptr;
+    const std::uint32_t* cubes = nullptr;
+    const std::uint32_t* counts = nullptr;  // models per slot (0 for a slot that does not report)
+    std::uint32_t n_slots = 0, stride = 0;
+    std::size_t nwords = 0;
 };
 
 struct EngineResult {
@@ -51,7 +57,7 @@ struct EngineResult {
 };
 
 struct EngineCallbacks {
-    std::function<bool(const EngineModel&)> on_model;  // return false to stop early
+    std::function<bool(const EngineDrain&)> on_models;  // return false to stop early
     std::function<void(std::uint32_t mode, std::int32_t conflict, std::uint32_t len, std::uint32_t bj)> on_trace;
 };
 

@@ -309,7 +309,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e1), "event");
     std::vector<dev::Ctl> ctl(n_slots);
-    std::vector<std::uint32_t> mb, mc;
+    std::vector<std::uint32_t> mb, mc, counts;
     dev::SmemCfg smc{};
     std::size_t smem = 0;
     std::uint32_t per_sm = 1;
@@ -390,7 +390,6 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         lap("ctl copied");
         bool more = false;
         std::uint32_t err = dev::kDone;
-        EngineModel em;  // reused: one allocation for all delivered models
         // all slots' model buffers in two strided copies (not two per slot)
         std::uint32_t maxm = 0;
         for (std::uint32_t s = 0; s < n_slots; ++s) maxm = std::max(maxm, ctl[s].n_mbuf);
@@ -411,19 +410,22 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
             for (std::uint32_t s = 0; s < n_slots; ++s)
                 if (ctl[s].status == dev::kDone && ctl[s].won) winner = s;
         lap("models copied");
+        if (maxm) {  // one drain for every slot's models (decoded on the host threads)
+            counts.assign(n_slots, 0u);
+            for (std::uint32_t s = 0; s < n_slots; ++s)
+                if (!(cfg.portfolio && s != winner)) counts[s] = ctl[s].n_mbuf;
+            EngineDrain dr;
+            dr.bits = mb.data();
+            dr.cubes = mc.data();
+            dr.counts = counts.data();
+            dr.n_slots = n_slots;
+            dr.stride = maxm;
+            dr.nwords = ar.K.mwords;
+            if (cb.on_models && !cb.on_models(dr)) stop_early = true;
+        }
         for (std::uint32_t s = 0; s < n_slots; ++s) {
             dev::Ctl& c = ctl[s];
-            if (cfg.portfolio && s != winner) c.n_mbuf = 0;
-            if (c.n_mbuf) {
-                const std::size_t b0 = static_cast<std::size_t>(s) * maxm * ar.K.mwords;
-                for (std::uint32_t m = 0; m < c.n_mbuf && !stop_early; ++m) {
-                    em.bits.assign(mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m) * ar.K.mwords),
-                                   mb.begin() + static_cast<std::ptrdiff_t>(b0 + static_cast<std::size_t>(m + 1) * ar.K.mwords));
-                    em.cube = mc[static_cast<std::size_t>(s) * maxm + m];
-                    if (cb.on_model && !cb.on_model(em)) stop_early = true;
-                }
-                c.n_mbuf = 0;
-            }
+            c.n_mbuf = 0;
             if (c.n_trace) {
                 std::vector<uint4> tb(c.n_trace);
                 ck(cudaMemcpy(tb.data(), ar.slots[s].tbuf(), tb.size() * sizeof(uint4), cudaMemcpyDeviceToHost), "trace");
@@ -461,6 +463,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     }
     res.stats = tot;
     if (std::getenv("YAS_PROFILE")) {
+        std::fprintf(stderr, "[yas host]   engine end at %.2f ms\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count());
         static const char* names[16] = {"loop", "offsets", "expand", "resolve", "apply", "compact", "decide",
                                         "conflict", "tiny", "warp", "n.tiny", "looptop", "n.smem", "n.global", "x14", "x15"};
         unsigned long long p[16] = {0};

@@ -3144,8 +3144,7 @@ __device__ void init_smem(G& g, Search<G>& s) {
         for (std::uint32_t i = g.tid(); i < (m.tcap() + 31) / 32; i += g.size()) m.bits()[i] = 0u;
     }
     s.rebuild_mirror();
-    if constexpr (G::kGrid) __syncthreads();  // block-local tables: no grid barrier needed
-    else g.sync();
+    g.sync();
 }
 
 template <class G>
@@ -3360,8 +3359,7 @@ __device__ void do_op(G& g, const Static& S, const Config& C, Slot sl, const Cap
                 }
                 carry += tot;
             }
-            // every thread took ts0 and gen at the start: the leader may move them
-            // on without waiting for the others (the op-ending barrier publishes them)
+            g.sync();
             if (g.leader()) {
                 c->ts = ts0 + static_cast<std::uint32_t>(carry);
                 c->gen = gen + 1;

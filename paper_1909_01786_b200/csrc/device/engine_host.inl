@@ -1,6 +1,7 @@
 // Host side of the engine: uploads, per-slot arenas, the launch/drain loop.
 // Included at the end of engine.cu (needs the kernel templates).
 #include <chrono>
+#include <mutex>
 #include <cstddef>
 #include <cstdlib>
 
@@ -60,9 +61,46 @@ std::uint32_t pow2_at_least(std::uint64_t x) {
 }
 
 // All device memory of one run: static store + S slots.
-// The createpolicy encodings of the expansion's two L2 policies, made once on
-// the current device.
+// Pinned host staging for the drained models, grown on demand and kept by the
+// host thread across calls (first-touch page faults of a fresh pageable buffer
+// cost milliseconds per enumeration).
+struct HostBuf {
+    std::uint32_t* p = nullptr;
+    std::size_t cap = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    void reserve(std::size_t words) {
+        if (words <= cap) return;
+        const std::size_t ncap = std::max<std::size_t>(words, 2 * cap);
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        cap = 0;
+        ck(cudaMallocHost(&p, ncap * sizeof(std::uint32_t)), "cudaMallocHost models");
+        cap = ncap;
+    }
+    std::uint32_t* data() const { return p; }
+};
+HostBuf& host_models_buf() {
+    thread_local HostBuf b;
+    return b;
+}
+
+// The createpolicy encodings of the expansion's two L2 policies, made on the
+// device once per process (the encoding does not depend on the device).
 void l2_policies(unsigned long long& first, unsigned long long& last) {
+    static std::mutex mu;
+    static bool made = false;
+    static unsigned long long cached[2] = {0, 0};
+    std::lock_guard<std::mutex> lock(mu);
+    if (made) {
+        first = cached[0];
+        last = cached[1];
+        return;
+    }
     unsigned long long* d = nullptr;
     ck(cudaMalloc(&d, 2 * sizeof(unsigned long long)), "cudaMalloc");
     dev::make_l2_policies<<<1, 1>>>(d);
@@ -70,8 +108,9 @@ void l2_policies(unsigned long long& first, unsigned long long& last) {
     const cudaError_t e = cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
     cudaFree(d);
     ck(e, "L2 policies");
-    first = h[0];
-    last = h[1];
+    first = cached[0] = h[0];
+    last = cached[1] = h[1];
+    made = true;
 }
 
 struct Arena {
@@ -309,7 +348,8 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
     ck(cudaEventCreate(&e0), "event");
     ck(cudaEventCreate(&e1), "event");
     std::vector<dev::Ctl> ctl(n_slots);
-    std::vector<std::uint32_t> mb, mc, counts;
+    std::vector<std::uint32_t> counts;
+    HostBuf& mb = host_models_buf();  // pinned, kept by this host thread across calls
     dev::SmemCfg smc{};
     std::size_t smem = 0;
     std::uint32_t per_sm = 1;
@@ -395,11 +435,11 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
         for (std::uint32_t s = 0; s < n_slots; ++s) maxm = std::max(maxm, ctl[s].n_mbuf);
         if (maxm) {
             const std::size_t mrow = static_cast<std::size_t>(maxm) * ar.K.mwords * 4;
-            mb.resize(mrow / 4 * n_slots);
-            mc.resize(static_cast<std::size_t>(maxm) * n_slots);
+            const std::size_t bits_words = mrow / 4 * n_slots;
+            mb.reserve(bits_words + static_cast<std::size_t>(maxm) * n_slots);
             ck(cudaMemcpy2D(mb.data(), mrow, ar.slots[0].mbuf(), ar.L.bytes, mrow, n_slots, cudaMemcpyDeviceToHost),
                "models");
-            ck(cudaMemcpy2D(mc.data(), 4ull * maxm, ar.slots[0].mcube(), ar.L.bytes, 4ull * maxm, n_slots,
+            ck(cudaMemcpy2D(mb.data() + bits_words, 4ull * maxm, ar.slots[0].mcube(), ar.L.bytes, 4ull * maxm, n_slots,
                             cudaMemcpyDeviceToHost),
                "models");
         }
@@ -416,7 +456,7 @@ EngineResult engine_solve(const EngineProgram& prog, const dev::Config& cfg_in, 
                 if (!(cfg.portfolio && s != winner)) counts[s] = ctl[s].n_mbuf;
             EngineDrain dr;
             dr.bits = mb.data();
-            dr.cubes = mc.data();
+            dr.cubes = mb.data() + static_cast<std::size_t>(maxm) * ar.K.mwords * n_slots;
             dr.counts = counts.data();
             dr.n_slots = n_slots;
             dr.stride = maxm;

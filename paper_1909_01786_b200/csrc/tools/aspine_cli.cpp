@@ -105,6 +105,8 @@ int run_solve(int argc, char** argv) {
             trace = true;
         } else if (a == "--cubes") {  // device extension: ladder width for enumeration
             cfg.cube_atoms = number<std::uint32_t>(a, val());
+        } else if (a == "--reference-order") {  // device extension: -n 0 as one search, the reference's model order
+            cfg.reference_order = true;
         } else if (a == "--portfolio") {  // device extension: first-model portfolio of N searches
             cfg.portfolio = number<std::uint32_t>(a, val());
         } else if (a == "--devices") {  // device extension: GPUs of this process, e.g. 0,1,2,3
@@ -186,6 +188,7 @@ int main(int argc, char** argv) {
                          "  aspine solve <file|-> [--mode fwd|res] [--heur occ|jw|act] [--workers N]\n"
                          "        [--restarts off|geometric:B:F] [-n N] [--deps-words W] [--fanout K]\n"
                          "        [--seed S] [--verify] [--stats csv|human] [--trace] [--cubes K] [--portfolio N]\n"
+                         "        [--devices D0,D1,...] [--reference-order]\n"
                          "  aspine oracle <file|->\n";
             return 0;
         }

@@ -57,3 +57,24 @@ def test_enumeration_on_two_devices(files, tmp_path):
     (tmp_path / "q6.lp").write_text(I.queens(6))
     rc, out = run(["solve", str(tmp_path / "q6.lp"), "-n", "0", "--cubes", "6", "--devices", "0,0"])
     assert rc == 10 and out.count("Answer:") == 4
+
+
+@pytest.mark.gpu
+def test_reference_order_flag(tmp_path):
+    """--reference-order: a -n 0 enumeration that would be cube-split runs as one search and prints
+    the models in the reference's order (the API's reference_order=True run); without the flag the
+    same answer sets come in cube order."""
+    import paper_1909_01786_b200 as Y
+    from workloads import instances as I
+    text = I.queens(8)
+    (tmp_path / "q8.lp").write_text(text)
+    want = [" ".join(m.atoms) for m in Y.solve(Y.parse_program(text), Y.SolverConfig(max_models=0, reference_order=True)).models]
+
+    def answers(out):
+        lines = out.splitlines()
+        return [lines[i + 1] for i, ln in enumerate(lines) if ln.startswith("Answer:")]
+
+    rc, out = run(["solve", str(tmp_path / "q8.lp"), "-n", "0", "--reference-order"])
+    assert rc == 10 and answers(out) == want and len(want) == 92
+    rc, out = run(["solve", str(tmp_path / "q8.lp"), "-n", "0"])
+    assert rc == 10 and sorted(answers(out)) == sorted(want)

@@ -856,6 +856,38 @@ struct Search {
         const std::uint32_t F = c->F;
         const std::int32_t* fr = sl.fr(c->cur);
         const bool mirror = sm.tcap() && F + 1 <= sm.fcap();
+        if constexpr (G::kBlock) {
+            if (F <= 32) {  // a decision or a few asserted literals: warp 0 alone, one barrier
+                if (threadIdx.x < 32) {
+                    const std::uint32_t lane = lane_id();
+                    const std::int32_t lit = lane < F ? fr[lane] : 0;
+                    const std::uint32_t v = lane < F ? occ_total(lidx(lit)) : 0u;
+                    std::uint32_t inc = v;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const std::uint32_t o = __shfl_up_sync(0xffffffffu, inc, d);
+                        if (lane >= static_cast<std::uint32_t>(d)) inc += o;
+                    }
+                    const std::uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+                    if (lane < F) {
+                        sl.froff()[lane] = inc - v;
+                        if (mirror) {
+                            sm.froff()[lane] = inc - v;
+                            sm.fr()[lane] = lit;
+                        }
+                    }
+                    if (lane == 0) {
+                        sl.froff()[F] = total;
+                        if (mirror) sm.froff()[F] = total;
+                        c->T = total;
+                        c->b[11] = 0;
+                    }
+                }
+                g.sync();
+                mark(1);
+                return;
+            }
+        }
         unsigned long long carry = 0;
         for (std::uint32_t base = 0; base < F; base += g.size()) {
             const std::uint32_t p = base + g.tid();

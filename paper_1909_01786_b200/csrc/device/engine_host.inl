@@ -553,7 +553,9 @@ struct Session::Impl {
     // arguments, control blocks, read-backs): counted, for end-to-end accounting
     mutable unsigned long long h2d_bytes = 0, d2h_bytes = 0;
 
-    std::size_t append(const void* src, std::size_t ints) {
+    // check: the ints are literals that must name atoms in [1, atoms] (checked
+    // while they are copied; nothing is staged when one does not)
+    std::size_t append(const void* src, std::size_t ints, bool check = false, std::uint32_t atoms = 0) {
         if (stage_inflight) {  // the previous batch's upload may still read the buffer
             ck(cudaEventSynchronize(staged), "staging");
             stage_inflight = false;
@@ -571,7 +573,20 @@ struct Session::Impl {
             h_stage = nb;
             h_stage_cap = ncap;
         }
-        if (ints) std::memcpy(h_stage + off, src, ints * sizeof(std::int32_t));
+        if (check) {
+            const std::int32_t* in = static_cast<const std::int32_t*>(src);
+            std::int32_t* out = h_stage + off;
+            std::uint32_t bad = 0;  // branch-free: the copy-and-check loop vectorises
+            for (std::size_t k = 0; k < ints; ++k) {
+                const std::int32_t l = in[k];
+                const std::uint32_t a = l < 0 ? 0u - static_cast<std::uint32_t>(l) : static_cast<std::uint32_t>(l);
+                bad |= (a - 1u) >= atoms ? 1u : 0u;  // atom 0 or above the range
+                out[k] = l;
+            }
+            if (bad) throw std::invalid_argument("seed: literal out of range");
+        } else if (ints) {
+            std::memcpy(h_stage + off, src, ints * sizeof(std::int32_t));
+        }
         h_used = off + ints;
         // a bulk input starts its upload now, overlapping the caller's next
         // calls; the launch copies only what is left (stream order keeps it
@@ -703,9 +718,10 @@ void flush_ops(Session::Impl& im, float* ms) {
 // Record one op (with optional staged literals / Deps words); a full batch is
 // launched right away.
 void record_op(Session::Impl& im, const dev::OpArgs& op, const std::int32_t* lits = nullptr, std::size_t n = 0,
-               const unsigned long long* deps = nullptr, std::size_t nd = 0) {
+               const unsigned long long* deps = nullptr, std::size_t nd = 0, bool check = false,
+               std::uint32_t atoms = 0) {
     const std::size_t none = ~static_cast<std::size_t>(0);
-    im.lits_off.push_back(lits ? im.append(lits, n) : none);
+    im.lits_off.push_back(lits ? im.append(lits, n, check, atoms) : none);
     im.deps_off.push_back(deps ? im.append(deps, 2 * nd) : none);
     im.pending.push_back(op);
     if (im.pending.size() == dev::kMaxOps) flush_ops(im, nullptr);
@@ -766,17 +782,10 @@ void Session::assign(const std::int32_t* lits_in, std::size_t n_in, std::uint32_
 void Session::seed(const std::int32_t* lits, std::size_t n) {
     const std::uint32_t A = impl_->ar.A;
     if (n > static_cast<std::size_t>(A) + 1) throw std::invalid_argument("seed: more literals than atoms");
-    std::uint32_t bad = 0;  // branch-free so the check over a bulk frontier vectorises
-    for (std::size_t k = 0; k < n; ++k) {
-        const std::int32_t l = lits[k];
-        const std::uint32_t a = l < 0 ? 0u - static_cast<std::uint32_t>(l) : static_cast<std::uint32_t>(l);
-        bad |= (a - 1u) >= A ? 1u : 0u;  // atom 0 or above A
-    }
-    if (bad) throw std::invalid_argument("seed: literal out of range");
     dev::OpArgs op{};
     op.op = dev::kOpSeed;
     op.n = static_cast<std::uint32_t>(n);
-    record_op(*impl_, op, lits, n);
+    record_op(*impl_, op, lits, n, nullptr, 0, true, A);  // the literals are range-checked while staged
 }
 
 void Session::clear_frontier() {

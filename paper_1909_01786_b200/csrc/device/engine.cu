@@ -3018,9 +3018,20 @@ struct Search {
             sl.reason()[a] = kReasonNone;
         }
         const std::uint32_t keys = (2 * S.A + 2) * 4;
-        if (c->learned_n > 0 || c->epoch == 0) {
+        if (c->epoch == 0) {  // a fresh slot: every learned occurrence header
             for (std::uint32_t i = g.tid(); i < 3 * keys; i += g.size()) sl.lhdr()[i] = 0;
             for (std::uint32_t i = g.tid(); i < 2 * S.A + 2; i += g.size()) sl.ltot()[i] = 0;
+        } else if (c->learned_n > 0) {
+            // only literals of learned nogoods (cube units and blocking nogoods
+            // included) have learned occurrences: clear just their headers
+            const std::uint32_t nl = c->lpool_used;
+            for (std::uint32_t i = g.tid(); i < nl; i += g.size()) {
+                const std::uint32_t li = lidx(sl.lpool()[i]);
+                std::uint32_t* h = sl.lhdr() + 3 * (li * 4);
+#pragma unroll
+                for (int k = 0; k < 12; ++k) h[k] = 0;
+                sl.ltot()[li] = 0;
+            }
         }
         std::uint32_t var = C.mode | C.heur << 1;
         if constexpr (!G::kGrid)
